@@ -1,0 +1,336 @@
+"""bench.py — displaced-MPS sampling throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
+
+Workload (default c3 = BASELINE.json configs[2], the single-GPU-resident config the
+metric's "at 1/2/4/8 B200" is quoted on): M=64, chi=1000, D=10, complex128 sites
+(~10 GB, random row-orthonormal, generated on the device from per-site seeds),
+alpha ~ CN(0, 0.5), micro-batch n=1024.  A *step* is one micro-batch of n samples
+through all M modes.  Multi-GPU is sample-sharded (scaling "weak"): every rank holds
+a replica of the MPS and takes its own contiguous sample-index blocks; there is no
+collective on the data path.  Timing: W warm-up steps, then K steps bracketed by
+barrier + synchronize, CUDA events on the launch stream, max over ranks.  The 10 GB
+of sites streamed per step exceed the 126 MB L2, so no explicit flush is needed.
+
+value    — samples/s with inputs (uniforms, alpha) already resident in HBM;
+e2e      — samples/s through the reference-facing call with HOST buffers: pinned
+           uniforms + alpha copied in and counts copied out inside the timed region;
+roofline — the dominant kernel (site_gemm, K1) against the measured FP64 DMMA peak
+           (profiles/fp64_peak.json), timed live with CUDA events on its stream;
+cpu_baseline — the NumPy oracle (all host cores via BLAS) on a bounded sample,
+           extrapolated by per-site flops (rank 0, N=1 only).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # name: (M, chi, D, n, alpha_sigma, N_total, description)
+    "c1": (8, 16, 4, 100, 0.5, 1000, "BASELINE configs[0]: M=8 chi=16 D=4 n=100 alpha~CN(0,0.25)"),
+    "c2": (16, 100, 10, 100, 0.5, 10000, "BASELINE configs[1]: M=16 chi=100 D=10 n=100 alpha~CN(0,0.25)"),
+    "c3": (64, 1000, 10, 1024, 0.5 ** 0.5, 100000, "BASELINE configs[2]: M=64 chi=1000 D=10 n=1024 alpha~CN(0,0.5)"),
+}
+METRIC = "MPS samples/sec (chi,D,M stated) at 1/2/4/8 B200; % of FP64 tensor-core peak"
+
+
+def fp64_peak():
+    p = ROOT / "profiles" / "fp64_peak.json"
+    try:
+        return float(json.loads(p.read_text())["fp64_dmma_tflops"]), "measured (profiles/fp64_peak.json, DMMA loop)"
+    except Exception:
+        return 37.2, "nominal (148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz)"
+
+
+def site_flops(dims, D, n):
+    return [8.0 * n * dims[m] * dims[m + 1] * D + 8.0 * n * dims[m + 1] * D * D for m in range(len(dims) - 1)]
+
+
+# ---------------------------------------------------------------------------------------------
+# CPU leg (oracle; only here and in tests)
+# ---------------------------------------------------------------------------------------------
+
+
+def cpu_sample_rate(cfg_name, target_s=15.0):
+    """Time the NumPy oracle (batched BLAS ZGEMM chain, all host cores) on a bounded sample:
+    n_cpu samples through a block of S consecutive full-chi sites; extrapolate to all M sites
+    by algorithmic flops.  Returns (samples/s, cores, sample description)."""
+    from oracle import mps_oracle as orc
+
+    M, chi, D, n, sigma, _, _ = CONFIGS[cfg_name]
+    dims = orc.bond_dims(M, chi, D)
+    try:
+        from threadpoolctl import threadpool_info
+
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] or [os.cpu_count() or 1])
+    except Exception:
+        cores = os.cpu_count() or 1
+    if M * chi * chi * D * 16 <= 2e9:
+        # whole chain fits: run it in full
+        sites = orc.random_mps(M, chi, D, seed=0)
+        n_cpu = n
+        u = orc.stream_uniforms(0, 0, n_cpu, M)
+        al = orc.alpha_stream(0, 0, n_cpu, M, sigma)
+        reps, t = 0, 0.0
+        while t < target_s and reps < 100:
+            t0 = time.perf_counter()
+            orc.sample_chain(sites, u, alpha=al)
+            t += time.perf_counter() - t0
+            reps += 1
+        return reps * n_cpu / t, cores, f"full chain, {reps} x {n_cpu} samples through all {M} sites"
+    mid = M // 2
+    S = 2
+    block = list(range(mid - S // 2, mid - S // 2 + S))
+    sites = [orc.random_site(0, m, dims[m], dims[m + 1], D) for m in block]
+    n_cpu = 256
+    u = orc.stream_uniforms(0, 0, n_cpu, S)
+    al = orc.alpha_stream(0, 0, n_cpu, S, sigma)
+    rng = np.random.default_rng(0)
+    v0 = rng.standard_normal((n_cpu, dims[block[0]])) + 1j * rng.standard_normal((n_cpu, dims[block[0]]))
+    v0 /= np.linalg.norm(v0, axis=1, keepdims=True)
+    reps, t = 0, 0.0
+    while t < target_s and reps < 50:
+        t0 = time.perf_counter()
+        v = v0
+        for j, G in enumerate(sites):  # the oracle's per-mode step (sample_chain body)
+            chl, chr_, _ = G.shape
+            C = (v @ G.reshape(chl, chr_ * D)).reshape(n_cpu, chr_, D)
+            E = np.einsum("bjd,bkd->bjk", C, orc.displacement_matrix(al[:, j], D))
+            p = (E.real * E.real + E.imag * E.imag).sum(axis=1)
+            k, ok, _ = orc.draw(p, u[:, j])
+            v = E[np.arange(n_cpu), :, k] / np.sqrt(p[np.arange(n_cpu), k])[:, None]
+        t += time.perf_counter() - t0
+        reps += 1
+    fl = site_flops(dims, D, n_cpu)
+    t_block = t / reps
+    t_all = t_block * sum(fl) / sum(fl[m] for m in block)
+    return (n_cpu / t_all, cores,
+            f"{reps} reps of {n_cpu} samples through sites {block[0]}..{block[-1]} (chi={chi}); "
+            f"per-sample time extrapolated to all {M} sites by algorithmic flops")
+
+
+# ---------------------------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------------------------
+
+
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = Path(f"/tmp/mps_bench_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        rows = [r.split(",") for r in self.path.read_text().strip().splitlines() if r.strip()]
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows if len(r) >= 9 for i in range(4) if "Active" in r[5 + i]
+                          and "Not" not in r[5 + i]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------------------------
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    W = max(args.warmup, 3)
+    K = args.steps
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    M, chi, D, n, sigma, N_total, desc = CONFIGS[args.config]
+    from paper_2511_14923_b200.mps import bond_dims
+
+    dims = bond_dims(M, chi, D)
+    config = {"workload": f"{args.config}: {desc}", "M": M, "chi": chi, "D": D, "n": n,
+              "alpha": "CN(0,%.3g)" % (sigma * sigma), "sites": "random row-orthonormal, seed 0",
+              "layout": "sample-sharded" if world > 1 else "single GPU",
+              "l2": "inputs larger than L2 (sites %.2f GB streamed per step)" % (
+                  sum(a * b for a, b in zip(dims[:-1], dims[1:])) * D * 16 / 1e9)}
+
+    if args.impl == "reference":
+        # The reference ships no MPS sampler; its arm is the CPU oracle
+        # restating PAPER.md:58-66 on the host cores, rank 0 only.
+        if rank != 0:
+            return
+        steps = []
+        for i in range(W + K):
+            v, cores, sample = cpu_sample_rate(args.config, target_s=max(1.0, 60.0 / (W + K)))
+            if i >= W:
+                steps.append(v)
+        v = float(np.median(steps))
+        line = {"metric": METRIC, "value": v, "unit": "samples/s", "impl": "reference", "n_gpus": 0, "steps": K,
+                "warmup": W, "ms_per_step": 1000.0 * n / v, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "c128", "data": "synthetic", "config": config,
+                "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cores, "kind": "port", "sample": sample},
+                "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2511_14923_b200 import MPS, MpsSampler, alpha_stream, stream_uniforms
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    t_setup = time.perf_counter()
+    mps = MPS.random(M, chi, D, seed=0, device=dev) if M * chi * chi * D * 16 > 2e8 else MPS.random(M, chi, D, 0)
+    eng = MpsSampler(mps, device=local)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t_setup
+    stream = torch.cuda.Stream(dev)  # explicit stream: events and kernels share it
+    torch.cuda.set_stream(stream)
+
+    def block_index(step):  # global first sample index of this rank's micro-batch
+        return (step * world + rank) * n
+
+    # resident inputs: uniforms + alpha for every step, in HBM before timing
+    nsteps = W + K
+    u_dev = [torch.from_numpy(stream_uniforms(0, block_index(s), n, M)).to(dev) for s in range(nsteps)]
+    a_dev = [torch.from_numpy(alpha_stream(0, block_index(s), n, M, sigma)).to(dev) for s in range(nsteps)]
+    counts = torch.empty((nsteps, n, M), dtype=torch.int32, device=dev)
+    status = torch.zeros((nsteps, n), dtype=torch.uint8, device=dev)
+
+    def step(s):
+        eng.run(block_index(s), n, counts[s], uniforms=u_dev[s], alpha=a_dev[s], status=status[s],
+                stream=stream.cuda_stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    for s in range(W):
+        step(s)
+    barrier()
+    clocks = Clocks(local)
+    clocks.start()
+    eng.profile(True)
+    l0 = eng.kernel_launches
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(stream)
+    for s in range(W, W + K):
+        step(s)
+    e1.record(stream)
+    barrier()
+    launches = eng.kernel_launches - l0
+    prof = eng.profile_read()
+    eng.profile(False)
+    ck = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * K * n / (ms / 1e3)
+
+    # e2e: host (pinned) uniforms + alpha in, counts out, through the same C ABI call
+    u_host = [torch.from_numpy(stream_uniforms(0, block_index(s), n, M)).pin_memory() for s in range(nsteps)]
+    a_host = [torch.from_numpy(alpha_stream(0, block_index(s), n, M, sigma)).pin_memory() for s in range(nsteps)]
+    c_host = torch.empty((n, M), dtype=torch.int32).pin_memory()
+    st_host = torch.zeros(n, dtype=torch.uint8).pin_memory()
+
+    def step_e2e(s):
+        st_host.zero_()
+        eng.run(block_index(s), n, c_host.numpy(), uniforms=u_host[s].numpy(), alpha=a_host[s].numpy(),
+                status=st_host.numpy(), stream=stream.cuda_stream)
+
+    for s in range(W):
+        step_e2e(s)
+    barrier()
+    e2 = torch.cuda.Event(enable_timing=True)
+    e3 = torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    for s in range(W, W + K):
+        step_e2e(s)
+    e3.record(stream)
+    barrier()
+    ms_e2e = e2.elapsed_time(e3)
+    if world > 1:
+        t = torch.tensor([ms_e2e], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+    e2e = world * K * n / (ms_e2e / 1e3)
+
+    ok = bool((counts[W:] >= 0).all().item()) and not bool((status[W:] & 1).any().item())
+    peak, peak_src = fp64_peak()
+    gemm_ms_avg = prof["gemm_ms"] / max(prof["gemm_launches"], 1)
+    gemm_flops_avg = prof["gemm_flops"] / max(prof["gemm_launches"], 1)
+    achieved = gemm_flops_avg / (gemm_ms_avg / 1e3) / 1e12 if gemm_ms_avg > 0 else 0.0
+    step_flops = sum(site_flops(dims, D, n))
+    whole_tf = world * K * step_flops / (ms / 1e3) / 1e12
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+        "data": "synthetic (random row-orthonormal sites from seeds, counter-stream uniforms and alpha)",
+        "config": config,
+        "e2e": {"value": e2e, "unit": "samples/s", "h2d_bytes_per_step": n * M * (8 + 16) + n,
+                "d2h_bytes_per_step": n * M * 4 + n},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": None, "kernel": "site_gemm_kernel (K1, FP64 DMMA)",
+                     "peak_source": peak_src,
+                     "per_launch": {"ms": gemm_ms_avg, "algorithmic_flops": gemm_flops_avg},
+                     "share_of_step": prof["gemm_ms"] / ms if ms > 0 else None,
+                     "whole_chain_tflops": whole_tf, "whole_chain_frac": whole_tf / (world * peak),
+                     "displace_draw": {"ms_per_launch": prof["draw_ms"] / max(prof["draw_launches"], 1),
+                                       "achieved_gbs": (prof["draw_bytes"] / (prof["draw_ms"] / 1e3) / 1e9)
+                                       if prof["draw_ms"] > 0 else None}},
+        "clocks": ck,
+        "valid_outputs": ok,
+        "setup_s": setup_s,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, cores, sample = cpu_sample_rate(args.config)
+        line["cpu_baseline"] = {"value": v, "unit": "samples/s", "cores": cores, "kind": "port", "sample": sample}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

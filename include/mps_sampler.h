@@ -1,0 +1,159 @@
+/*
+ * mps_sampler.h — C ABI of the B200-native displaced-MPS sampler.
+ *
+ * This is the drop-in boundary for the hot path named by BASELINE.json
+ * north_star: the per-mode chain  temp(n x chi) . Gamma(chi x chi D)  ->
+ * displacement einsum -> |amplitude|^2 marginal -> inverse-CDF draw ->
+ * gather + renormalise.
+ *
+ * The reference (gbsemu) exposes its samplers through method dispatch in
+ * batch_sample(config, ...) (pkg/src/gbsemu/sampler.py:706-723) with a frozen
+ * validated config (sampler.py:51-79) and a SampleBatch result
+ * (sampler.py:82-95).  It has no native layer; this library is what a new
+ * method "mps" in that dispatch binds through ctypes (INTEGRATION.md shows
+ * the stub).  Entry points and the reference interface each replaces:
+ *
+ *   mps_create / mps_destroy  — per-process engine state; replaces the
+ *       per-worker initializer _pool_init (sampler.py:658-663): one context
+ *       per GPU, one process per GPU.
+ *   mps_set_site              — loads Gamma^[m]; replaces "load the stored
+ *       MPS from disk" / the read-only table hand-off to
+ *       workers (sampler.py:661-663).
+ *   mps_set_streams           — seeds the counter-based streams; replaces
+ *       SamplerConfig.seed + _stream_uniforms (sampler.py:109-125).
+ *   mps_sample                — N-sample batch; replaces _chunk_chain
+ *       (sampler.py:628-655) for method "mps".
+ *   mps_sample_range          — one pipeline stage (modes [m_begin, m_end)),
+ *       state in/out on the device; the mode-pipelined layout.
+ *   mps_last_error            — message for the last non-zero status.
+ *
+ * Status codes mirror gbsemu/errors.py:8-29 (and the CLI exit codes):
+ *   0 ok, 1 generic GbsError (CUDA runtime failure), 2 ValidationError,
+ *   3 ResourceGuardError (out of memory / budget), 4 NumericalError.
+ *
+ * Conventions:
+ *   * Gamma^[m] is chi_l x chi_r x D complex, C order (d fastest), so its
+ *     reshape(chi_l, chi_r*D) is free.
+ *   * disp[b][m] is D x D complex indexed [out k][in d];
+ *     E[j][k] = sum_d C[j][d] disp[k][d].
+ *   * complex numbers are interleaved (re, im) float64 pairs (complex128).
+ *   * counts are int32, N x M row-major; uniforms are float64 N x M.
+ *   * Any array argument may be a host or a device pointer (detected with
+ *     cudaPointerGetAttributes).  When every output is a device pointer the
+ *     call is asynchronous on `stream`; otherwise it returns after the
+ *     results are on the host.
+ *   * The caller owns every buffer; the library borrows pointers for the
+ *     call only (sites: see MPS_SITE_*).
+ *   * Calls on one context are serialised by the caller; distinct contexts
+ *     are independent.  ctypes releases the GIL around every call.
+ */
+#ifndef MPS_SAMPLER_H
+#define MPS_SAMPLER_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MPS_OK 0
+#define MPS_ERR_GENERIC 1
+#define MPS_ERR_VALIDATION 2
+#define MPS_ERR_RESOURCE 3
+#define MPS_ERR_NUMERICAL 4
+
+/* mps_set_site flags */
+#define MPS_SITE_HOST 0          /* gamma is host memory: copied into context-owned HBM */
+#define MPS_SITE_DEVICE_COPY 1   /* gamma is device memory: copied */
+#define MPS_SITE_DEVICE_BORROW 2 /* gamma is device memory: borrowed, caller keeps it alive */
+
+/* dtype */
+#define MPS_C128 0
+
+/* per-sample status bits written to `status` */
+#define MPS_STATUS_FAILED 1      /* step norm sum_k p(k) not finite / not positive */
+#define MPS_STATUS_FLAGGED 2     /* some draw had |cdf[k] - u| <= 1e-10 */
+
+typedef struct mps_ctx mps_ctx;
+
+/* Create a context on one device.  n_dev must be 1 (one process per GPU; the
+ * multi-GPU layouts run one context per rank).  layout: 0 sample-sharded,
+ * 1 mode-pipelined (informational: a stage simply holds a subset of sites). */
+int mps_create(int n_dev, const int* dev_ids, int layout, mps_ctx** out);
+
+/* Declare the chain: M sites of physical dimension D.  Must precede set_site. */
+int mps_configure(mps_ctx* ctx, int M, int D);
+
+/* Load site m (chi_l x chi_r x D complex128).  chi_l must equal the chi_r of
+ * site m-1 when that site is loaded; chi_0 = chi_M = 1 is not enforced so
+ * a stage may start mid-chain. */
+int mps_set_site(mps_ctx* ctx, int m, int chi_l, int chi_r, int D,
+                 const void* gamma, int flags, int dtype);
+
+/* Seed the on-device counter streams (used when uniforms / alpha are NULL):
+ * uniforms of sample i are _stream_uniforms(seed, i, M) bit-for-bit
+ * (sampler.py:109-125); alpha_sigma >= 0 enables on-device alpha ~ CN(0, sigma^2)
+ * from the alpha stream (oracle decision 7); alpha_sigma < 0 disables it. */
+int mps_set_streams(mps_ctx* ctx, uint64_t seed, double alpha_sigma);
+
+/* Sample n paths (global sample indices first_index .. first_index+n-1)
+ * through all M sites.  uniforms: n x M or NULL (device stream); disp:
+ * n x M x D x D complex or NULL; alpha: n x M complex or NULL (if both are
+ * NULL the on-device alpha stream is used when enabled, else no displacement).
+ * counts: n x M int32 out (failed samples: row of -1); marginals: n x M x D
+ * normalised float64 out or NULL; n_flagged: out, may be NULL. */
+int mps_sample(mps_ctx* ctx, int64_t first_index, int n,
+               const double* uniforms, const void* disp, const void* alpha,
+               int32_t* counts, double* marginals, uint64_t* n_flagged);
+
+/* One stage: modes [m_begin, m_end) for n samples.  Arrays are full-width
+ * (column = absolute mode index) with row strides ld_u / ld_c (elements);
+ * marginals use row stride ld_c * D.  state_in: device n x chi_{m_begin}
+ * complex or NULL (= ones, only valid when chi_{m_begin} == 1); state_out:
+ * device n x chi_{m_end} complex or NULL.  status: n bytes in/out (bits
+ * MPS_STATUS_*), may be NULL.  stream: the cudaStream_t to run on (0 = the
+ * legacy default stream); mps_sample runs on the context's own stream. */
+int mps_sample_range(mps_ctx* ctx, int m_begin, int m_end, int64_t first_index, int n,
+                     const double* uniforms, int64_t ld_u,
+                     const void* disp, const void* alpha,
+                     const void* state_in, void* state_out,
+                     int32_t* counts, int64_t ld_c, double* marginals,
+                     uint8_t* status, uint64_t stream);
+
+/* Device launches issued by this context since creation (kernels only). */
+uint64_t mps_kernel_launches(const mps_ctx* ctx);
+
+/* Live per-kernel timing: when enabled, every K1/K2+K3 launch is bracketed by
+ * CUDA events on its own stream.  mps_profile_read synchronises on them and
+ * returns (and resets) out6 = {site_gemm ms, launches, algorithmic flops,
+ * displace_draw ms, launches, algorithmic bytes}. */
+int mps_profile(mps_ctx* ctx, int enable);
+int mps_profile_read(mps_ctx* ctx, double* out6);
+
+const char* mps_last_error(const mps_ctx* ctx);
+void mps_destroy(mps_ctx* ctx);
+
+/* Kernel-level entry points, exposed for unit tests and the bench roofline.
+ * All pointers are device pointers; stream 0 = legacy default stream. */
+
+/* C (n x N complex, row stride ldc) = V (n x K complex, row stride K) . G (K x N complex) */
+int mps_site_gemm(const void* V, const void* G, void* C, int n, int K, int N,
+                  int64_t ldc, uint64_t stream);
+/* Same with an explicit K1 tile config (-1 auto, 0 128x128, 1 64x128 8 warps,
+ * 2 64x128 4 warps x 2 CTAs/SM, 3 32x64); every config gives bit-identical C. */
+int mps_site_gemm_cfg(const void* V, const void* G, void* C, int n, int K, int N,
+                      int64_t ldc, uint64_t stream, int cfg);
+/* Pin the K1 tile config of a context (-1 = auto). */
+int mps_set_gemm_config(mps_ctx* ctx, int cfg);
+/* D x D truncated displacement matrices for `count` alphas: out[count][D][D] */
+int mps_displacement(const void* alpha, int count, int D, void* out, uint64_t stream);
+/* Uniforms of samples first..first+count-1 (count x M float64), bit-equal to
+ * numpy Philox / _stream_uniforms. */
+int mps_stream_uniforms(uint64_t seed, int64_t first, int count, int M, double* out,
+                        uint64_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MPS_SAMPLER_H */

@@ -1,0 +1,314 @@
+// displace_draw.cuh — K2+K3 for one mode: displacement einsum, |amplitude|^2 marginal,
+// inverse-CDF draw, gather + renormalise, plus the
+// counter-based streams (row a10) and D(alpha) construction (row a2).
+//
+// One CTA per sample b.  Pass 1 streams C[b] (chi_r x D complex, written by K1),
+// forms E[j][k] = sum_d Disp[k][d] C[j][d] in registers and
+// accumulates p[k] = sum_j |E[j][k]|^2 in a fixed order (thread-strided partials ->
+// xor-shuffle tree -> warps summed in index order), so p is bit-identical for any
+// batch size / grid.  Thread 0 draws k against u[b][m] with the sampler.py:692-697
+// rule.  Pass 2 re-reads C[b] and writes v'[j] = E[j][k] / sqrt(p[k]) — the
+// recomputation costs D MACs per j and saves storing E (16 n chi D bytes).
+#pragma once
+#include <cstdint>
+
+namespace mps {
+
+constexpr int DMAX = 16;
+constexpr int DRAW_THREADS = 256;
+constexpr double TIE_EPS = 1e-10;
+constexpr uint8_t ST_FAILED = 1;
+constexpr uint8_t ST_FLAGGED = 2;
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+// ---------------------------------------------------------------------------
+// numpy-compatible Philox4x64-10 (Random123 constants); numpy increments the
+// 256-bit counter before each block, so output word q of key (k0, k1) is
+// philox(ctr = q/4 + 1)[q % 4]; Generator.random() = (x >> 11) * 2^-53.
+// ---------------------------------------------------------------------------
+__host__ __device__ inline void philox4x64_10(uint64_t ctr[4], uint64_t k0, uint64_t k1) {
+  const uint64_t M0 = 0xD2E7470EE14C6C93ull, M1 = 0xCA5A826395121157ull;
+  const uint64_t W0 = 0x9E3779B97F4A7C15ull, W1 = 0xBB67AE8584CAA73Bull;
+  for (int r = 0; r < 10; ++r) {
+#ifdef __CUDA_ARCH__
+    uint64_t hi0 = __umul64hi(M0, ctr[0]), lo0 = M0 * ctr[0];
+    uint64_t hi1 = __umul64hi(M1, ctr[2]), lo1 = M1 * ctr[2];
+#else
+    unsigned __int128 p0 = (unsigned __int128)M0 * ctr[0], p1 = (unsigned __int128)M1 * ctr[2];
+    uint64_t hi0 = (uint64_t)(p0 >> 64), lo0 = (uint64_t)p0, hi1 = (uint64_t)(p1 >> 64), lo1 = (uint64_t)p1;
+#endif
+    uint64_t c0 = hi1 ^ ctr[1] ^ k0, c2 = hi0 ^ ctr[3] ^ k1;
+    ctr[0] = c0; ctr[1] = lo1; ctr[2] = c2; ctr[3] = lo0;
+    k0 += W0; k1 += W1;
+  }
+}
+
+// numpy turns the key list [seed, blk] into an array first; a seed >= 2^63 does not fit
+// int64, so the list is converted through float64 (seed rounded to 53 bits, >= 2^64 -> 0).
+// _stream_uniforms inherits that, and so do we, bit-for-bit.
+__host__ __device__ inline uint64_t numpy_key0(uint64_t seed) {
+  if (seed < (1ull << 63)) return seed;
+  const double f = (double)seed;
+  return f >= 18446744073709551616.0 ? 0ull : (uint64_t)f;
+}
+
+// The q-th double of numpy Generator(Philox(key=[k0, k1])).random(...)
+__host__ __device__ inline double philox_double(uint64_t k0, uint64_t k1, uint64_t q) {
+  uint64_t ctr[4] = {q / 4 + 1, 0, 0, 0};
+  if (ctr[0] == 0) ctr[1] = 1;  // carry (unreachable for realistic q)
+  philox4x64_10(ctr, k0, k1);
+  return (double)(ctr[q & 3] >> 11) * (1.0 / 9007199254740992.0);
+}
+
+// uniforms of samples first..first+count-1, mode m: row i%64, column m of block i/64
+__global__ void stream_uniforms_kernel(uint64_t seed, long long first, int count, int M, double* out,
+                                       long long ld) {
+  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)count * M) return;
+  long long b = idx / M;
+  int m = (int)(idx % M);
+  unsigned long long i = (unsigned long long)(first + b);
+  uint64_t q = (i % 64) * (uint64_t)M + m;
+  out[b * ld + m] = philox_double(numpy_key0(seed), i / 64, q);
+}
+
+// alpha ~ CN(0, sigma^2) from the key (seed, 2^62 + i/64), 2M uniforms per sample row
+__device__ inline double2 stream_alpha(uint64_t seed, unsigned long long i, int M, int m, double sigma) {
+  const uint64_t blk = (1ull << 62) + i / 64;
+  uint64_t q = (i % 64) * (uint64_t)(2 * M) + 2 * m;
+  double u1 = philox_double(seed, blk, q), u2 = philox_double(seed, blk, q + 1);
+  double rad = sigma * sqrt(-log1p(-u1));
+  double ph = 2.0 * 3.141592653589793 * u2;
+  double sn, cs;
+  sincos(ph, &sn, &cs);
+  return make_double2(rad * cs, rad * sn);
+}
+
+// Exact truncated <k|D(alpha)|d> (oracle decision 6), row-major T[k*D + d].  The
+// operation order mirrors the oracle's numpy expressions with explicit _rn
+// intrinsics (no FMA contraction), so host and device agree to the last bit except
+// where exp() differs by an ulp.
+__device__ __forceinline__ double2 cmul_rn(double2 a, double2 b) {  // numpy complex multiply
+  return make_double2(__dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)),
+                      __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x)));
+}
+
+__device__ inline void displacement_column0(double2 a, int D, double2* T) {
+  // T[0,0] = exp(-0.5 |a|^2); T[k,0] = T[k-1,0] * a / sqrt(k)  (numpy's complex / real
+  // division multiplies by the reciprocal: Smith's algorithm with a zero imaginary part)
+  const double e = exp(__dmul_rn(-0.5, __dadd_rn(__dmul_rn(a.x, a.x), __dmul_rn(a.y, a.y))));
+  T[0] = make_double2(e, 0.0);
+  for (int k = 1; k < D; ++k) {
+    const double2 v = cmul_rn(T[(k - 1) * D], a);
+    const double scl = __ddiv_rn(1.0, sqrt((double)k));
+    T[k * D] = make_double2(__dmul_rn(v.x, scl), __dmul_rn(v.y, scl));
+  }
+}
+
+__device__ inline double2 displacement_entry(double2 a, int D, const double2* T, int k, int d) {
+  // T[k,d] = (sqrt(k) T[k-1,d-1] - conj(a) T[k,d-1]) * (1/sqrt(d));  row 0: (-conj(a) T[0,d-1]) * inv
+  const double inv = __ddiv_rn(1.0, sqrt((double)d));
+  const double2 t2 = cmul_rn(make_double2(a.x, -a.y), T[k * D + d - 1]);
+  if (k == 0) return make_double2(__dmul_rn(-t2.x, inv), __dmul_rn(-t2.y, inv));
+  const double sk = sqrt((double)k);
+  const double2 t1 = T[(k - 1) * D + d - 1];
+  return make_double2(__dmul_rn(__dsub_rn(__dmul_rn(sk, t1.x), t2.x), inv),
+                      __dmul_rn(__dsub_rn(__dmul_rn(sk, t1.y), t2.y), inv));
+}
+
+__global__ void displacement_kernel(const double2* __restrict__ alpha, int count, int D, double2* __restrict__ out) {
+  int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= count) return;
+  double2 a = alpha[idx];
+  double2* T = out + (long long)idx * D * D;
+  displacement_column0(a, D, T);
+  for (int d = 1; d < D; ++d)
+    for (int k = 0; k < D; ++k) T[k * D + d] = displacement_entry(a, D, T, k, d);
+}
+
+struct DrawArgs {
+  const double2* C;         // n x (chi_r*D)
+  long long ldc;            // complex elements per C row
+  int chi_r, D, m, M;
+  long long first_index;
+  const double* u;          // uniforms (n x ld_u) or null -> device stream
+  long long ld_u;
+  uint64_t seed;
+  const double2* disp;      // n x M x D x D or null
+  const double2* alpha;     // n x M or null
+  double alpha_sigma;       // >= 0: device alpha stream when disp & alpha are null
+  double2* v_out;           // n x chi_r
+  int32_t* counts;          // n x ld_c
+  long long ld_c;
+  double* marg;             // n x ld_c x D or null
+  uint8_t* status;          // n
+};
+
+__global__ void __launch_bounds__(DRAW_THREADS)
+    displace_draw_kernel(DrawArgs A) {
+  __shared__ double2 T[DMAX * DMAX];
+  __shared__ double red[DRAW_THREADS / 32][DMAX];
+  __shared__ double p_s[DMAX];
+  __shared__ int k_s;
+  __shared__ double scale_s;
+  __shared__ int mode_s;  // 0 identity, 1 matrix
+
+  const int b = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int D = A.D;
+  const unsigned long long gi = (unsigned long long)(A.first_index + b);
+
+  const bool dead = (A.status[b] & ST_FAILED) != 0;
+  if (dead) {  // keep the chain deterministic: zero state, count -1
+    for (int j = tid; j < A.chi_r; j += DRAW_THREADS) A.v_out[(long long)b * A.chi_r + j] = make_double2(0.0, 0.0);
+    if (tid == 0) A.counts[(long long)b * A.ld_c + A.m] = -1;
+    if (A.marg && tid < D) A.marg[((long long)b * A.ld_c + A.m) * D + tid] = 0.0;
+    return;
+  }
+
+  // ---- displacement matrix for (b, m) ----
+  if (A.disp) {
+    const double2* src = A.disp + ((long long)b * A.M + A.m) * D * D;
+    for (int e = tid; e < D * D; e += DRAW_THREADS) T[e] = src[e];
+    if (tid == 0) mode_s = 1;
+  } else if (A.alpha || A.alpha_sigma >= 0.0) {
+    double2 a;
+    if (A.alpha) a = A.alpha[(long long)b * A.M + A.m];
+    else a = stream_alpha(A.seed, gi, A.M, A.m, A.alpha_sigma);
+    if (tid == 0) { displacement_column0(a, D, T); mode_s = 1; }
+    __syncthreads();
+    for (int d = 1; d < D; ++d) {
+      double2 v;
+      if (tid < D) v = displacement_entry(a, D, T, tid, d);
+      __syncthreads();
+      if (tid < D) T[tid * D + d] = v;
+      __syncthreads();
+    }
+  } else {
+    if (tid == 0) mode_s = 0;
+  }
+  __syncthreads();
+  const bool ident = (mode_s == 0);
+
+  // ---- pass 1: partial marginals ----
+  double acc[DMAX];
+#pragma unroll
+  for (int k = 0; k < DMAX; ++k) acc[k] = 0.0;
+  const double2* Cb = A.C + (long long)b * A.ldc;
+  for (int j = tid; j < A.chi_r; j += DRAW_THREADS) {
+    double2 c[DMAX];
+#pragma unroll
+    for (int d = 0; d < DMAX; ++d)
+      if (d < D) c[d] = Cb[(long long)j * D + d];
+#pragma unroll
+    for (int k = 0; k < DMAX; ++k) {
+      if (k >= D) break;
+      double2 e;
+      if (ident) {
+        e = c[k];
+      } else {
+        e = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int d = 0; d < DMAX; ++d) {
+          if (d >= D) break;
+          double2 tk = T[k * D + d];
+          e.x = fma(tk.x, c[d].x, e.x);
+          e.x = fma(-tk.y, c[d].y, e.x);
+          e.y = fma(tk.x, c[d].y, e.y);
+          e.y = fma(tk.y, c[d].x, e.y);
+        }
+      }
+      acc[k] = fma(e.x, e.x, fma(e.y, e.y, acc[k]));
+    }
+  }
+  const int lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+  for (int k = 0; k < DMAX; ++k) {
+    if (k >= D) break;
+    double v = acc[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp][k] = v;
+  }
+  __syncthreads();
+
+  // ---- draw (sampler.py:692-697 rule on the normalised cdf) ----
+  if (tid == 0) {
+    double p[DMAX];
+    double P = 0.0;
+    for (int k = 0; k < D; ++k) {
+      double s = 0.0;
+      for (int w = 0; w < DRAW_THREADS / 32; ++w) s += red[w][k];
+      p[k] = s;
+      p_s[k] = s;
+      P += s;
+    }
+    uint8_t st = A.status[b];
+    int ksel = 0;
+    if (!(P > 0.0) || !isfinite(P)) {
+      st |= ST_FAILED;
+      ksel = -1;
+    } else {
+      const double u = A.u ? A.u[(long long)b * A.ld_u + A.m]
+                           : philox_double(numpy_key0(A.seed), gi / 64, (gi % 64) * (uint64_t)A.M + A.m);
+      double run = 0.0;
+      int cnt = 0;
+      double mind = 1e300;
+      for (int k = 0; k < D; ++k) {
+        run += p[k];
+        double cdf = (k == D - 1) ? 1.0 : run / P;
+        if (cdf <= u) ++cnt;
+        if (k < D - 1) mind = fmin(mind, fabs(cdf - u));
+      }
+      ksel = cnt < D - 1 ? cnt : D - 1;
+      while (ksel > 0 && !(p[ksel] > 0.0)) --ksel;
+      if (mind <= TIE_EPS) st |= ST_FLAGGED;
+      if (A.marg)
+        for (int k = 0; k < D; ++k) A.marg[((long long)b * A.ld_c + A.m) * D + k] = p[k] / P;
+    }
+    A.status[b] = st;
+    A.counts[(long long)b * A.ld_c + A.m] = ksel;
+    k_s = ksel;
+    scale_s = (ksel >= 0) ? 1.0 / sqrt(p[ksel]) : 0.0;
+  }
+  __syncthreads();
+  const int ks = k_s;
+  const double scale = scale_s;
+
+  // ---- pass 2: gather + renormalise ----
+  double2* vb = A.v_out + (long long)b * A.chi_r;
+  if (ks < 0) {
+    if (A.marg && tid < D) A.marg[((long long)b * A.ld_c + A.m) * D + tid] = 0.0;
+    for (int j = tid; j < A.chi_r; j += DRAW_THREADS) vb[j] = make_double2(0.0, 0.0);
+    return;
+  }
+  for (int j = tid; j < A.chi_r; j += DRAW_THREADS) {
+    double2 e;
+    if (ident) {
+      e = Cb[(long long)j * D + ks];
+    } else {
+      e = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int d = 0; d < DMAX; ++d) {
+        if (d >= D) break;
+        double2 c = Cb[(long long)j * D + d];
+        double2 tk = T[ks * D + d];
+        e.x = fma(tk.x, c.x, e.x);
+        e.x = fma(-tk.y, c.y, e.x);
+        e.y = fma(tk.x, c.y, e.y);
+        e.y = fma(tk.y, c.x, e.y);
+      }
+    }
+    vb[j] = make_double2(e.x * scale, e.y * scale);
+  }
+}
+
+__global__ void fill_ones_kernel(double2* v, int n) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = make_double2(1.0, 0.0);
+}
+
+}  // namespace mps

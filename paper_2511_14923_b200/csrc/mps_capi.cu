@@ -1,0 +1,588 @@
+// mps_capi.cu — the C ABI (include/mps_sampler.h) over the sm_100a kernels.
+//
+// One context per GPU per process.  A context owns: the resident site tensors
+// Gamma^[m] (or borrowed device pointers), their TMA descriptors, the per-batch
+// workspaces (state ping-pong, C buffer, staged inputs/outputs) and a stream.
+// Per mode it launches K1 (site_gemm_kernel) then K2+K3 (displace_draw_kernel);
+// there is no host synchronisation inside the mode loop.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/mps_sampler.h"
+#include "displace_draw.cuh"
+#include "site_gemm.cuh"
+
+using namespace mps;
+
+namespace {
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 2-D row-major float64 matrix (rows x cols doubles, row pitch in bytes), box {16, box_rows}, 128B swizzle.
+bool make_tmap(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t pitch_bytes,
+               uint32_t box_rows) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {pitch_bytes};
+  cuuint32_t box[2] = {16, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+struct Site {
+  int chi_l = 0, chi_r = 0;
+  double2* data = nullptr;
+  bool owned = false;
+  CUtensorMap tmap;
+};
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t cap = 0;  // elements
+  cudaError_t ensure(size_t n) {
+    if (n <= cap) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    cudaError_t e = cudaMalloc(&p, n * sizeof(T));
+    if (e == cudaSuccess) cap = n;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+
+}  // namespace
+
+struct mps_ctx {
+  int device = 0;
+  int layout = 0;
+  int M = 0, D = 0;
+  std::vector<Site> sites;
+  cudaStream_t stream = nullptr;
+  uint64_t seed = 0;
+  double alpha_sigma = -1.0;
+  int gemm_cfg = -1;  // -1: auto (choose_gemm_cfg)
+  uint64_t launches = 0;
+  std::string err;
+  // workspaces
+  DevBuf<double2> v0, v1, cbuf, ones, alpha_d, disp_d;
+  DevBuf<double> u_d, marg_d;
+  DevBuf<int32_t> counts_d;
+  DevBuf<uint8_t> status_d;
+  // live kernel timing (mps_profile): event pairs bracketing each launch on its stream
+  bool profile = false;
+  struct Rec {
+    int kind;  // 0 site_gemm, 1 displace_draw
+    cudaEvent_t a, b;
+    double work;  // algorithmic flops (gemm) or bytes (draw)
+  };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> event_pool;
+  cudaEvent_t get_event() {
+    if (!event_pool.empty()) {
+      cudaEvent_t e = event_pool.back();
+      event_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+
+static int fail(mps_ctx* c, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return code;
+}
+
+static int cuda_fail(mps_ctx* c, cudaError_t e, const char* what) {
+  cudaGetLastError();
+  int code = (e == cudaErrorMemoryAllocation) ? MPS_ERR_RESOURCE : MPS_ERR_GENERIC;
+  return fail(c, code, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define CU(c, x, what)                          \
+  do {                                          \
+    cudaError_t e_ = (x);                       \
+    if (e_ != cudaSuccess) return cuda_fail(c, e_, what); \
+  } while (0)
+
+// K1 tile configurations.  All share BK_C = 8 and the same k-step order, so the
+// per-element summation order (and hence every bit of C) is config-independent.
+using GemmWide = GemmCfgT<128, 128, 4, 2, 6, 1>;   // 0: 128 x 128 real, 8 warps of 32 x 64
+using GemmBig = GemmCfgT<64, 128, 2, 4, 6, 1>;     // 1: 64 x 128 real, 8 warps of 32 x 32
+using GemmPair = GemmCfgT<64, 128, 2, 2, 4, 2>;    // 2: 64 x 128 real, 4 warps of 32 x 64, 2 CTAs/SM
+using GemmSmall = GemmCfgT<32, 64, 1, 2, 4, 4>;    // 3: 32 x 64 real, 2 warps, 4 CTAs/SM
+constexpr int N_GEMM_CFGS = 4;
+static const int kCfgBM[N_GEMM_CFGS] = {GemmWide::BM, GemmBig::BM, GemmPair::BM, GemmSmall::BM};
+static const int kCfgBN[N_GEMM_CFGS] = {GemmWide::BN_R, GemmBig::BN_R, GemmPair::BN_R, GemmSmall::BN_R};
+static const int kCfgOcc[N_GEMM_CFGS] = {1, 1, 2, 4};
+static int g_num_sms = 148;
+
+// Pick the tile config with the smallest modelled time: waves x per-tile DMMA cycles
+// (an SM's FP64 pipe shared by its resident CTAs) + a per-wave latency term.
+static int choose_gemm_cfg(int n, int K, int N) {
+  double best = 1e300;
+  int arg = 1;
+  for (int c = 0; c < N_GEMM_CFGS; ++c) {
+    const double tiles = (double)((n + kCfgBM[c] - 1) / kCfgBM[c]) * ((2 * N + kCfgBN[c] - 1) / kCfgBN[c]);
+    const double conc = (double)g_num_sms * kCfgOcc[c];
+    const double waves = std::ceil(tiles / conc);
+    const double tile_cycles = (double)kCfgBM[c] * kCfgBN[c] * 16.0 * ((K + 7) / 8) / 64.0 * kCfgOcc[c];
+    const double t = waves * (tile_cycles + 3000.0);
+    if (t < best * 0.999) {
+      best = t;
+      arg = c;
+    }
+  }
+  return arg;
+}
+
+template <class Cfg>
+static cudaError_t launch_cfg(const CUtensorMap& tv, const CUtensorMap& tg, double2* C, int n, int K, int N,
+                              long long ldc, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(site_gemm_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Cfg::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  dim3 grid((n + Cfg::BM - 1) / Cfg::BM, (2 * N + Cfg::BN_R - 1) / Cfg::BN_R);
+  int KT = (K + Cfg::BK_C - 1) / Cfg::BK_C;
+  site_gemm_kernel<Cfg><<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(tv, tg, C, n, N, KT, ldc);
+  return cudaGetLastError();
+}
+
+// V tensor maps use box rows = BM of the chosen config; Gamma maps always box 8 rows.
+static int launch_site_gemm(mps_ctx* ctx, const void* V, const CUtensorMap& tg, double2* C, int n, int K, int N,
+                            long long ldc, cudaStream_t st, int cfg) {
+  if (cfg < 0 || cfg >= N_GEMM_CFGS) cfg = choose_gemm_cfg(n, K, N);
+  CUtensorMap tv;
+  if (!make_tmap(&tv, V, n, 2 * (uint64_t)K, 16 * (uint64_t)K, kCfgBM[cfg]))
+    return fail(ctx, MPS_ERR_GENERIC, "state tensor map encode failed (n=%d, K=%d)", n, K);
+  cudaError_t e;
+  switch (cfg) {
+    case 0: e = launch_cfg<GemmWide>(tv, tg, C, n, K, N, ldc, st); break;
+    case 1: e = launch_cfg<GemmBig>(tv, tg, C, n, K, N, ldc, st); break;
+    case 2: e = launch_cfg<GemmPair>(tv, tg, C, n, K, N, ldc, st); break;
+    default: e = launch_cfg<GemmSmall>(tv, tg, C, n, K, N, ldc, st); break;
+  }
+  if (ctx) ctx->launches++;
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "site_gemm launch");
+  return MPS_OK;
+}
+
+extern "C" {
+
+int mps_create(int n_dev, const int* dev_ids, int layout, mps_ctx** out) {
+  if (!out) return MPS_ERR_VALIDATION;
+  *out = nullptr;
+  if (n_dev != 1) return MPS_ERR_VALIDATION;  // one context per GPU per process
+  if (layout != 0 && layout != 1) return MPS_ERR_VALIDATION;
+  int dev = dev_ids ? dev_ids[0] : 0;
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return MPS_ERR_RESOURCE;
+  }
+  if (dev < 0 || dev >= count) return MPS_ERR_VALIDATION;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess || prop.major != 10) return MPS_ERR_RESOURCE;
+  if (cudaSetDevice(dev) != cudaSuccess) return MPS_ERR_GENERIC;
+  if (!get_encode_fn()) return MPS_ERR_GENERIC;
+  g_num_sms = prop.multiProcessorCount;
+  mps_ctx* c = new mps_ctx();
+  c->device = dev;
+  c->layout = layout;
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete c;
+    return MPS_ERR_GENERIC;
+  }
+  *out = c;
+  return MPS_OK;
+}
+
+int mps_configure(mps_ctx* c, int M, int D) {
+  if (!c) return MPS_ERR_VALIDATION;
+  if (M < 1) return fail(c, MPS_ERR_VALIDATION, "M must be >= 1, got %d", M);
+  if (D < 1 || D > DMAX) return fail(c, MPS_ERR_VALIDATION, "D must lie in [1, %d], got %d", DMAX, D);
+  cudaSetDevice(c->device);
+  for (auto& s : c->sites)
+    if (s.owned && s.data) cudaFree(s.data);
+  c->sites.assign(M, Site());
+  c->M = M;
+  c->D = D;
+  return MPS_OK;
+}
+
+int mps_set_site(mps_ctx* c, int m, int chi_l, int chi_r, int D, const void* gamma, int flags, int dtype) {
+  if (!c) return MPS_ERR_VALIDATION;
+  if (c->M == 0) return fail(c, MPS_ERR_VALIDATION, "mps_configure must precede mps_set_site");
+  if (m < 0 || m >= c->M) return fail(c, MPS_ERR_VALIDATION, "site index %d outside [0, %d)", m, c->M);
+  if (D != c->D) return fail(c, MPS_ERR_VALIDATION, "site %d: D=%d but the chain has D=%d", m, D, c->D);
+  if (chi_l < 1 || chi_r < 1) return fail(c, MPS_ERR_VALIDATION, "site %d: bond dims must be >= 1", m);
+  if (dtype != MPS_C128) return fail(c, MPS_ERR_VALIDATION, "site %d: only complex128 (dtype 0) is supported", m);
+  if (!gamma) return fail(c, MPS_ERR_VALIDATION, "site %d: null tensor", m);
+  if (m > 0 && c->sites[m - 1].data && c->sites[m - 1].chi_r != chi_l)
+    return fail(c, MPS_ERR_VALIDATION, "site %d: chi_l=%d != chi_r=%d of site %d", m, chi_l, c->sites[m - 1].chi_r,
+                m - 1);
+  if (m + 1 < c->M && c->sites[m + 1].data && c->sites[m + 1].chi_l != chi_r)
+    return fail(c, MPS_ERR_VALIDATION, "site %d: chi_r=%d != chi_l=%d of site %d", m, chi_r, c->sites[m + 1].chi_l,
+                m + 1);
+  cudaSetDevice(c->device);
+  Site& s = c->sites[m];
+  if (s.owned && s.data) cudaFree(s.data);
+  s = Site();
+  const size_t elems = (size_t)chi_l * chi_r * D;
+  const bool dev = is_device_ptr(gamma);
+  if (flags == MPS_SITE_DEVICE_BORROW) {
+    if (!dev) return fail(c, MPS_ERR_VALIDATION, "site %d: BORROW needs a device pointer", m);
+    s.data = (double2*)gamma;
+  } else {
+    CU(c, cudaMalloc(&s.data, elems * sizeof(double2)), "cudaMalloc(site)");
+    s.owned = true;
+    CU(c, cudaMemcpy(s.data, gamma, elems * sizeof(double2), dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice),
+       "copy site");
+  }
+  s.chi_l = chi_l;
+  s.chi_r = chi_r;
+  const uint64_t N = (uint64_t)chi_r * D;
+  if (!make_tmap(&s.tmap, s.data, chi_l, 2 * N, 16 * N, 8))
+    return fail(c, MPS_ERR_GENERIC, "site %d: cuTensorMapEncodeTiled failed", m);
+  return MPS_OK;
+}
+
+int mps_set_streams(mps_ctx* c, uint64_t seed, double alpha_sigma) {
+  if (!c) return MPS_ERR_VALIDATION;
+  if (!(alpha_sigma == alpha_sigma)) return fail(c, MPS_ERR_VALIDATION, "alpha_sigma is NaN");
+  c->seed = seed;
+  c->alpha_sigma = alpha_sigma;
+  return MPS_OK;
+}
+
+int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, int n, const double* uniforms,
+                     int64_t ld_u, const void* disp, const void* alpha, const void* state_in, void* state_out,
+                     int32_t* counts, int64_t ld_c, double* marginals, uint8_t* status, uint64_t stream) {
+  if (!c) return MPS_ERR_VALIDATION;
+  c->err.clear();
+  if (c->M == 0) return fail(c, MPS_ERR_VALIDATION, "context not configured");
+  if (m_begin < 0 || m_end > c->M || m_begin >= m_end)
+    return fail(c, MPS_ERR_VALIDATION, "mode range [%d, %d) invalid for M=%d", m_begin, m_end, c->M);
+  if (n < 0) return fail(c, MPS_ERR_VALIDATION, "n must be >= 0");
+  if (first_index < 0) return fail(c, MPS_ERR_VALIDATION, "first_index must be >= 0");
+  if (!counts) return fail(c, MPS_ERR_VALIDATION, "counts output is required");
+  if (ld_c < c->M || (uniforms && ld_u < c->M)) return fail(c, MPS_ERR_VALIDATION, "row strides must be >= M");
+  for (int m = m_begin; m < m_end; ++m)
+    if (!c->sites[m].data) return fail(c, MPS_ERR_VALIDATION, "site %d not loaded", m);
+  for (int m = m_begin + 1; m < m_end; ++m)
+    if (c->sites[m].chi_l != c->sites[m - 1].chi_r)
+      return fail(c, MPS_ERR_VALIDATION, "bond mismatch between sites %d and %d", m - 1, m);
+  if (n == 0) return MPS_OK;
+  if (!state_in && c->sites[m_begin].chi_l != 1)
+    return fail(c, MPS_ERR_VALIDATION, "state_in is required when chi_l of site %d is %d", m_begin,
+                c->sites[m_begin].chi_l);
+  if (state_in && !is_device_ptr(state_in)) return fail(c, MPS_ERR_VALIDATION, "state_in must be device memory");
+  if (state_out && !is_device_ptr(state_out)) return fail(c, MPS_ERR_VALIDATION, "state_out must be device memory");
+
+  cudaSetDevice(c->device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);  // 0 = legacy default stream
+  const int M = c->M, D = c->D;
+  int chi_max = 1;
+  for (int m = m_begin; m < m_end; ++m) chi_max = std::max(chi_max, std::max(c->sites[m].chi_l, c->sites[m].chi_r));
+  CU(c, c->v0.ensure((size_t)n * chi_max), "alloc state");
+  CU(c, c->v1.ensure((size_t)n * chi_max), "alloc state");
+  size_t cmax = 0;
+  for (int m = m_begin; m < m_end; ++m) cmax = std::max(cmax, (size_t)c->sites[m].chi_r * D);
+  CU(c, c->cbuf.ensure((size_t)n * cmax), "alloc C buffer");
+
+  // ---- inputs: stage host arrays on the device ----
+  const double* u_dev = uniforms;
+  int64_t ldu = ld_u;
+  if (uniforms && !is_device_ptr(uniforms)) {
+    CU(c, c->u_d.ensure((size_t)n * ld_u), "alloc uniforms");
+    CU(c, cudaMemcpyAsync(c->u_d.p, uniforms, (size_t)n * ld_u * sizeof(double), cudaMemcpyHostToDevice, st), "H2D u");
+    u_dev = c->u_d.p;
+  }
+  const double2* alpha_dev = (const double2*)alpha;
+  if (alpha && !is_device_ptr(alpha)) {
+    CU(c, c->alpha_d.ensure((size_t)n * M), "alloc alpha");
+    CU(c, cudaMemcpyAsync(c->alpha_d.p, alpha, (size_t)n * M * sizeof(double2), cudaMemcpyHostToDevice, st), "H2D alpha");
+    alpha_dev = c->alpha_d.p;
+  }
+  const double2* disp_dev = (const double2*)disp;
+  if (disp && !is_device_ptr(disp)) {
+    CU(c, c->disp_d.ensure((size_t)n * M * D * D), "alloc disp");
+    CU(c, cudaMemcpyAsync(c->disp_d.p, disp, (size_t)n * M * D * D * sizeof(double2), cudaMemcpyHostToDevice, st),
+       "H2D disp");
+    disp_dev = c->disp_d.p;
+  }
+  const bool counts_host = !is_device_ptr(counts);
+  const bool marg_host = marginals && !is_device_ptr(marginals);
+  const bool status_host = status && !is_device_ptr(status);
+  int32_t* counts_dev = counts;
+  if (counts_host) {
+    CU(c, c->counts_d.ensure((size_t)n * ld_c), "alloc counts");
+    counts_dev = c->counts_d.p;
+  }
+  double* marg_dev = marginals;
+  if (marg_host) {
+    CU(c, c->marg_d.ensure((size_t)n * ld_c * D), "alloc marginals");
+    marg_dev = c->marg_d.p;
+  }
+  uint8_t* status_dev = status;
+  if (!status || status_host) {
+    CU(c, c->status_d.ensure((size_t)n), "alloc status");
+    status_dev = c->status_d.p;
+    if (status_host)
+      CU(c, cudaMemcpyAsync(status_dev, status, n, cudaMemcpyHostToDevice, st), "H2D status");
+    else
+      CU(c, cudaMemsetAsync(status_dev, 0, n, st), "memset status");
+  }
+  if (counts_host && m_end - m_begin < M) {
+    // partial range into host arrays: keep the untouched columns
+    CU(c, cudaMemcpyAsync(counts_dev, counts, (size_t)n * ld_c * sizeof(int32_t), cudaMemcpyHostToDevice, st),
+       "H2D counts");
+  }
+  if (marg_host && m_end - m_begin < M) {
+    CU(c, cudaMemcpyAsync(marg_dev, marginals, (size_t)n * ld_c * D * sizeof(double), cudaMemcpyHostToDevice, st),
+       "H2D marginals");
+  }
+
+  // ---- the mode loop ----
+  const double2* v_in = (const double2*)state_in;
+  if (!v_in) {
+    CU(c, c->ones.ensure((size_t)n), "alloc ones");
+    fill_ones_kernel<<<(n + 255) / 256, 256, 0, st>>>(c->ones.p, n);
+    c->launches++;
+    v_in = c->ones.p;
+  }
+  double2* bufs[2] = {c->v0.p, c->v1.p};
+  int cur = 0;
+  for (int m = m_begin; m < m_end; ++m) {
+    const Site& s = c->sites[m];
+    const int N = s.chi_r * D;
+    mps_ctx::Rec rg{0, nullptr, nullptr, 8.0 * n * (double)s.chi_l * N};
+    if (c->profile) {
+      rg.a = c->get_event();
+      rg.b = c->get_event();
+      cudaEventRecord(rg.a, st);
+    }
+    int rc = launch_site_gemm(c, v_in, s.tmap, c->cbuf.p, n, s.chi_l, N, N, st, c->gemm_cfg);
+    if (rc) return rc;
+    if (c->profile) {
+      cudaEventRecord(rg.b, st);
+      c->recs.push_back(rg);
+    }
+    double2* v_out = (m == m_end - 1 && state_out) ? (double2*)state_out : bufs[cur];
+    DrawArgs a;
+    a.C = c->cbuf.p;
+    a.ldc = N;
+    a.chi_r = s.chi_r;
+    a.D = D;
+    a.m = m;
+    a.M = M;
+    a.first_index = first_index;
+    a.u = u_dev;
+    a.ld_u = ldu;
+    a.seed = c->seed;
+    a.disp = disp_dev;
+    a.alpha = alpha_dev;
+    a.alpha_sigma = (disp_dev || alpha_dev) ? -1.0 : c->alpha_sigma;
+    a.v_out = v_out;
+    a.counts = counts_dev;
+    a.ld_c = ld_c;
+    a.marg = marg_dev;
+    a.status = status_dev;
+    // algorithmic bytes: C read once, v' written, u read, count written
+    mps_ctx::Rec rd{1, nullptr, nullptr, 16.0 * n * N + 16.0 * n * s.chi_r + 12.0 * n};
+    if (c->profile) {
+      rd.a = c->get_event();
+      rd.b = c->get_event();
+      cudaEventRecord(rd.a, st);
+    }
+    displace_draw_kernel<<<n, DRAW_THREADS, 0, st>>>(a);
+    c->launches++;
+    if (c->profile) {
+      cudaEventRecord(rd.b, st);
+      c->recs.push_back(rd);
+    }
+    CU(c, cudaGetLastError(), "displace_draw launch");
+    v_in = v_out;
+    cur ^= 1;
+  }
+
+  // ---- outputs back to the host ----
+  bool sync = false;
+  if (counts_host) {
+    CU(c, cudaMemcpyAsync(counts, counts_dev, (size_t)n * ld_c * sizeof(int32_t), cudaMemcpyDeviceToHost, st), "D2H counts");
+    sync = true;
+  }
+  if (marg_host) {
+    CU(c, cudaMemcpyAsync(marginals, marg_dev, (size_t)n * ld_c * D * sizeof(double), cudaMemcpyDeviceToHost, st),
+       "D2H marginals");
+    sync = true;
+  }
+  if (status_host) {
+    CU(c, cudaMemcpyAsync(status, status_dev, n, cudaMemcpyDeviceToHost, st), "D2H status");
+    sync = true;
+  }
+  if (sync || uniforms != u_dev || alpha != (const void*)alpha_dev || disp != (const void*)disp_dev)
+    CU(c, cudaStreamSynchronize(st), "stream sync");
+  return MPS_OK;
+}
+
+int mps_sample(mps_ctx* c, int64_t first_index, int n, const double* uniforms, const void* disp, const void* alpha,
+               int32_t* counts, double* marginals, uint64_t* n_flagged) {
+  if (!c) return MPS_ERR_VALIDATION;
+  if (c->M == 0) return fail(c, MPS_ERR_VALIDATION, "context not configured");
+  if (n < 0) return fail(c, MPS_ERR_VALIDATION, "n must be >= 0");
+  std::vector<uint8_t> st(n > 0 ? n : 1, 0);
+  int rc = mps_sample_range(c, 0, c->M, first_index, n, uniforms, c->M, disp, alpha, nullptr, nullptr, counts, c->M,
+                            marginals, st.data(), reinterpret_cast<uint64_t>(c->stream));
+  if (rc) return rc;
+  uint64_t fl = 0;
+  for (int i = 0; i < n; ++i) fl += (st[i] & ST_FLAGGED) ? 1 : 0;
+  if (n_flagged) *n_flagged = fl;
+  return MPS_OK;
+}
+
+uint64_t mps_kernel_launches(const mps_ctx* c) { return c ? c->launches : 0; }
+
+int mps_profile(mps_ctx* c, int enable) {
+  if (!c) return MPS_ERR_VALIDATION;
+  c->profile = enable != 0;
+  return MPS_OK;
+}
+
+int mps_profile_read(mps_ctx* c, double* out6) {
+  if (!c || !out6) return MPS_ERR_VALIDATION;
+  double acc[6] = {0, 0, 0, 0, 0, 0};  // gemm: ms, launches, flops; draw: ms, launches, bytes
+  for (auto& r : c->recs) {
+    cudaEventSynchronize(r.b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    acc[3 * r.kind + 0] += ms;
+    acc[3 * r.kind + 1] += 1;
+    acc[3 * r.kind + 2] += r.work;
+    c->event_pool.push_back(r.a);
+    c->event_pool.push_back(r.b);
+  }
+  c->recs.clear();
+  for (int i = 0; i < 6; ++i) out6[i] = acc[i];
+  return MPS_OK;
+}
+
+const char* mps_last_error(const mps_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+void mps_destroy(mps_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (auto& s : c->sites)
+    if (s.owned && s.data) cudaFree(s.data);
+  c->v0.release();
+  c->v1.release();
+  c->cbuf.release();
+  c->ones.release();
+  c->alpha_d.release();
+  c->disp_d.release();
+  c->u_d.release();
+  c->marg_d.release();
+  c->counts_d.release();
+  c->status_d.release();
+  for (auto& r : c->recs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (auto e : c->event_pool) cudaEventDestroy(e);
+  cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+int mps_site_gemm_cfg(const void* V, const void* G, void* C, int n, int K, int N, int64_t ldc, uint64_t stream,
+                      int cfg) {
+  if (!V || !G || !C || n < 1 || K < 1 || N < 1 || ldc < N) return MPS_ERR_VALIDATION;
+  CUtensorMap tg;
+  if (!make_tmap(&tg, G, K, 2 * (uint64_t)N, 16 * (uint64_t)N, 8)) return MPS_ERR_GENERIC;
+  return launch_site_gemm(nullptr, V, tg, (double2*)C, n, K, N, ldc, reinterpret_cast<cudaStream_t>(stream), cfg);
+}
+
+int mps_site_gemm(const void* V, const void* G, void* C, int n, int K, int N, int64_t ldc, uint64_t stream) {
+  return mps_site_gemm_cfg(V, G, C, n, K, N, ldc, stream, -1);
+}
+
+int mps_set_gemm_config(mps_ctx* c, int cfg) {
+  if (!c) return MPS_ERR_VALIDATION;
+  if (cfg < -1 || cfg >= N_GEMM_CFGS) return fail(c, MPS_ERR_VALIDATION, "gemm config %d outside [-1, %d)", cfg,
+                                                  N_GEMM_CFGS);
+  c->gemm_cfg = cfg;
+  return MPS_OK;
+}
+
+int mps_displacement(const void* alpha, int count, int D, void* out, uint64_t stream) {
+  if (!alpha || !out || count < 0 || D < 1 || D > DMAX) return MPS_ERR_VALIDATION;
+  if (count == 0) return MPS_OK;
+  displacement_kernel<<<(count + 127) / 128, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      (const double2*)alpha, count, D, (double2*)out);
+  return cudaGetLastError() == cudaSuccess ? MPS_OK : MPS_ERR_GENERIC;
+}
+
+int mps_stream_uniforms(uint64_t seed, int64_t first, int count, int M, double* out, uint64_t stream) {
+  if (!out || count < 0 || M < 1 || first < 0) return MPS_ERR_VALIDATION;
+  if (count == 0) return MPS_OK;
+  long long total = (long long)count * M;
+  stream_uniforms_kernel<<<(unsigned)((total + 255) / 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      seed, first, count, M, out, M);
+  return cudaGetLastError() == cudaSuccess ? MPS_OK : MPS_ERR_GENERIC;
+}
+
+}  // extern "C"

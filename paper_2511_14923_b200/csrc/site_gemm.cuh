@@ -1,0 +1,154 @@
+// site_gemm.cuh — K1: the per-mode site contraction C = V . Gamma.
+//
+//   V     : n x K complex128 (the n in-flight temp_tensors)
+//   Gamma : K x N complex128, N = chi_r * D (Gamma^[m] reshaped chi_l x chi_r D)
+//   C     : n x N complex128
+//
+// B200 has no FP64 tcgen05 kind, so the FP64 tensor pipe is reached through
+// mma.sync .f64 (SASS DMMA.8x8x4: 256 FMA per warp instruction, measured peak
+// 37.0 TFLOP/s, profiles/fp64_peak.json).  The complex product is a "real-doubled"
+// 4M GEMM done without any repacking:
+//   A_r[b][2i+p]  = V[b][i].(re, im)[p]          (V's own interleaved layout)
+//   B_r[2i][2c+q] = Gamma[i][c].(re, im)[q]       (Gamma's own interleaved layout)
+//   B_r[2i+1][2c] = -Gamma[i][c].im,  B_r[2i+1][2c+1] = Gamma[i][c].re
+// so C_r = A_r B_r holds C interleaved, and the odd rows of B_r are produced while
+// loading fragments (component swap + sign flip) from the same smem tile.
+//
+// Pipeline: thread 0 issues TMA loads of the V tile (BM x 16 doubles) and BN_R/16
+// Gamma boxes (8 rows x 16 doubles each), 128-byte swizzled, into a STAGES-deep ring
+// guarded by full/empty mbarriers, refilling each slot one iteration after it was
+// consumed.  No dedicated producer warp: 8 warps = 2 per SM sub-partition keeps the
+// 255-register budget (a 9th warp caps every warp at 168 and spills).  Each warp owns
+// a (8 MF) x (8 NF) real sub-tile of DMMA fragments.  The k order inside a 16-double
+// stage row is permuted (x = 2s + 8(t&1) + (t>>1) for lane-in-group t, step s) so both
+// fragment loads are bank-conflict free against the TMA 128B swizzle.
+//
+// Summation order per output element is fixed by (K, stage, step) only — the same for
+// every tile configuration, n, tile position and grid — so results are bit-identical
+// across batch sizes and GPU counts (sampler.py:272-285 invariance tests).
+#pragma once
+#include "ptx.cuh"
+
+namespace mps {
+
+template <int BM_, int BN_R_, int WARPS_M_, int WARPS_N_, int STAGES_, int MIN_BLOCKS_>
+struct GemmCfgT {
+  static constexpr int BM = BM_;          // rows (samples) per CTA tile
+  static constexpr int BN_R = BN_R_;      // real columns per CTA tile
+  static constexpr int BK_C = 8;          // complex K rows per stage (16 real) — fixed: sets the sum order
+  static constexpr int STAGES = STAGES_;
+  static constexpr int WARPS_M = WARPS_M_, WARPS_N = WARPS_N_;
+  static constexpr int WARPS = WARPS_M * WARPS_N;
+  static constexpr int THREADS = WARPS * 32;
+  static constexpr int MIN_BLOCKS = MIN_BLOCKS_;
+  static constexpr int WM = BM / WARPS_M, WN = BN_R / WARPS_N;  // warp tile (real)
+  static constexpr int MF = WM / 8, NF = WN / 8;                // DMMA 8x8 fragments per warp
+  static constexpr int A_BYTES = BM * 16 * 8;
+  static constexpr int B_GROUPS = BN_R / 16;
+  static constexpr int B_BYTES = B_GROUPS * BK_C * 128;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 2 * STAGES * 8;
+  static_assert(BM % (8 * WARPS_M) == 0 && BN_R % (16 * WARPS_N) == 0 && WN % 16 == 0, "tile shape");
+  static_assert(A_BYTES % 1024 == 0 && B_BYTES % 1024 == 0, "128B-swizzle atoms need 1 KiB alignment");
+};
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
+    site_gemm_kernel(const __grid_constant__ CUtensorMap tmap_v, const __grid_constant__ CUtensorMap tmap_g,
+                     double2* __restrict__ C, int n, int N, int KT, long long ldc) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  // align to 1 KiB by pointer arithmetic on the __shared__ array (keeps LDS addressing)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint64_t* empty = full + Cfg::STAGES;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * Cfg::BM;
+  const int n0r = blockIdx.y * Cfg::BN_R;
+
+  auto issue = [&](int kt) {  // one k-stage: the V tile + B_GROUPS Gamma boxes
+    const int s = kt % Cfg::STAGES;
+    uint8_t* As = smem + s * Cfg::STAGE_BYTES;
+    uint8_t* Bs = As + Cfg::A_BYTES;
+    mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
+    tma_load_2d(As, &tmap_v, kt * 16, m0, &full[s]);
+#pragma unroll
+    for (int gi = 0; gi < Cfg::B_GROUPS; ++gi)
+      tma_load_2d(Bs + gi * (Cfg::BK_C * 128), &tmap_g, n0r + gi * 16, kt * Cfg::BK_C, &full[s]);
+  };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < Cfg::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], Cfg::WARPS);
+    }
+    fence_barrier_init();
+    prefetch_tmap(&tmap_v);
+    prefetch_tmap(&tmap_g);
+    for (int kt = 0; kt < Cfg::STAGES && kt < KT; ++kt) issue(kt);
+  }
+  __syncthreads();
+
+  const int g = lane >> 2;  // group id: fragment row (A) / column (B)
+  const int t = lane & 3;   // thread in group: fragment k index
+  const int warp_m = warp % Cfg::WARPS_M;
+  const int warp_n = warp / Cfg::WARPS_M;
+  const int p = t >> 1;  // 0: real row of B_r, 1: rotated row
+  const uint64_t sign = ((p == 1) && ((g & 1) == 0)) ? 0x8000000000000000ull : 0ull;
+
+  double acc[Cfg::MF][Cfg::NF][2];
+#pragma unroll
+  for (int i = 0; i < Cfg::MF; ++i)
+#pragma unroll
+    for (int j = 0; j < Cfg::NF; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  for (int kt = 0; kt < KT; ++kt) {
+    const int s = kt % Cfg::STAGES;
+    mbar_wait(&full[s], (kt / Cfg::STAGES) & 1);
+    const uint8_t* As = smem + s * Cfg::STAGE_BYTES + (warp_m * Cfg::WM + g) * 128 + (p << 3);
+    const uint8_t* Bs = smem + s * Cfg::STAGE_BYTES + Cfg::A_BYTES + warp_n * (Cfg::WN / 16) * (Cfg::BK_C * 128);
+#pragma unroll
+    for (int step = 0; step < 4; ++step) {
+      const int i = step + 4 * (t & 1);  // complex row of the stage == 16B chunk of the A row
+      double a[Cfg::MF], b[Cfg::NF];
+#pragma unroll
+      for (int mf = 0; mf < Cfg::MF; ++mf)
+        a[mf] = *reinterpret_cast<const double*>(As + mf * 8 * 128 + ((i ^ g) << 4));
+#pragma unroll
+      for (int nf = 0; nf < Cfg::NF; ++nf) {
+        const int xb = (((nf & 1) * 8) + g) ^ p;
+        const uint64_t bits = *reinterpret_cast<const uint64_t*>(
+            Bs + (nf >> 1) * (Cfg::BK_C * 128) + i * 128 + (((xb >> 1) ^ i) << 4) + ((xb & 1) << 3));
+        b[nf] = __longlong_as_double(static_cast<long long>(bits ^ sign));
+      }
+#pragma unroll
+      for (int mf = 0; mf < Cfg::MF; ++mf)
+#pragma unroll
+        for (int nf = 0; nf < Cfg::NF; ++nf) dmma_8x8x4(acc[mf][nf][0], acc[mf][nf][1], a[mf], b[nf]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    // Producer (thread 0): refill the slot of k-stage kt-1 — every warp has long left it
+    // by the time warp 0 finishes kt, so this wait rarely blocks.
+    if (threadIdx.x == 0 && kt >= 1 && kt - 1 + Cfg::STAGES < KT) {
+      mbar_wait(&empty[(kt - 1) % Cfg::STAGES], ((kt - 1) / Cfg::STAGES) & 1);
+      issue(kt - 1 + Cfg::STAGES);
+    }
+  }
+
+  // ---------------- epilogue: (c0, c1) of a fragment is one complex entry ----------------
+#pragma unroll
+  for (int mf = 0; mf < Cfg::MF; ++mf) {
+    const int row = m0 + warp_m * Cfg::WM + mf * 8 + g;
+    if (row >= n) continue;
+    double2* crow = C + (long long)row * ldc;
+#pragma unroll
+    for (int nf = 0; nf < Cfg::NF; ++nf) {
+      const int col = (n0r >> 1) + warp_n * (Cfg::WN / 2) + nf * 4 + t;
+      if (col < N) crow[col] = make_double2(acc[mf][nf][0], acc[mf][nf][1]);
+    }
+  }
+}
+
+}  // namespace mps

@@ -1,0 +1,121 @@
+"""The MPS container: site tensors Gamma^[m] (chi_l x chi_r x D, complex128).
+
+Convention: the amplitude of |d_0 .. d_{M-1}> is the ordered
+product of Gamma^[m][:, :, d_m]; chi_0 = chi_M = 1.  Sites are row-orthonormal
+(Gamma.reshape(chi_l, chi_r D) has orthonormal rows) so the left-to-right
+chain rule samples the Born distribution exactly.
+
+Random sites follow the reference's Haar recipe, QR of a complex Gaussian with
+the diagonal phase fix (gaussian.py:387-391), on the host (numpy, seeded by
+(seed, m)) or on the device (torch + cuSOLVER, for sites too large to build on
+the host; BASELINE.json config 5 "generated on device from per-site seeds").
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .errors import ValidationError
+
+
+def bond_dims(M: int, chi: int, D: int) -> list[int]:
+    """chi_0 .. chi_M: 1 at both ends, min(chi, D^m, D^(M-m)) inside."""
+    if M < 1 or chi < 1 or D < 1:
+        raise ValidationError("M, chi and D must be >= 1")
+    dims = [1]
+    for m in range(1, M):
+        e = min(m, M - m)
+        p = 1
+        for _ in range(e):
+            p *= D
+            if p >= chi:
+                break
+        dims.append(min(chi, p))
+    dims.append(1)
+    return dims
+
+
+def host_site(seed: int, m: int, chi_l: int, chi_r: int, D: int) -> np.ndarray:
+    if chi_l > chi_r * D:
+        raise ValidationError(f"site {m}: chi_l={chi_l} > chi_r*D={chi_r * D}: no row-orthonormal site")
+    rng = np.random.default_rng([seed, m])
+    Z = (rng.standard_normal((chi_r * D, chi_l)) + 1j * rng.standard_normal((chi_r * D, chi_l))) / np.sqrt(2.0)
+    Q, R = np.linalg.qr(Z)
+    d = np.diagonal(R)
+    Q = Q * (d / np.abs(d))
+    return np.ascontiguousarray(Q.conj().T.reshape(chi_l, chi_r, D))
+
+
+def device_site(seed: int, m: int, chi_l: int, chi_r: int, D: int, device="cuda"):
+    """Same recipe on the device; the Gaussian comes from torch's CUDA Philox keyed
+    (seed, m), so values differ from :func:`host_site` but the law is identical."""
+    import torch
+
+    if chi_l > chi_r * D:
+        raise ValidationError(f"site {m}: chi_l={chi_l} > chi_r*D={chi_r * D}: no row-orthonormal site")
+    g = torch.Generator(device=device)
+    g.manual_seed((int(seed) * 1_000_003 + int(m)) & (2**63 - 1))
+    Z = torch.randn(chi_r * D, chi_l, dtype=torch.complex128, device=device, generator=g)
+    Q, R = torch.linalg.qr(Z)
+    d = torch.diagonal(R)
+    Q = Q * (d / d.abs())
+    out = Q.conj().T.reshape(chi_l, chi_r, D).contiguous()
+    del Z, Q, R
+    return out
+
+
+@dataclass
+class MPS:
+    """Ordered site tensors (numpy arrays or CUDA torch tensors, complex128)."""
+
+    sites: list
+
+    def __post_init__(self):
+        if not self.sites:
+            raise ValidationError("an MPS needs at least one site")
+        D = None
+        prev = None
+        for m, G in enumerate(self.sites):
+            shape = tuple(G.shape)
+            if len(shape) != 3:
+                raise ValidationError(f"site {m}: expected (chi_l, chi_r, D), got shape {shape}")
+            if str(G.dtype) not in ("complex128", "torch.complex128"):
+                raise ValidationError(f"site {m}: dtype {G.dtype} is not complex128")
+            if D is None:
+                D = shape[2]
+            elif shape[2] != D:
+                raise ValidationError(f"site {m}: D={shape[2]} differs from D={D}")
+            if prev is not None and shape[0] != prev:
+                raise ValidationError(f"site {m}: chi_l={shape[0]} != chi_r={prev} of site {m - 1}")
+            prev = shape[1]
+        if self.sites[0].shape[0] != 1:
+            raise ValidationError("chi_0 must be 1")
+
+    @property
+    def M(self) -> int:
+        return len(self.sites)
+
+    @property
+    def D(self) -> int:
+        return int(self.sites[0].shape[2])
+
+    @property
+    def bond_dims(self) -> list[int]:
+        return [int(G.shape[0]) for G in self.sites] + [int(self.sites[-1].shape[1])]
+
+    @property
+    def chi(self) -> int:
+        return max(self.bond_dims)
+
+    @property
+    def nbytes(self) -> int:
+        return sum(int(np.prod(G.shape)) * 16 for G in self.sites)
+
+    @classmethod
+    def random(cls, M: int, chi: int, D: int, seed: int = 0, device: str = "cpu") -> "MPS":
+        dims = bond_dims(M, chi, D)
+        if device == "cpu":
+            return cls([host_site(seed, m, dims[m], dims[m + 1], D) for m in range(M)])
+        return cls([device_site(seed, m, dims[m], dims[m + 1], D, device) for m in range(M)])

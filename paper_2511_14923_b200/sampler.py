@@ -1,0 +1,276 @@
+"""Sampling entry point for method "mps" — the reference's interface, B200 engine.
+
+Mirrors ``gbsemu.sampler`` (pkg/src/gbsemu/sampler.py):
+
+* :class:`MpsSamplerConfig` — frozen, validated on construction, raising
+  :class:`ValidationError` (SamplerConfig, sampler.py:51-79);
+* :class:`MpsSampleBatch` — samples plus provenance and timing, with
+  ``n_failed`` / ``n_flagged`` accounting (SampleBatch, sampler.py:82-95);
+* :func:`batch_sample` — N samples, chunked into micro-batches, failed samples
+  dropped and counted (sampler.py:706-761);
+* :func:`sample_one` — sample ``index`` of the configured stream
+  (sampler.py:672-676);
+* randomness is counter-based: the uniforms of sample i are
+  ``_stream_uniforms(seed, i, M)`` (sampler.py:109-125), evaluated on the device
+  bit-for-bit, so output is identical for any batch size and GPU count.
+
+Everything heavy runs in libmps_b200.so (include/mps_sampler.h) through ctypes;
+torch only allocates device memory.  There is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from .errors import ValidationError
+from .mps import MPS
+
+METHODS = ("mps",)
+DEFAULT_BATCH = 1024
+
+
+@dataclass(frozen=True)
+class MpsSamplerConfig:
+    """Sampling parameters.
+
+    N: samples; seed: counter-stream seed (uniforms and alpha); alpha_sigma:
+    displacement alpha ~ CN(0, alpha_sigma^2) per sample and mode (None: no
+    displacement unless explicit ``disp`` / ``alpha`` arrays are passed);
+    batch_size: samples in flight per micro-batch (n); device: CUDA ordinal.
+    """
+
+    N: int
+    seed: int = 0
+    alpha_sigma: float | None = None
+    batch_size: int | None = None
+    device: int = 0
+    method: str = "mps"
+
+    def __post_init__(self):
+        if self.method not in METHODS:
+            raise ValidationError(f"unknown method {self.method!r}")
+        if self.N < 0:
+            raise ValidationError("N must be >= 0")
+        if self.seed < 0 or self.seed >= 2**63:
+            # numpy routes key lists holding ints >= 2^63 through float64, which would
+            # collapse the alpha stream's block keys; the uniform stream alone keeps the quirk
+            raise ValidationError("seed must lie in [0, 2^63)")
+        if self.alpha_sigma is not None and not (self.alpha_sigma >= 0.0 and np.isfinite(self.alpha_sigma)):
+            raise ValidationError("alpha_sigma must be a finite number >= 0")
+        if self.batch_size is not None and self.batch_size < 1:
+            raise ValidationError("batch_size must be >= 1")
+        if self.device < 0:
+            raise ValidationError("device must be >= 0")
+
+
+@dataclass
+class MpsSampleBatch:
+    """Photon-count samples (N x M int32) plus provenance and per-sample timing."""
+
+    M: int
+    N: int
+    counts: np.ndarray
+    method: str
+    seed: int
+    D: int = 0
+    chi: int = 0
+    wall_time: float = 0.0
+    per_sample_mean: float = 0.0
+    n_failed: int = 0
+    n_flagged: int = 0
+    indices: np.ndarray = field(default=None, repr=False)
+
+    @property
+    def bitstrings(self) -> np.ndarray:
+        """Threshold-detector view (clicks = counts > 0), the reference's sample format."""
+        return (self.counts > 0).astype(np.uint8)
+
+
+def _ptr(x) -> int | None:
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        return x.ctypes.data
+    return x.data_ptr()  # torch tensor
+
+
+class MpsSampler:
+    """A native context on one GPU holding (a block of) the sites of an MPS.
+
+    ``sites_range`` = (m_begin, m_end) loads only that block (mode-pipelined stage).
+    """
+
+    def __init__(self, mps: MPS, device: int = 0, layout: int = 0, sites_range=None, borrow: bool = True):
+        _native.require_cuda()
+        import torch
+
+        self._torch = torch
+        self.L = _native.lib()
+        self.mps = mps
+        self.M, self.D = mps.M, mps.D
+        self.device = device
+        self.dims = mps.bond_dims
+        self.sites_range = tuple(sites_range) if sites_range else (0, mps.M)
+        ctx = ctypes.c_void_p()
+        dev = (ctypes.c_int * 1)(device)
+        _native.check(self.L.mps_create(1, dev, layout, ctypes.byref(ctx)))
+        self.ctx = ctx
+        try:
+            _native.check(self.L.mps_configure(self.ctx, self.M, self.D), self.ctx)
+            self._keep = []
+            for m in range(*self.sites_range):
+                G = mps.sites[m]
+                if isinstance(G, np.ndarray):
+                    G = np.ascontiguousarray(G, dtype=np.complex128)
+                    flags = _native.MPS_SITE_HOST
+                else:
+                    G = G.contiguous()
+                    flags = _native.MPS_SITE_DEVICE_BORROW if borrow else _native.MPS_SITE_DEVICE_COPY
+                    if borrow:
+                        self._keep.append(G)
+                chl, chr_, D = (int(s) for s in G.shape)
+                _native.check(self.L.mps_set_site(self.ctx, m, chl, chr_, D, _ptr(G), flags, _native.MPS_C128),
+                              self.ctx)
+        except Exception:
+            self.close()
+            raise
+
+    # -- low level -------------------------------------------------------------
+    def set_streams(self, seed: int, alpha_sigma: float | None):
+        _native.check(self.L.mps_set_streams(self.ctx, seed, -1.0 if alpha_sigma is None else float(alpha_sigma)),
+                      self.ctx)
+
+    def run(self, first_index: int, n: int, counts, *, m_begin=None, m_end=None, uniforms=None, disp=None,
+            alpha=None, state_in=None, state_out=None, marginals=None, status=None, stream=None):
+        """One mps_sample_range call.  Arrays are numpy (host) or torch (device);
+        full-width (column = absolute mode)."""
+        mb = self.sites_range[0] if m_begin is None else m_begin
+        me = self.sites_range[1] if m_end is None else m_end
+        ld_u = uniforms.shape[1] if uniforms is not None else self.M
+        ld_c = counts.shape[1]
+        if stream is None:  # run on torch's current stream so torch ops stay ordered with ours
+            stream = self._torch.cuda.current_stream(self.device).cuda_stream
+        rc = self.L.mps_sample_range(self.ctx, mb, me, first_index, n, _ptr(uniforms), ld_u, _ptr(disp), _ptr(alpha),
+                                     _ptr(state_in), _ptr(state_out), _ptr(counts), ld_c, _ptr(marginals),
+                                     _ptr(status), 0 if stream is None else int(stream))
+        _native.check(rc, self.ctx)
+
+    def profile(self, enable: bool = True):
+        _native.check(self.L.mps_profile(self.ctx, int(enable)), self.ctx)
+
+    def profile_read(self) -> dict:
+        buf = (ctypes.c_double * 6)()
+        _native.check(self.L.mps_profile_read(self.ctx, buf), self.ctx)
+        return dict(gemm_ms=buf[0], gemm_launches=int(buf[1]), gemm_flops=buf[2],
+                    draw_ms=buf[3], draw_launches=int(buf[4]), draw_bytes=buf[5])
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(self.L.mps_kernel_launches(self.ctx)) if self.ctx else 0
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            self.L.mps_destroy(self.ctx)
+            self.ctx = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- batch sampling ------------------------------------------------------------
+    def sample(self, config: MpsSamplerConfig, start: int = 0, stop: int | None = None, disp=None, alpha=None,
+               uniforms=None, return_marginals: bool = False):
+        """Samples start..stop-1 of the configured stream (device-resident counts,
+        one D2H at the end).  Explicit disp (N x M x D x D) / alpha (N x M) /
+        uniforms (N x M) host arrays are indexed by global sample index - start."""
+        torch = self._torch
+        stop = config.N if stop is None else stop
+        n_all = stop - start
+        M, D = self.M, self.D
+        dev = torch.device("cuda", self.device)
+        counts = torch.empty((max(n_all, 0), M), dtype=torch.int32, device=dev)
+        status = torch.zeros(max(n_all, 0), dtype=torch.uint8, device=dev)
+        marg = torch.empty((n_all, M, D), dtype=torch.float64, device=dev) if return_marginals else None
+        self.set_streams(config.seed, config.alpha_sigma)
+        B = config.batch_size or DEFAULT_BATCH
+        for s0 in range(0, n_all, B):
+            b = min(B, n_all - s0)
+            sl = slice(s0, s0 + b)
+            u = None if uniforms is None else np.ascontiguousarray(uniforms[sl], dtype=np.float64)
+            dsp = None if disp is None else np.ascontiguousarray(disp[sl], dtype=np.complex128)
+            alp = None if alpha is None else np.ascontiguousarray(alpha[sl], dtype=np.complex128)
+            self.run(start + s0, b, counts[sl], m_begin=0, m_end=M, uniforms=u, disp=dsp, alpha=alp,
+                     marginals=None if marg is None else marg[sl], status=status[sl])
+        torch.cuda.synchronize(dev)
+        out = dict(counts=counts.cpu().numpy(), status=status.cpu().numpy())
+        if marg is not None:
+            out["marginals"] = marg.cpu().numpy()
+        return out
+
+
+def batch_sample(config: MpsSamplerConfig, mps: MPS, disp=None, alpha=None, uniforms=None,
+                 sampler: MpsSampler | None = None) -> MpsSampleBatch:
+    """Generate N samples with the B200 engine (gbsemu batch_sample, sampler.py:706-761).
+
+    Failed samples (non-finite or zero step norm) are dropped and counted;
+    flagged samples (a draw within 1e-10 of a CDF boundary) are kept and counted.
+    """
+    if config.method not in METHODS:
+        raise ValidationError(f"unknown method {config.method!r}")
+    if not isinstance(mps, MPS):
+        raise ValidationError("batch_sample needs an MPS")
+    for name, arr, tail in (("disp", disp, (mps.M, mps.D, mps.D)), ("alpha", alpha, (mps.M,)),
+                            ("uniforms", uniforms, (mps.M,))):
+        if arr is not None and tuple(arr.shape) != (config.N,) + tail:
+            raise ValidationError(f"{name} must have shape {(config.N,) + tail}, got {tuple(arr.shape)}")
+    if disp is not None and alpha is not None:
+        raise ValidationError("pass disp or alpha, not both")
+    t0 = time.perf_counter()
+    own = sampler is None
+    eng = sampler or MpsSampler(mps, device=config.device)
+    try:
+        res = eng.sample(config, disp=disp, alpha=alpha, uniforms=uniforms)
+    finally:
+        if own:
+            eng.close()
+    st = res["status"]
+    failed = (st & _native.MPS_STATUS_FAILED) != 0
+    keep = ~failed
+    counts = res["counts"][keep]
+    wall = time.perf_counter() - t0
+    n_ok = int(keep.sum())
+    return MpsSampleBatch(
+        M=mps.M, N=n_ok, counts=counts, method="mps", seed=config.seed, D=mps.D, chi=mps.chi,
+        wall_time=wall, per_sample_mean=wall / max(n_ok, 1), n_failed=int(config.N - n_ok),
+        n_flagged=int(((st & _native.MPS_STATUS_FLAGGED) != 0)[keep].sum()),
+        indices=np.nonzero(keep)[0],
+    )
+
+
+def sample_one(mps: MPS, config: MpsSamplerConfig, index: int = 0, sampler: MpsSampler | None = None) -> np.ndarray:
+    """Counts of sample ``index`` of the configured stream (sampler.py:672-676)."""
+    if index < 0:
+        raise ValidationError("index must be >= 0")
+    own = sampler is None
+    eng = sampler or MpsSampler(mps, device=config.device)
+    try:
+        res = eng.sample(config, start=index, stop=index + 1)
+    finally:
+        if own:
+            eng.close()
+    if res["status"][0] & _native.MPS_STATUS_FAILED:
+        raise ValidationError("sample failed: non-finite or zero step norm")
+    return res["counts"][0]

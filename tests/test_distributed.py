@@ -1,0 +1,111 @@
+"""Multi-rank host logic over gloo on CPU (world size 2): the sample-sharded layout
+and the mode-pipelined schedule produce exactly the single-process result.  The stage
+compute is the oracle here (the schedule does not care what computes a stage); the
+native stage (mps_sample_range with state in/out) is covered in tests/test_gpu_parity.py."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+from oracle import mps_oracle as orc
+from paper_2511_14923_b200.distributed import gather_columns, gather_rows, run_pipeline, shard_range, stage_blocks
+
+M, CHI, D, N, NMICRO, SIGMA, SEED = 8, 12, 3, 96, 4, 0.5, 3
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, mode, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sites = orc.random_mps(M, CHI, D, seed=1)
+        if mode == "sharded":
+            a, b = shard_range(N, rank, world)
+            res = orc.sample_chain(sites, orc.stream_uniforms(SEED, a, b - a, M),
+                                   alpha=orc.alpha_stream(SEED, a, b - a, M, SIGMA))
+            out = gather_rows(torch.from_numpy(res["counts"]), rank, world)
+        else:
+            dims = orc.bond_dims(M, CHI, D)
+            mb, me = stage_blocks(dims, D, world)[rank]
+            n = N // NMICRO
+            counts = np.zeros((N, me - mb), dtype=np.int32)
+
+            def stage(t, x):
+                s0 = t * n
+                u = orc.stream_uniforms(SEED, s0, n, M)[:, mb:me]
+                al = orc.alpha_stream(SEED, s0, n, M, SIGMA)[:, mb:me]
+                res = orc.sample_chain(sites[mb:me], u, alpha=al, state_in=None if x is None else x.numpy(),
+                                       return_state=True)
+                counts[s0:s0 + n] = res["counts"]
+                return torch.from_numpy(res["state"])
+
+            run_pipeline(stage, NMICRO,
+                         recv_like=lambda: torch.empty(n, dims[mb], dtype=torch.complex128),
+                         send_like=lambda: torch.empty(n, dims[me], dtype=torch.complex128),
+                         rank=rank, world=world)
+            out = gather_columns(torch.from_numpy(counts), mb, M, rank, world)
+        if rank == 0:
+            q.put(out.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(mode, world=2):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = q.get(timeout=120)
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    return out
+
+
+def _single():
+    sites = orc.random_mps(M, CHI, D, seed=1)
+    return orc.sample_chain(sites, orc.stream_uniforms(SEED, 0, N, M), alpha=orc.alpha_stream(SEED, 0, N, M, SIGMA))
+
+
+def test_shard_range_partition():
+    for Ntot in (0, 1, 7, 100, 1001):
+        for world in (1, 2, 3, 8):
+            parts = [shard_range(Ntot, r, world) for r in range(world)]
+            assert parts[0][0] == 0 and parts[-1][1] == Ntot
+            assert all(parts[i][1] == parts[i + 1][0] for i in range(world - 1))
+            assert max(b - a for a, b in parts) - min(b - a for a, b in parts) <= 1
+
+
+def test_stage_blocks_balanced_and_contiguous():
+    dims = orc.bond_dims(144, 4000, 10)
+    blocks = stage_blocks(dims, 10, 8)
+    assert blocks[0][0] == 0 and blocks[-1][1] == 144
+    assert all(blocks[i][1] == blocks[i + 1][0] for i in range(7))
+    w = [sum(dims[m] * dims[m + 1] for m in range(a, b)) for a, b in blocks]
+    assert max(w) / min(w) < 1.3
+    assert stage_blocks(orc.bond_dims(4, 3, 2), 2, 4) == [(0, 1), (1, 2), (2, 3), (3, 4)]
+
+
+@pytest.mark.timeout(300)
+def test_sample_sharded_gloo_equals_single_process():
+    assert np.array_equal(_run("sharded"), _single()["counts"])
+
+
+@pytest.mark.timeout(300)
+def test_mode_pipelined_gloo_equals_single_process():
+    assert np.array_equal(_run("pipelined"), _single()["counts"])

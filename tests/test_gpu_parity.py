@@ -1,0 +1,262 @@
+"""CUDA path vs the CPU oracle (needs a B200).  Everything goes through the C ABI.
+
+Parity bar (BASELINE.json north_star): along the GPU's realised
+path (teacher-forced oracle, the pattern of sampler.py:394-416) the normalised
+marginals agree within 1e-10 absolute (they sum to 1, so this is relative to
+the marginal vector), and free-running counts are identical except for samples
+the engine flagged (a draw within 1e-10 of a CDF boundary).
+"""
+
+import ctypes
+import itertools
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from oracle import mps_oracle as orc  # noqa: E402
+from paper_2511_14923_b200 import (  # noqa: E402
+    MPS,
+    MpsSampler,
+    MpsSamplerConfig,
+    ValidationError,
+    alpha_stream,
+    batch_sample,
+    sample_one,
+    stream_uniforms,
+)
+from paper_2511_14923_b200 import _native  # noqa: E402
+
+MARG_TOL = 1e-10
+
+
+def _c(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def _check_parity(sites, res, u, alpha=None, disp=None):
+    ref_forced = orc.sample_chain(sites, u, alpha=alpha, disp=disp, forced=res["counts"], return_marginals=True)
+    err = np.abs(res["marginals"] - ref_forced["marginals"]).max()
+    assert err <= MARG_TOL, f"max |p_gpu - p_cpu| = {err}"
+    free = orc.sample_chain(sites, u, alpha=alpha, disp=disp)
+    flagged = (res["status"] & _native.MPS_STATUS_FLAGGED) != 0
+    mism = (res["counts"] != free["counts"]).any(axis=1)
+    assert not (mism & ~flagged & ~free["flagged"]).any(), "counts differ on unflagged samples"
+    return err
+
+
+# ------------------------------------------------------------------ kernels
+
+
+@pytest.mark.parametrize("n,K,N", [(1, 1, 4), (3, 2, 10), (100, 16, 40), (130, 37, 90), (128, 100, 1000),
+                                   (257, 250, 2500), (1024, 1000, 10000)])
+def test_site_gemm_vs_torch(n, K, N):
+    L = _native.lib()
+    g = torch.Generator(device="cuda").manual_seed(n * 7 + K)
+    V = torch.randn(n, K, dtype=torch.complex128, device="cuda", generator=g)
+    G = torch.randn(K, N, dtype=torch.complex128, device="cuda", generator=g)
+    C = torch.full((n, N), complex(np.nan, np.nan), dtype=torch.complex128, device="cuda")
+    assert L.mps_site_gemm(V.data_ptr(), G.data_ptr(), C.data_ptr(), n, K, N, N, 0) == 0
+    torch.cuda.synchronize()
+    ref = V @ G
+    err = (C - ref).abs().max().item()
+    scale = (V.abs().max() * G.abs().max()).item() * K
+    assert err <= 1e-14 * scale, (err, scale)
+
+
+def test_site_gemm_batch_rows_bit_identical():
+    """Row b of C does not depend on how many rows are in flight (batch invariance)."""
+    L = _native.lib()
+    g = torch.Generator(device="cuda").manual_seed(5)
+    V = torch.randn(300, 200, dtype=torch.complex128, device="cuda", generator=g)
+    G = torch.randn(200, 700, dtype=torch.complex128, device="cuda", generator=g)
+    C1 = torch.empty(300, 700, dtype=torch.complex128, device="cuda")
+    C2 = torch.empty(37, 700, dtype=torch.complex128, device="cuda")
+    assert L.mps_site_gemm(V.data_ptr(), G.data_ptr(), C1.data_ptr(), 300, 200, 700, 700, 0) == 0
+    V2 = V[150:187].contiguous()
+    assert L.mps_site_gemm(V2.data_ptr(), G.data_ptr(), C2.data_ptr(), 37, 200, 700, 700, 0) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(C1[150:187], C2)
+
+
+def test_displacement_kernel_vs_oracle():
+    L = _native.lib()
+    a = alpha_stream(4, 0, 50, 3, 0.7).reshape(-1)
+    for D in (1, 4, 10, 16):
+        out = torch.empty(len(a), D, D, dtype=torch.complex128, device="cuda")
+        assert L.mps_displacement(_c(a).data_ptr(), len(a), D, out.data_ptr(), 0) == 0
+        torch.cuda.synchronize()
+        # same operation order as the oracle; residual differences are exp() ulps and
+        # numpy's SIMD complex loops (FMA) amplified by the recurrence: 1e-13 << the 1e-10 bar
+        assert np.abs(out.cpu().numpy() - orc.displacement_matrix(a, D)).max() < 1e-13
+
+
+@pytest.mark.parametrize("seed,first,count,M", [(0, 0, 200, 8), (7, 100, 300, 16), (123456789, 63, 3, 64),
+                                                 (2**63 + 5, 1000, 130, 5), (2**64 - 1, 7, 9, 3),
+                                                 (1, 10**9, 70, 144)])
+def test_device_uniforms_bit_exact(seed, first, count, M):
+    L = _native.lib()
+    out = torch.empty(count, M, dtype=torch.float64, device="cuda")
+    assert L.mps_stream_uniforms(seed, first, count, M, out.data_ptr(), 0) == 0
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), orc.stream_uniforms(seed, first, count, M))
+
+
+# ------------------------------------------------------------------ the chain
+
+
+def test_c1_parity_alpha_host_arrays(c1_sites):
+    """BASELINE config 1: M=8, chi=16, D=4, alpha ~ CN(0, 0.25), N=1000, n=100."""
+    N, M = 1000, 8
+    u = stream_uniforms(0, 0, N, M)
+    al = alpha_stream(0, 0, N, M, 0.5)
+    cfg = MpsSamplerConfig(N=N, seed=0, batch_size=100)
+    with MpsSampler(MPS(c1_sites)) as eng:
+        res = eng.sample(cfg, uniforms=u, alpha=al, return_marginals=True)
+    _check_parity(c1_sites, res, u, alpha=al)
+
+
+def test_c1_parity_device_streams(c1_sites):
+    """uniforms and alpha generated on the device from the seed (no host arrays)."""
+    N, M = 1000, 8
+    cfg = MpsSamplerConfig(N=N, seed=0, alpha_sigma=0.5, batch_size=100)
+    with MpsSampler(MPS(c1_sites)) as eng:
+        res = eng.sample(cfg, return_marginals=True)
+    _check_parity(c1_sites, res, stream_uniforms(0, 0, N, M), alpha=alpha_stream(0, 0, N, M, 0.5))
+
+
+def test_c2_parity(c2_sites):
+    """BASELINE config 2: M=16, chi=100, D=10, alpha ~ CN(0, 0.25), n=100 (N reduced to 2000)."""
+    N, M = 2000, 16
+    cfg = MpsSamplerConfig(N=N, seed=0, alpha_sigma=0.5, batch_size=100)
+    with MpsSampler(MPS(c2_sites)) as eng:
+        res = eng.sample(cfg, return_marginals=True)
+    _check_parity(c2_sites, res, stream_uniforms(0, 0, N, M), alpha=alpha_stream(0, 0, N, M, 0.5))
+
+
+def test_explicit_disp_matrices_unitary(c1_sites):
+    N, M, D = 300, 8, 4
+    rng = np.random.default_rng(3)
+    Z = rng.standard_normal((N, M, D, D)) + 1j * rng.standard_normal((N, M, D, D))
+    disp = np.linalg.qr(Z)[0]
+    u = stream_uniforms(5, 0, N, M)
+    cfg = MpsSamplerConfig(N=N, seed=5, batch_size=64)
+    with MpsSampler(MPS(c1_sites)) as eng:
+        res = eng.sample(cfg, disp=disp, uniforms=u, return_marginals=True)
+    _check_parity(c1_sites, res, u, disp=disp)
+
+
+def test_no_displacement(c1_sites):
+    N, M = 500, 8
+    cfg = MpsSamplerConfig(N=N, seed=2, batch_size=128)
+    with MpsSampler(MPS(c1_sites)) as eng:
+        res = eng.sample(cfg, return_marginals=True)
+    _check_parity(c1_sites, res, stream_uniforms(2, 0, N, M))
+
+
+def test_chi_1000_block_parity():
+    """chi = 1000 sites (the C3 bond dimension) on a short chain: M=6, D=10."""
+    M, chi, D, N = 6, 1000, 10, 64
+    sites = orc.random_mps(M, chi, D, seed=1)
+    cfg = MpsSamplerConfig(N=N, seed=1, alpha_sigma=0.7071067811865476, batch_size=64)
+    with MpsSampler(MPS(sites)) as eng:
+        res = eng.sample(cfg, return_marginals=True)
+    _check_parity(sites, res, stream_uniforms(1, 0, N, M), alpha=alpha_stream(1, 0, N, M, 0.7071067811865476))
+
+
+def test_batch_size_invariance(c2_sites):
+    N = 700
+    outs = []
+    with MpsSampler(MPS(c2_sites)) as eng:
+        for B in (7, 64, 700):
+            outs.append(eng.sample(MpsSamplerConfig(N=N, seed=9, alpha_sigma=0.5, batch_size=B),
+                                   return_marginals=True))
+    for o in outs[1:]:
+        assert np.array_equal(o["counts"], outs[0]["counts"])
+        assert np.array_equal(o["marginals"], outs[0]["marginals"])
+
+
+def test_shard_invariance(c2_sites):
+    """Contiguous index shards (the sample-sharded multi-GPU layout) reproduce the batch."""
+    N = 600
+    cfg = MpsSamplerConfig(N=N, seed=4, alpha_sigma=0.5, batch_size=128)
+    with MpsSampler(MPS(c2_sites)) as eng:
+        full = eng.sample(cfg)["counts"]
+        parts = [eng.sample(cfg, start=s, stop=min(s + 150, N))["counts"] for s in range(0, N, 150)]
+    assert np.array_equal(np.concatenate(parts), full)
+
+
+def test_sample_one_matches_batch(c1_sites):
+    cfg = MpsSamplerConfig(N=6, seed=9, alpha_sigma=0.5)
+    mps = MPS(c1_sites)
+    b = batch_sample(cfg, mps)
+    for i in range(6):
+        assert np.array_equal(sample_one(mps, cfg, index=i), b.counts[i])
+
+
+def test_batch_sample_api(c1_sites):
+    cfg = MpsSamplerConfig(N=250, seed=1, alpha_sigma=0.5, batch_size=100)
+    b = batch_sample(cfg, MPS(c1_sites))
+    assert b.N == 250 and b.counts.shape == (250, 8) and b.n_failed == 0
+    assert b.counts.min() >= 0 and b.counts.max() <= 3
+    assert b.bitstrings.dtype == np.uint8 and np.array_equal(b.bitstrings, b.counts > 0)
+    empty = batch_sample(MpsSamplerConfig(N=0), MPS(c1_sites))
+    assert empty.N == 0 and empty.counts.shape == (0, 8)
+
+
+def test_device_resident_sites_borrowed():
+    M, chi, D = 6, 40, 5
+    sites = orc.random_mps(M, chi, D, seed=8)
+    dev = MPS([_c(s) for s in sites])
+    cfg = MpsSamplerConfig(N=200, seed=3, alpha_sigma=0.5, batch_size=200)
+    with MpsSampler(dev) as eng:
+        res = eng.sample(cfg, return_marginals=True)
+    _check_parity(sites, res, stream_uniforms(3, 0, 200, M), alpha=alpha_stream(3, 0, 200, M, 0.5))
+
+
+def test_failed_samples_dropped():
+    sites = [s.copy() for s in orc.random_mps(4, 3, 2, seed=0)]
+    sites[2][:] = 0.0
+    b = batch_sample(MpsSamplerConfig(N=10, seed=0), MPS(sites))
+    assert b.N == 0 and b.n_failed == 10
+
+
+def test_gpu_tvd_vs_born():
+    """Distribution-level check of the GPU sampler against brute-force Born probabilities."""
+    M, chi, D, N = 4, 6, 3, 200000
+    sites = orc.random_mps(M, chi, D, seed=4)
+    rng = np.random.default_rng(1)
+    ops = np.array([np.linalg.qr(rng.standard_normal((D, D)) + 1j * rng.standard_normal((D, D)))[0] for _ in range(M)])
+    born = orc.born_distribution(sites, ops).reshape(-1)
+    disp = np.broadcast_to(ops, (N, M, D, D))
+    b = batch_sample(MpsSamplerConfig(N=N, seed=11, batch_size=50000), MPS(sites), disp=disp)
+    codes = (b.counts * (D ** np.arange(M - 1, -1, -1))).sum(axis=1)
+    emp = np.bincount(codes, minlength=D**M) / N
+    assert 0.5 * np.abs(emp - born).sum() < 3 * np.sqrt(D**M / N) / 2
+
+
+def test_validation_errors(c1_sites):
+    with pytest.raises(ValidationError):
+        MpsSamplerConfig(N=-1)
+    with pytest.raises(ValidationError):
+        MpsSamplerConfig(N=1, alpha_sigma=-0.1)
+    with pytest.raises(ValidationError):
+        batch_sample(MpsSamplerConfig(N=3), MPS(c1_sites), alpha=np.zeros((2, 8), complex))
+    L = _native.lib()
+    ctx = ctypes.c_void_p()
+    assert L.mps_create(2, None, 0, ctypes.byref(ctx)) == 2
+    assert L.mps_create(1, None, 0, ctypes.byref(ctx)) == 0
+    assert L.mps_configure(ctx, 4, 17) == 2
+    assert L.mps_configure(ctx, 4, 3) == 0
+    G = np.zeros((1, 2, 3), complex)
+    assert L.mps_set_site(ctx, 5, 1, 2, 3, G.ctypes.data, 0, 0) == 2
+    assert L.mps_set_site(ctx, 0, 1, 2, 4, G.ctypes.data, 0, 0) == 2
+    counts = np.zeros((4, 4), np.int32)
+    assert L.mps_sample(ctx, 0, 4, None, None, None, counts.ctypes.data, None, None) == 2  # sites missing
+    assert b"not loaded" in L.mps_last_error(ctx)
+    L.mps_destroy(ctx)

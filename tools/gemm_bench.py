@@ -1,0 +1,47 @@
+"""K1 (site_gemm) tile-config sweep vs cuBLAS ZGEMM on the BASELINE site shapes.
+
+python tools/gemm_bench.py  ->  one JSON line per (shape, config)."""
+import json
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2511_14923_b200 import _native  # noqa: E402
+
+L = _native.lib()
+SHAPES = {"c2": (100, 100, 1000), "c3": (1024, 1000, 10000), "c4": (2048, 4000, 40000), "c3_n512": (512, 1000, 10000)}
+
+
+def timeit(fn, reps=5):
+    fn()
+    torch.cuda.synchronize()
+    best = 1e30
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        e1.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    return best
+
+
+for name in sys.argv[1:] or list(SHAPES):
+    n, K, N = SHAPES[name]
+    g = torch.Generator(device="cuda").manual_seed(0)
+    V = torch.randn(n, K, dtype=torch.complex128, device="cuda", generator=g)
+    G = torch.randn(K, N, dtype=torch.complex128, device="cuda", generator=g)
+    C = torch.empty(n, N, dtype=torch.complex128, device="cuda")
+    flops = 8.0 * n * K * N
+    ref = V @ G
+    ms = timeit(lambda: torch.matmul(V, G, out=C))
+    print(json.dumps({"shape": name, "cfg": "cublas", "ms": ms, "tflops": flops / ms / 1e9}), flush=True)
+    for cfg in (-1, 0, 1, 2, 3):
+        ms = timeit(lambda: L.mps_site_gemm_cfg(V.data_ptr(), G.data_ptr(), C.data_ptr(), n, K, N, N, 0, cfg))
+        err = ((C - ref).abs().max() / ref.abs().max()).item()
+        print(json.dumps({"shape": name, "cfg": cfg, "ms": ms, "tflops": flops / ms / 1e9, "rel_err": err}),
+              flush=True)
+    del V, G, C, ref
+    torch.cuda.empty_cache()
