@@ -123,8 +123,8 @@ int mps_sample_range(mps_ctx* ctx, int m_begin, int m_end, int64_t first_index, 
 /* Device launches issued by this context since creation (kernels only). */
 uint64_t mps_kernel_launches(const mps_ctx* ctx);
 
-/* Live per-kernel timing: when enabled, every K1/K2+K3 launch is bracketed by
- * CUDA events on its own stream.  mps_profile_read synchronises on them and
+/* Live per-kernel timing: enable is a mask (bit 0: K1 site_gemm, bit 1: K2+K3
+ * displace_draw); each selected launch is bracketed by CUDA events on its own stream.  mps_profile_read synchronises on them and
  * returns (and resets) out6 = {site_gemm ms, launches, algorithmic flops,
  * displace_draw ms, launches, algorithmic bytes}. */
 int mps_profile(mps_ctx* ctx, int enable);
@@ -136,15 +136,20 @@ void mps_destroy(mps_ctx* ctx);
 /* Kernel-level entry points, exposed for unit tests and the bench roofline.
  * All pointers are device pointers; stream 0 = legacy default stream. */
 
-/* C (n x N complex, row stride ldc) = V (n x K complex, row stride K) . G (K x N complex) */
+/* C (n x N complex, row stride ldc) = V (n x K complex, row stride K) . G (K x N complex);
+ * 3M, autotuned tile config. */
 int mps_site_gemm(const void* V, const void* G, void* C, int n, int K, int N,
                   int64_t ldc, uint64_t stream);
-/* Same with an explicit K1 tile config (-1 auto, 0 128x128, 1 64x128 8 warps,
- * 2 64x128 4 warps x 2 CTAs/SM, 3 32x64); every config gives bit-identical C. */
+/* Same with an explicit K1 tile config (-1 autotune, cached per shape; -2 analytic
+ * model; 0..3 fixed tiles) and product mode (3: 3M, three real GEMMs; 4: 4M
+ * real-doubled).  Within a mode every config gives bit-identical C. */
 int mps_site_gemm_cfg(const void* V, const void* G, void* C, int n, int K, int N,
-                      int64_t ldc, uint64_t stream, int cfg);
-/* Pin the K1 tile config of a context (-1 = auto). */
+                      int64_t ldc, uint64_t stream, int cfg, int mode);
+/* Pin the K1 tile config of a context (-1 = autotune, the default; -2 = model). */
 int mps_set_gemm_config(mps_ctx* ctx, int cfg);
+/* K1 complex product: 3 = 3M (default), 4 = 4M.  Results of the two modes differ at
+ * rounding level; each is deterministic across batch sizes and GPU counts. */
+int mps_set_gemm_mode(mps_ctx* ctx, int mode);
 /* D x D truncated displacement matrices for `count` alphas: out[count][D][D] */
 int mps_displacement(const void* alpha, int count, int D, void* out, uint64_t stream);
 /* Uniforms of samples first..first+count-1 (count x M float64), bit-equal to

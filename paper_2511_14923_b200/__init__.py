@@ -5,7 +5,7 @@ sampler config / batch / entry points, the MPS container and the counter streams
 """
 
 from .errors import GbsError, NumericalError, ResourceGuardError, ValidationError
-from .mps import MPS, bond_dims, device_site, host_site
+from .mps import MPS, SiteShape, bond_dims, device_site, host_site
 from .sampler import (
     METHODS,
     MpsSampleBatch,

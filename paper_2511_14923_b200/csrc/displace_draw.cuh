@@ -9,13 +9,16 @@
 // batch size / grid.  Thread 0 draws k against u[b][m] with the sampler.py:692-697
 // rule.  Pass 2 re-reads C[b] and writes v'[j] = E[j][k] / sqrt(p[k]) — the
 // recomputation costs D MACs per j and saves storing E (16 n chi D bytes).
+
 #pragma once
 #include <cstdint>
+
+#include "ptx.cuh"
 
 namespace mps {
 
 constexpr int DMAX = 16;
-constexpr int DRAW_THREADS = 256;
+constexpr int DRAW_THREADS = 128;
 constexpr double TIE_EPS = 1e-10;
 constexpr uint8_t ST_FAILED = 1;
 constexpr uint8_t ST_FLAGGED = 2;
@@ -87,6 +90,10 @@ __device__ inline double2 stream_alpha(uint64_t seed, unsigned long long i, int 
   return make_double2(rad * cs, rad * sn);
 }
 
+// sqrt(k) and 1/sqrt(k) (correctly rounded, as Python's math.sqrt and 1.0/x give them)
+__constant__ double c_sqrt[17] = {0.0, 1.0, 1.4142135623730951, 1.7320508075688772, 2.0, 2.23606797749979, 2.449489742783178, 2.6457513110645907, 2.8284271247461903, 3.0, 3.1622776601683795, 3.3166247903554, 3.4641016151377544, 3.605551275463989, 3.7416573867739413, 3.872983346207417, 4.0};
+__constant__ double c_rsqrt[17] = {0.0, 1.0, 0.7071067811865475, 0.5773502691896258, 0.5, 0.4472135954999579, 0.4082482904638631, 0.3779644730092272, 0.35355339059327373, 0.3333333333333333, 0.31622776601683794, 0.30151134457776363, 0.2886751345948129, 0.2773500981126146, 0.2672612419124244, 0.2581988897471611, 0.25};
+
 // Exact truncated <k|D(alpha)|d> (oracle decision 6), row-major T[k*D + d].  The
 // operation order mirrors the oracle's numpy expressions with explicit _rn
 // intrinsics (no FMA contraction), so host and device agree to the last bit except
@@ -103,17 +110,17 @@ __device__ inline void displacement_column0(double2 a, int D, double2* T) {
   T[0] = make_double2(e, 0.0);
   for (int k = 1; k < D; ++k) {
     const double2 v = cmul_rn(T[(k - 1) * D], a);
-    const double scl = __ddiv_rn(1.0, sqrt((double)k));
+    const double scl = c_rsqrt[k];
     T[k * D] = make_double2(__dmul_rn(v.x, scl), __dmul_rn(v.y, scl));
   }
 }
 
 __device__ inline double2 displacement_entry(double2 a, int D, const double2* T, int k, int d) {
   // T[k,d] = (sqrt(k) T[k-1,d-1] - conj(a) T[k,d-1]) * (1/sqrt(d));  row 0: (-conj(a) T[0,d-1]) * inv
-  const double inv = __ddiv_rn(1.0, sqrt((double)d));
+  const double inv = c_rsqrt[d];
   const double2 t2 = cmul_rn(make_double2(a.x, -a.y), T[k * D + d - 1]);
   if (k == 0) return make_double2(__dmul_rn(-t2.x, inv), __dmul_rn(-t2.y, inv));
-  const double sk = sqrt((double)k);
+  const double sk = c_sqrt[k];
   const double2 t1 = T[(k - 1) * D + d - 1];
   return make_double2(__dmul_rn(__dsub_rn(__dmul_rn(sk, t1.x), t2.x), inv),
                       __dmul_rn(__dsub_rn(__dmul_rn(sk, t1.y), t2.y), inv));
@@ -147,141 +154,149 @@ struct DrawArgs {
   uint8_t* status;          // n
 };
 
-__global__ void __launch_bounds__(DRAW_THREADS)
+// Broadcast read of a D(alpha) entry.  volatile: keeps ptxas from hoisting all D^2
+// loop-invariant entries into registers across the j loop (which spills 2 KB).
+__device__ __forceinline__ double2 lds_c128(const double2* p) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(smem_u32(p)));
+  return v;
+}
+
+// E[k] = sum_d T[k][d] c[d] for one j (T in shared memory, broadcast reads)
+template <int DT>
+__device__ __forceinline__ double2 disp_row(const double2* T, int D, int k, const double2* c) {
+  double2 e = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int d = 0; d < (DT ? DT : DMAX); ++d) {
+    if (!DT && d >= D) break;
+    const double2 tk = lds_c128(&T[k * D + d]);
+    e.x = fma(tk.x, c[d].x, e.x);
+    e.x = fma(-tk.y, c[d].y, e.x);
+    e.y = fma(tk.x, c[d].y, e.y);
+    e.y = fma(tk.y, c[d].x, e.y);
+  }
+  return e;
+}
+
+// One CTA of DRAW_THREADS per sample; DT = compile-time D (0: runtime D <= DMAX).
+// Pass 1 reads C[b] with 16-B loads (L1-resident per thread), pass 2 re-reads it
+// (L2 hits: the row was touched microseconds earlier).  128 threads and <= 128 regs
+// keep 4 CTAs per SM so one CTA's serial sections (D(alpha), the draw) hide behind
+// the others' streaming.
+template <int DT>
+__global__ void __launch_bounds__(DRAW_THREADS, 4)
     displace_draw_kernel(DrawArgs A) {
   __shared__ double2 T[DMAX * DMAX];
   __shared__ double red[DRAW_THREADS / 32][DMAX];
   __shared__ double p_s[DMAX];
   __shared__ int k_s;
   __shared__ double scale_s;
-  __shared__ int mode_s;  // 0 identity, 1 matrix
 
   const int b = blockIdx.x;
   const int tid = threadIdx.x;
-  const int D = A.D;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int D = DT ? DT : A.D;
   const unsigned long long gi = (unsigned long long)(A.first_index + b);
+  const long long crow = (long long)b * A.ld_c + A.m;
 
-  const bool dead = (A.status[b] & ST_FAILED) != 0;
-  if (dead) {  // keep the chain deterministic: zero state, count -1
+  if (A.status[b] & ST_FAILED) {  // dead sample: zero state, count -1 (deterministic chain)
     for (int j = tid; j < A.chi_r; j += DRAW_THREADS) A.v_out[(long long)b * A.chi_r + j] = make_double2(0.0, 0.0);
-    if (tid == 0) A.counts[(long long)b * A.ld_c + A.m] = -1;
-    if (A.marg && tid < D) A.marg[((long long)b * A.ld_c + A.m) * D + tid] = 0.0;
+    if (tid == 0) A.counts[crow] = -1;
+    if (A.marg && tid < D) A.marg[crow * D + tid] = 0.0;
     return;
   }
+  const double2* Cb = A.C + (long long)b * A.ldc;
 
-  // ---- displacement matrix for (b, m) ----
+  // ---- displacement matrix for (b, m): warp 0 only, column by column ----
+  const bool ident = !(A.disp || A.alpha || A.alpha_sigma >= 0.0);
   if (A.disp) {
     const double2* src = A.disp + ((long long)b * A.M + A.m) * D * D;
     for (int e = tid; e < D * D; e += DRAW_THREADS) T[e] = src[e];
-    if (tid == 0) mode_s = 1;
-  } else if (A.alpha || A.alpha_sigma >= 0.0) {
-    double2 a;
-    if (A.alpha) a = A.alpha[(long long)b * A.M + A.m];
-    else a = stream_alpha(A.seed, gi, A.M, A.m, A.alpha_sigma);
-    if (tid == 0) { displacement_column0(a, D, T); mode_s = 1; }
-    __syncthreads();
-    for (int d = 1; d < D; ++d) {
-      double2 v;
-      if (tid < D) v = displacement_entry(a, D, T, tid, d);
-      __syncthreads();
-      if (tid < D) T[tid * D + d] = v;
-      __syncthreads();
+  } else if (!ident && warp == 0) {
+    const double2 a = A.alpha ? A.alpha[(long long)b * A.M + A.m] : stream_alpha(A.seed, gi, A.M, A.m, A.alpha_sigma);
+    if (lane == 0) displacement_column0(a, D, T);
+    __syncwarp();
+    for (int d = 1; d < D; ++d) {  // column d from column d-1: no intra-step hazard
+      if (lane < D) T[lane * D + d] = displacement_entry(a, D, T, lane, d);
+      __syncwarp();
     }
-  } else {
-    if (tid == 0) mode_s = 0;
   }
   __syncthreads();
-  const bool ident = (mode_s == 0);
 
   // ---- pass 1: partial marginals ----
-  double acc[DMAX];
+  constexpr int DR = DT ? DT : DMAX;
+  double acc[DR];
 #pragma unroll
-  for (int k = 0; k < DMAX; ++k) acc[k] = 0.0;
-  const double2* Cb = A.C + (long long)b * A.ldc;
+  for (int k = 0; k < DR; ++k) acc[k] = 0.0;
   for (int j = tid; j < A.chi_r; j += DRAW_THREADS) {
-    double2 c[DMAX];
+    double2 c[DR];
 #pragma unroll
-    for (int d = 0; d < DMAX; ++d)
-      if (d < D) c[d] = Cb[(long long)j * D + d];
+    for (int d = 0; d < DR; ++d)
+      if (DT || d < D) c[d] = Cb[(long long)j * D + d];
 #pragma unroll
-    for (int k = 0; k < DMAX; ++k) {
-      if (k >= D) break;
-      double2 e;
-      if (ident) {
-        e = c[k];
-      } else {
-        e = make_double2(0.0, 0.0);
-#pragma unroll
-        for (int d = 0; d < DMAX; ++d) {
-          if (d >= D) break;
-          double2 tk = T[k * D + d];
-          e.x = fma(tk.x, c[d].x, e.x);
-          e.x = fma(-tk.y, c[d].y, e.x);
-          e.y = fma(tk.x, c[d].y, e.y);
-          e.y = fma(tk.y, c[d].x, e.y);
-        }
-      }
+    for (int k = 0; k < DR; ++k) {
+      if (!DT && k >= D) break;
+      const double2 e = ident ? c[k] : disp_row<DT>(T, D, k, c);
       acc[k] = fma(e.x, e.x, fma(e.y, e.y, acc[k]));
     }
   }
-  const int lane = tid & 31, warp = tid >> 5;
 #pragma unroll
-  for (int k = 0; k < DMAX; ++k) {
-    if (k >= D) break;
+  for (int k = 0; k < DR; ++k) {
+    if (!DT && k >= D) break;
     double v = acc[k];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     if (lane == 0) red[warp][k] = v;
   }
   __syncthreads();
+  if (tid < D) {  // fixed order over warps
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < DRAW_THREADS / 32; ++w) s += red[w][tid];
+    p_s[tid] = s;
+  }
+  __syncthreads();
 
   // ---- draw (sampler.py:692-697 rule on the normalised cdf) ----
   if (tid == 0) {
-    double p[DMAX];
     double P = 0.0;
-    for (int k = 0; k < D; ++k) {
-      double s = 0.0;
-      for (int w = 0; w < DRAW_THREADS / 32; ++w) s += red[w][k];
-      p[k] = s;
-      p_s[k] = s;
-      P += s;
-    }
+    for (int k = 0; k < D; ++k) P += p_s[k];
     uint8_t st = A.status[b];
-    int ksel = 0;
+    int ksel = -1;
     if (!(P > 0.0) || !isfinite(P)) {
       st |= ST_FAILED;
-      ksel = -1;
     } else {
       const double u = A.u ? A.u[(long long)b * A.ld_u + A.m]
                            : philox_double(numpy_key0(A.seed), gi / 64, (gi % 64) * (uint64_t)A.M + A.m);
-      double run = 0.0;
+      double run = 0.0, mind = 1e300;
       int cnt = 0;
-      double mind = 1e300;
       for (int k = 0; k < D; ++k) {
-        run += p[k];
-        double cdf = (k == D - 1) ? 1.0 : run / P;
-        if (cdf <= u) ++cnt;
+        run += p_s[k];
+        const double cdf = (k == D - 1) ? 1.0 : run / P;
+        cnt += (cdf <= u);
         if (k < D - 1) mind = fmin(mind, fabs(cdf - u));
       }
       ksel = cnt < D - 1 ? cnt : D - 1;
-      while (ksel > 0 && !(p[ksel] > 0.0)) --ksel;
+      while (ksel > 0 && !(p_s[ksel] > 0.0)) --ksel;
       if (mind <= TIE_EPS) st |= ST_FLAGGED;
-      if (A.marg)
-        for (int k = 0; k < D; ++k) A.marg[((long long)b * A.ld_c + A.m) * D + k] = p[k] / P;
     }
     A.status[b] = st;
-    A.counts[(long long)b * A.ld_c + A.m] = ksel;
+    A.counts[crow] = ksel;
     k_s = ksel;
-    scale_s = (ksel >= 0) ? 1.0 / sqrt(p[ksel]) : 0.0;
+    scale_s = (ksel >= 0) ? 1.0 / sqrt(p_s[ksel]) : 0.0;
+    red[0][0] = P;  // red[] is free again: its reads finished before the last barrier
   }
   __syncthreads();
   const int ks = k_s;
   const double scale = scale_s;
+  if (A.marg && tid < D) {
+    const double P = red[0][0];
+    A.marg[crow * D + tid] = (ks >= 0) ? p_s[tid] / P : 0.0;
+  }
 
   // ---- pass 2: gather + renormalise ----
   double2* vb = A.v_out + (long long)b * A.chi_r;
   if (ks < 0) {
-    if (A.marg && tid < D) A.marg[((long long)b * A.ld_c + A.m) * D + tid] = 0.0;
     for (int j = tid; j < A.chi_r; j += DRAW_THREADS) vb[j] = make_double2(0.0, 0.0);
     return;
   }
@@ -292,10 +307,10 @@ __global__ void __launch_bounds__(DRAW_THREADS)
     } else {
       e = make_double2(0.0, 0.0);
 #pragma unroll
-      for (int d = 0; d < DMAX; ++d) {
-        if (d >= D) break;
-        double2 c = Cb[(long long)j * D + d];
-        double2 tk = T[ks * D + d];
+      for (int d = 0; d < DR; ++d) {
+        if (!DT && d >= D) break;
+        const double2 c = Cb[(long long)j * D + d];
+        const double2 tk = lds_c128(&T[ks * D + d]);
         e.x = fma(tk.x, c.x, e.x);
         e.x = fma(-tk.y, c.y, e.x);
         e.y = fma(tk.x, c.y, e.y);

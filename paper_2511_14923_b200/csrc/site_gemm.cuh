@@ -42,7 +42,8 @@ struct GemmCfgT {
   static constexpr int THREADS = WARPS * 32;
   static constexpr int MIN_BLOCKS = MIN_BLOCKS_;
   static constexpr int WM = BM / WARPS_M, WN = BN_R / WARPS_N;  // warp tile (real)
-  static constexpr int MF = WM / 8, NF = WN / 8;                // DMMA 8x8 fragments per warp
+  static constexpr int MF = WM / 8, NF = WN / 8;                // DMMA 8x8 fragments per warp (4M)
+  static constexpr int NF3 = WN / 16;                           // 8-complex-column fragments (3M)
   static constexpr int A_BYTES = BM * 16 * 8;
   static constexpr int B_GROUPS = BN_R / 16;
   static constexpr int B_BYTES = B_GROUPS * BK_C * 128;
@@ -147,6 +148,125 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     for (int nf = 0; nf < Cfg::NF; ++nf) {
       const int col = (n0r >> 1) + warp_n * (Cfg::WN / 2) + nf * 4 + t;
       if (col < N) crow[col] = make_double2(acc[mf][nf][0], acc[mf][nf][1]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// 3M variant: three real GEMMs instead of four (Gauss / Karatsuba):
+//   T1 = Vr.Gr,  T2 = Vi.Gi,  T3 = (Vr+Vi).(Gr+Gi);   Re C = T1 - T2,  Im C = T3 - (T1 + T2)
+// 25% fewer DMMAs for the same algorithmic (8 flops per complex MAC) work.  Same TMA
+// tiles as 4M; the MMA k index is the complex index, each lane reads (re, im) pairs
+// with one LDS.128 (k of lane t at step s is i = 2t + s: conflict-free against the
+// 128B swizzle for both operands) and forms the sums with one DADD per operand.
+// All 3M configs share this k order, so 3M results are bit-identical across configs,
+// batch sizes and GPU counts (they differ from 4M at rounding level).
+// ---------------------------------------------------------------------------------------
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
+    site_gemm3m_kernel(const __grid_constant__ CUtensorMap tmap_v, const __grid_constant__ CUtensorMap tmap_g,
+                       double2* __restrict__ C, int n, int N, int KT, long long ldc) {
+  static_assert(Cfg::NF3 >= 1 && Cfg::WN % 16 == 0, "3M warp tile needs whole 8-complex fragments");
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint64_t* empty = full + Cfg::STAGES;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * Cfg::BM;
+  const int n0r = blockIdx.y * Cfg::BN_R;
+
+  auto issue = [&](int kt) {
+    const int s = kt % Cfg::STAGES;
+    uint8_t* As = smem + s * Cfg::STAGE_BYTES;
+    uint8_t* Bs = As + Cfg::A_BYTES;
+    mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
+    tma_load_2d(As, &tmap_v, kt * 16, m0, &full[s]);
+#pragma unroll
+    for (int gi = 0; gi < Cfg::B_GROUPS; ++gi)
+      tma_load_2d(Bs + gi * (Cfg::BK_C * 128), &tmap_g, n0r + gi * 16, kt * Cfg::BK_C, &full[s]);
+  };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < Cfg::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], Cfg::WARPS);
+    }
+    fence_barrier_init();
+    prefetch_tmap(&tmap_v);
+    prefetch_tmap(&tmap_g);
+    for (int kt = 0; kt < Cfg::STAGES && kt < KT; ++kt) issue(kt);
+  }
+  __syncthreads();
+
+  const int g = lane >> 2;
+  const int t = lane & 3;
+  const int warp_m = warp % Cfg::WARPS_M;
+  const int warp_n = warp / Cfg::WARPS_M;
+  constexpr int MF = Cfg::MF, NF = Cfg::NF3;
+
+  double t1[MF][NF][2], t2[MF][NF][2], t3[MF][NF][2];
+#pragma unroll
+  for (int i = 0; i < MF; ++i)
+#pragma unroll
+    for (int j = 0; j < NF; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) t1[i][j][e] = t2[i][j][e] = t3[i][j][e] = 0.0;
+
+  for (int kt = 0; kt < KT; ++kt) {
+    const int s = kt % Cfg::STAGES;
+    mbar_wait(&full[s], (kt / Cfg::STAGES) & 1);
+    const uint8_t* As = smem + s * Cfg::STAGE_BYTES + (warp_m * Cfg::WM + g) * 128;
+    const uint8_t* Bs = smem + s * Cfg::STAGE_BYTES + Cfg::A_BYTES + warp_n * NF * (Cfg::BK_C * 128);
+#pragma unroll
+    for (int step = 0; step < 2; ++step) {
+      const int i = 2 * t + step;  // complex k of this lane: row of the Gamma box, chunk of the V row
+      double ar[MF], ai[MF], as[MF], br[NF], bi[NF], bs[NF];
+#pragma unroll
+      for (int mf = 0; mf < MF; ++mf) {
+        const double2 v = *reinterpret_cast<const double2*>(As + mf * 8 * 128 + ((i ^ g) << 4));
+        ar[mf] = v.x;
+        ai[mf] = v.y;
+        as[mf] = v.x + v.y;
+      }
+#pragma unroll
+      for (int nf = 0; nf < NF; ++nf) {
+        const double2 w = *reinterpret_cast<const double2*>(Bs + nf * (Cfg::BK_C * 128) + i * 128 + ((g ^ i) << 4));
+        br[nf] = w.x;
+        bi[nf] = w.y;
+        bs[nf] = w.x + w.y;
+      }
+#pragma unroll
+      for (int mf = 0; mf < MF; ++mf)
+#pragma unroll
+        for (int nf = 0; nf < NF; ++nf) {
+          dmma_8x8x4(t1[mf][nf][0], t1[mf][nf][1], ar[mf], br[nf]);
+          dmma_8x8x4(t2[mf][nf][0], t2[mf][nf][1], ai[mf], bi[nf]);
+          dmma_8x8x4(t3[mf][nf][0], t3[mf][nf][1], as[mf], bs[nf]);
+        }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (threadIdx.x == 0 && kt >= 1 && kt - 1 + Cfg::STAGES < KT) {
+      mbar_wait(&empty[(kt - 1) % Cfg::STAGES], ((kt - 1) / Cfg::STAGES) & 1);
+      issue(kt - 1 + Cfg::STAGES);
+    }
+  }
+
+  // epilogue: lane holds complex columns 2t, 2t+1 of row g in each fragment
+#pragma unroll
+  for (int mf = 0; mf < MF; ++mf) {
+    const int row = m0 + warp_m * Cfg::WM + mf * 8 + g;
+    if (row >= n) continue;
+    double2* crow = C + (long long)row * ldc;
+#pragma unroll
+    for (int nf = 0; nf < NF; ++nf) {
+      const int col = (n0r >> 1) + warp_n * (Cfg::WN / 2) + nf * 8 + 2 * t;
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        if (col + e < N)
+          crow[col + e] = make_double2(t1[mf][nf][e] - t2[mf][nf][e], t3[mf][nf][e] - (t1[mf][nf][e] + t2[mf][nf][e]));
     }
   }
 }

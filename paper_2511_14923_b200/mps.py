@@ -66,6 +66,14 @@ def device_site(seed: int, m: int, chi_l: int, chi_r: int, D: int, device="cuda"
     return out
 
 
+@dataclass(frozen=True)
+class SiteShape:
+    """Shape-only stand-in for a site held by another rank (mode-pipelined layout)."""
+
+    shape: tuple
+    dtype: str = "complex128"
+
+
 @dataclass
 class MPS:
     """Ordered site tensors (numpy arrays or CUDA torch tensors, complex128)."""
@@ -113,9 +121,21 @@ class MPS:
     def nbytes(self) -> int:
         return sum(int(np.prod(G.shape)) * 16 for G in self.sites)
 
+    def holds(self, m: int) -> bool:
+        return not isinstance(self.sites[m], SiteShape)
+
     @classmethod
-    def random(cls, M: int, chi: int, D: int, seed: int = 0, device: str = "cpu") -> "MPS":
+    def random(cls, M: int, chi: int, D: int, seed: int = 0, device: str = "cpu", block=None) -> "MPS":
+        """Random row-orthonormal MPS; ``block=(m_begin, m_end)`` materialises only those
+        sites (the rest are :class:`SiteShape` placeholders), for a pipeline stage."""
         dims = bond_dims(M, chi, D)
-        if device == "cpu":
-            return cls([host_site(seed, m, dims[m], dims[m + 1], D) for m in range(M)])
-        return cls([device_site(seed, m, dims[m], dims[m + 1], D, device) for m in range(M)])
+        lo, hi = block if block is not None else (0, M)
+        sites = []
+        for m in range(M):
+            if not lo <= m < hi:
+                sites.append(SiteShape((dims[m], dims[m + 1], D)))
+            elif device == "cpu":
+                sites.append(host_site(seed, m, dims[m], dims[m + 1], D))
+            else:
+                sites.append(device_site(seed, m, dims[m], dims[m + 1], D, device))
+        return cls(sites)

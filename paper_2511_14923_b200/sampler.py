@@ -124,6 +124,8 @@ class MpsSampler:
             _native.check(self.L.mps_configure(self.ctx, self.M, self.D), self.ctx)
             self._keep = []
             for m in range(*self.sites_range):
+                if not mps.holds(m):
+                    raise ValidationError(f"site {m} is in this context's range but not materialised")
                 G = mps.sites[m]
                 if isinstance(G, np.ndarray):
                     G = np.ascontiguousarray(G, dtype=np.complex128)
@@ -160,8 +162,9 @@ class MpsSampler:
                                      _ptr(status), 0 if stream is None else int(stream))
         _native.check(rc, self.ctx)
 
-    def profile(self, enable: bool = True):
-        _native.check(self.L.mps_profile(self.ctx, int(enable)), self.ctx)
+    def profile(self, mask: int = 3):
+        """Time kernel launches live with CUDA events (mask bit 0: K1, bit 1: K2+K3)."""
+        _native.check(self.L.mps_profile(self.ctx, int(mask)), self.ctx)
 
     def profile_read(self) -> dict:
         buf = (ctypes.c_double * 6)()
