@@ -147,6 +147,11 @@ int mps_site_gemm_cfg(const void* V, const void* G, void* C, int n, int K, int N
                       int64_t ldc, uint64_t stream, int cfg, int mode);
 /* Pin the K1 tile config of a context (-1 = autotune, the default; -2 = model). */
 int mps_set_gemm_config(mps_ctx* ctx, int cfg);
+/* Concurrent chains per call (1..4, default 2): the micro-batch is split into contiguous
+ * row blocks of >= 64 samples, each run on its own stream (forked from and joined back
+ * to the caller's stream) so one block's draw kernels and GEMM tails overlap another's
+ * GEMMs.  Per-sample results are identical for any lane count. */
+int mps_set_lanes(mps_ctx* ctx, int lanes);
 /* K1 complex product: 3 = 3M (default), 4 = 4M.  Results of the two modes differ at
  * rounding level; each is deterministic across batch sizes and GPU counts. */
 int mps_set_gemm_mode(mps_ctx* ctx, int mode);

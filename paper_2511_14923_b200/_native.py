@@ -18,7 +18,7 @@ LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
 EXPORTS = (
     "mps_create", "mps_configure", "mps_set_site", "mps_set_streams", "mps_sample",
     "mps_sample_range", "mps_kernel_launches", "mps_profile", "mps_profile_read", "mps_last_error", "mps_destroy",
-    "mps_site_gemm", "mps_site_gemm_cfg", "mps_set_gemm_config", "mps_set_gemm_mode", "mps_displacement", "mps_stream_uniforms",
+    "mps_site_gemm", "mps_site_gemm_cfg", "mps_set_gemm_config", "mps_set_gemm_mode", "mps_set_lanes", "mps_displacement", "mps_stream_uniforms",
 )
 
 MPS_SITE_HOST, MPS_SITE_DEVICE_COPY, MPS_SITE_DEVICE_BORROW = 0, 1, 2
@@ -51,6 +51,7 @@ def _declare(L):
     L.mps_site_gemm.argtypes = [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int64, c_uint64]
     L.mps_site_gemm_cfg.argtypes = [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int64, c_uint64, c_int, c_int]
     L.mps_set_gemm_mode.argtypes = [c_void_p, c_int]
+    L.mps_set_lanes.argtypes = [c_void_p, c_int]
     L.mps_set_gemm_config.argtypes = [c_void_p, c_int]
     L.mps_displacement.argtypes = [c_void_p, c_int, c_int, c_void_p, c_uint64]
     L.mps_stream_uniforms.argtypes = [c_uint64, c_int64, c_int, c_int, c_void_p, c_uint64]
@@ -59,7 +60,7 @@ def _declare(L):
         if fn.restype is ctypes.c_int or name in ("mps_create", "mps_configure", "mps_set_site",
                                                   "mps_set_streams", "mps_sample", "mps_sample_range",
                                                   "mps_profile", "mps_profile_read", "mps_site_gemm_cfg",
-                                                  "mps_set_gemm_config", "mps_set_gemm_mode",
+                                                  "mps_set_gemm_config", "mps_set_gemm_mode", "mps_set_lanes",
                                                   "mps_site_gemm", "mps_displacement", "mps_stream_uniforms"):
             fn.restype = c_int
 

@@ -199,15 +199,11 @@ __global__ void __launch_bounds__(DRAW_THREADS, 4)
   const unsigned long long gi = (unsigned long long)(A.first_index + b);
   const long long crow = (long long)b * A.ld_c + A.m;
 
-  if (A.status[b] & ST_FAILED) {  // dead sample: zero state, count -1 (deterministic chain)
-    for (int j = tid; j < A.chi_r; j += DRAW_THREADS) A.v_out[(long long)b * A.chi_r + j] = make_double2(0.0, 0.0);
-    if (tid == 0) A.counts[crow] = -1;
-    if (A.marg && tid < D) A.marg[crow * D + tid] = 0.0;
-    return;
-  }
   const double2* Cb = A.C + (long long)b * A.ldc;
 
-  // ---- displacement matrix for (b, m): warp 0 only, column by column ----
+  // ---- displacement matrix for (b, m): inputs only, so it runs before the PDL wait and
+  //      overlaps the tail of the site GEMM that produces C ----
+  griddep_launch_dependents();
   const bool ident = !(A.disp || A.alpha || A.alpha_sigma >= 0.0);
   if (A.disp) {
     const double2* src = A.disp + ((long long)b * A.M + A.m) * D * D;
@@ -221,7 +217,15 @@ __global__ void __launch_bounds__(DRAW_THREADS, 4)
       __syncwarp();
     }
   }
+  griddep_wait();  // the GEMM (and transitively the previous draw) is complete: C, status valid
   __syncthreads();
+
+  if (A.status[b] & ST_FAILED) {  // dead sample: zero state, count -1 (deterministic chain)
+    for (int j = tid; j < A.chi_r; j += DRAW_THREADS) A.v_out[(long long)b * A.chi_r + j] = make_double2(0.0, 0.0);
+    if (tid == 0) A.counts[crow] = -1;
+    if (A.marg && tid < D) A.marg[crow * D + tid] = 0.0;
+    return;
+  }
 
   // ---- pass 1: partial marginals ----
   constexpr int DR = DT ? DT : DMAX;

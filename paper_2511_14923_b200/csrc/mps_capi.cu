@@ -9,6 +9,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdarg>
+#include <cstdlib>
+#include <utility>
 #include <cstdio>
 #include <algorithm>
 #include <cmath>
@@ -110,8 +112,16 @@ struct mps_ctx {
   int gemm_mode = 3;   // 3: 3M (default, 25% fewer DMMAs), 4: 4M real-doubled
   uint64_t launches = 0;
   std::string err;
+  // lanes: the micro-batch is split into up to MAX_LANES contiguous row blocks, each run
+  // as its own chain on its own stream, so one lane's draw kernel and GEMM tail overlap
+  // the other lane's GEMM (per-sample results do not depend on the split)
+  static constexpr int MAX_LANES = 4;
+  int lanes = 2;
+  cudaStream_t lane_st[MAX_LANES] = {};
+  cudaEvent_t fork_ev = nullptr, join_ev[MAX_LANES] = {};
+  DevBuf<double2> lv0[MAX_LANES], lv1[MAX_LANES], lcbuf[MAX_LANES];
   // workspaces
-  DevBuf<double2> v0, v1, cbuf, ones, alpha_d, disp_d;
+  DevBuf<double2> ones, alpha_d, disp_d;
   DevBuf<double> u_d, marg_d;
   DevBuf<int32_t> counts_d;
   DevBuf<uint8_t> status_d;
@@ -158,6 +168,34 @@ static int cuda_fail(mps_ctx* c, cudaError_t e, const char* what) {
     if (e_ != cudaSuccess) return cuda_fail(c, e_, what); \
   } while (0)
 
+// Programmatic dependent launch: each chain kernel may start while its predecessor in the
+// stream drains (its prologue overlaps the predecessor's tail wave); the kernels call
+// griddepcontrol.wait before touching dependent data.  MPS_NO_PDL=1 disables it.
+static bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MPS_NO_PDL");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // K1 tile configurations, one list per product mode.  Within a mode all configs share
 // BK_C = 8 and the same k-step order, so the per-element summation order (and hence
 // every bit of C) is config-independent; the autotuner only changes speed.
@@ -177,8 +215,7 @@ static cudaError_t launch_cfg(const CUtensorMap& tv, const CUtensorMap& tg, doub
   }
   dim3 grid((n + Cfg::BM - 1) / Cfg::BM, (2 * N + Cfg::BN_R - 1) / Cfg::BN_R);
   int KT = (K + Cfg::BK_C - 1) / Cfg::BK_C;
-  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(tv, tg, C, n, N, KT, ldc);
-  return cudaGetLastError();
+  return launch_pdl(kern, grid, dim3(Cfg::THREADS), Cfg::SMEM_BYTES, st, tv, tg, C, n, N, KT, ldc);
 }
 
 typedef cudaError_t (*LaunchFn)(const CUtensorMap&, const CUtensorMap&, double2*, int, int, int, long long,
@@ -201,14 +238,16 @@ using G16x32 = GemmCfgT<16, 32, 1, 1, 4, 8>;
 using G128x64 = GemmCfgT<128, 64, 4, 2, 6, 1>;
 using G64x64 = GemmCfgT<64, 64, 2, 2, 4, 3>;
 using G32x128 = GemmCfgT<32, 128, 1, 4, 4, 2>;
+using G64x80 = GemmCfgT<64, 80, 4, 1, 4, 3>;  // 40 complex columns: whole D=10 groups, 4000 tiles at C3
 static const GemmCfgInfo kGemm4[] = {
     cfg_info<G128x128, 4>("4m_128x128_w4x2"), cfg_info<G64x128, 4>("4m_64x128_w2x4"),
     cfg_info<G64x128p, 4>("4m_64x128_w2x2_occ2"), cfg_info<G32x64, 4>("4m_32x64_w1x2_occ4"),
-    cfg_info<G16x32, 4>("4m_16x32_w1x1_occ8")};
+    cfg_info<G16x32, 4>("4m_16x32_w1x1_occ8"), cfg_info<G64x80, 4>("4m_64x80_w4x1_occ3")};
 static const GemmCfgInfo kGemm3[] = {
     cfg_info<G128x64, 3>("3m_128x64_w4x2"), cfg_info<G64x128, 3>("3m_64x128_w2x4"),
     cfg_info<G64x64, 3>("3m_64x64_w2x2_occ3"), cfg_info<G32x64, 3>("3m_32x64_w1x2_occ4"),
-    cfg_info<G16x32, 3>("3m_16x32_w1x1_occ8"), cfg_info<G32x128, 3>("3m_32x128_w1x4_occ2")};
+    cfg_info<G16x32, 3>("3m_16x32_w1x1_occ8"), cfg_info<G32x128, 3>("3m_32x128_w1x4_occ2"),
+    cfg_info<G64x80, 3>("3m_64x80_w4x1_occ3")};
 constexpr int N_GEMM4 = sizeof(kGemm4) / sizeof(kGemm4[0]);
 constexpr int N_GEMM3 = sizeof(kGemm3) / sizeof(kGemm3[0]);
 constexpr int N_GEMM_CFGS = N_GEMM3 > N_GEMM4 ? N_GEMM3 : N_GEMM4;  // index bound for the API
@@ -328,7 +367,13 @@ int mps_create(int n_dev, const int* dev_ids, int layout, mps_ctx** out) {
   mps_ctx* c = new mps_ctx();
   c->device = dev;
   c->layout = layout;
-  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+  bool ok = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming) == cudaSuccess;
+  for (int l = 0; ok && l < mps_ctx::MAX_LANES; ++l)
+    ok = cudaStreamCreateWithFlags(&c->lane_st[l], cudaStreamNonBlocking) == cudaSuccess &&
+         cudaEventCreateWithFlags(&c->join_ev[l], cudaEventDisableTiming) == cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
     delete c;
     return MPS_ERR_GENERIC;
   }
@@ -423,11 +468,18 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
   const int M = c->M, D = c->D;
   int chi_max = 1;
   for (int m = m_begin; m < m_end; ++m) chi_max = std::max(chi_max, std::max(c->sites[m].chi_l, c->sites[m].chi_r));
-  CU(c, c->v0.ensure((size_t)n * chi_max), "alloc state");
-  CU(c, c->v1.ensure((size_t)n * chi_max), "alloc state");
   size_t cmax = 0;
   for (int m = m_begin; m < m_end; ++m) cmax = std::max(cmax, (size_t)c->sites[m].chi_r * D);
-  CU(c, c->cbuf.ensure((size_t)n * cmax), "alloc C buffer");
+  // lanes: only when every lane keeps >= 64 rows (below that one chain is latency-bound anyway)
+  int L = std::max(1, std::min(c->lanes, n / 64));
+  int lane_r0[mps_ctx::MAX_LANES + 1];
+  for (int l = 0; l <= L; ++l) lane_r0[l] = (int)((long long)n * l / L);
+  for (int l = 0; l < L; ++l) {
+    const size_t nl = (size_t)(lane_r0[l + 1] - lane_r0[l]);
+    CU(c, c->lv0[l].ensure(nl * chi_max), "alloc state");
+    CU(c, c->lv1[l].ensure(nl * chi_max), "alloc state");
+    CU(c, c->lcbuf[l].ensure(nl * cmax), "alloc C buffer");
+  }
 
   // ---- inputs: stage host arrays on the device ----
   const double* u_dev = uniforms;
@@ -482,72 +534,97 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
        "H2D marginals");
   }
 
-  // ---- the mode loop ----
-  const double2* v_in = (const double2*)state_in;
-  if (!v_in) {
+  // ---- the mode loop: L lanes (row blocks), each a chain on its own stream ----
+  if (!state_in) {
     CU(c, c->ones.ensure((size_t)n), "alloc ones");
     fill_ones_kernel<<<(n + 255) / 256, 256, 0, st>>>(c->ones.p, n);
     c->launches++;
-    v_in = c->ones.p;
   }
-  double2* bufs[2] = {c->v0.p, c->v1.p};
-  int cur = 0;
+  cudaStream_t lst[mps_ctx::MAX_LANES];
+  if (L == 1) {
+    lst[0] = st;
+  } else {
+    CU(c, cudaEventRecord(c->fork_ev, st), "fork");
+    for (int l = 0; l < L; ++l) {
+      lst[l] = c->lane_st[l];
+      CU(c, cudaStreamWaitEvent(lst[l], c->fork_ev, 0), "fork wait");
+    }
+  }
+  const double2* v_in[mps_ctx::MAX_LANES];
+  int cur[mps_ctx::MAX_LANES];
+  for (int l = 0; l < L; ++l) {
+    const int r0 = lane_r0[l];
+    v_in[l] = state_in ? (const double2*)state_in + (size_t)r0 * c->sites[m_begin].chi_l : c->ones.p + r0;
+    cur[l] = 0;
+  }
   for (int m = m_begin; m < m_end; ++m) {
     const Site& s = c->sites[m];
     const int N = s.chi_r * D;
-    mps_ctx::Rec rg{0, nullptr, nullptr, 8.0 * n * (double)s.chi_l * N};
-    if (c->profile & 1) {
-      rg.a = c->get_event();
-      rg.b = c->get_event();
-      cudaEventRecord(rg.a, st);
+    for (int l = 0; l < L; ++l) {  // K1 of every lane, then K2+K3 of every lane
+      const int nl = lane_r0[l + 1] - lane_r0[l];
+      mps_ctx::Rec rg{0, nullptr, nullptr, 8.0 * nl * (double)s.chi_l * N};
+      if (c->profile & 1) {
+        rg.a = c->get_event();
+        rg.b = c->get_event();
+        cudaEventRecord(rg.a, lst[l]);
+      }
+      int rc = launch_site_gemm(c, v_in[l], s.tmap, c->lcbuf[l].p, nl, s.chi_l, N, N, lst[l], c->gemm_cfg,
+                                c->gemm_mode);
+      if (rc) return rc;
+      if (c->profile & 1) {
+        cudaEventRecord(rg.b, lst[l]);
+        c->recs.push_back(rg);
+      }
     }
-    int rc = launch_site_gemm(c, v_in, s.tmap, c->cbuf.p, n, s.chi_l, N, N, st, c->gemm_cfg, c->gemm_mode);
-    if (rc) return rc;
-    if (c->profile & 1) {
-      cudaEventRecord(rg.b, st);
-      c->recs.push_back(rg);
+    for (int l = 0; l < L; ++l) {
+      const int r0 = lane_r0[l], nl = lane_r0[l + 1] - r0;
+      double2* v_out = (m == m_end - 1 && state_out) ? (double2*)state_out + (size_t)r0 * s.chi_r
+                                                      : (cur[l] ? c->lv1[l].p : c->lv0[l].p);
+      DrawArgs a;
+      a.C = c->lcbuf[l].p;
+      a.ldc = N;
+      a.chi_r = s.chi_r;
+      a.D = D;
+      a.m = m;
+      a.M = M;
+      a.first_index = first_index + r0;
+      a.u = u_dev ? u_dev + (size_t)r0 * ldu : nullptr;
+      a.ld_u = ldu;
+      a.seed = c->seed;
+      a.disp = disp_dev ? disp_dev + (size_t)r0 * M * D * D : nullptr;
+      a.alpha = alpha_dev ? alpha_dev + (size_t)r0 * M : nullptr;
+      a.alpha_sigma = (disp_dev || alpha_dev) ? -1.0 : c->alpha_sigma;
+      a.v_out = v_out;
+      a.counts = counts_dev + (size_t)r0 * ld_c;
+      a.ld_c = ld_c;
+      a.marg = marg_dev ? marg_dev + (size_t)r0 * ld_c * D : nullptr;
+      a.status = status_dev + r0;
+      // algorithmic bytes: C read once, v' written, u read, count written
+      mps_ctx::Rec rd{1, nullptr, nullptr, 16.0 * nl * N + 16.0 * nl * s.chi_r + 12.0 * nl};
+      if (c->profile & 2) {
+        rd.a = c->get_event();
+        rd.b = c->get_event();
+        cudaEventRecord(rd.a, lst[l]);
+      }
+      {
+        void (*dk)(DrawArgs) = (D == 10) ? displace_draw_kernel<10> : (D == 4) ? displace_draw_kernel<4>
+                                                                                 : displace_draw_kernel<0>;
+        CU(c, launch_pdl(dk, dim3(nl), dim3(DRAW_THREADS), 0, lst[l], a), "displace_draw launch");
+      }
+      c->launches++;
+      if (c->profile & 2) {
+        cudaEventRecord(rd.b, lst[l]);
+        c->recs.push_back(rd);
+      }
+      v_in[l] = v_out;
+      cur[l] ^= 1;
     }
-    double2* v_out = (m == m_end - 1 && state_out) ? (double2*)state_out : bufs[cur];
-    DrawArgs a;
-    a.C = c->cbuf.p;
-    a.ldc = N;
-    a.chi_r = s.chi_r;
-    a.D = D;
-    a.m = m;
-    a.M = M;
-    a.first_index = first_index;
-    a.u = u_dev;
-    a.ld_u = ldu;
-    a.seed = c->seed;
-    a.disp = disp_dev;
-    a.alpha = alpha_dev;
-    a.alpha_sigma = (disp_dev || alpha_dev) ? -1.0 : c->alpha_sigma;
-    a.v_out = v_out;
-    a.counts = counts_dev;
-    a.ld_c = ld_c;
-    a.marg = marg_dev;
-    a.status = status_dev;
-    // algorithmic bytes: C read once, v' written, u read, count written
-    mps_ctx::Rec rd{1, nullptr, nullptr, 16.0 * n * N + 16.0 * n * s.chi_r + 12.0 * n};
-    if (c->profile & 2) {
-      rd.a = c->get_event();
-      rd.b = c->get_event();
-      cudaEventRecord(rd.a, st);
+  }
+  if (L > 1) {
+    for (int l = 0; l < L; ++l) {
+      CU(c, cudaEventRecord(c->join_ev[l], lst[l]), "join");
+      CU(c, cudaStreamWaitEvent(st, c->join_ev[l], 0), "join wait");
     }
-    if (D == 10)
-      displace_draw_kernel<10><<<n, DRAW_THREADS, 0, st>>>(a);
-    else if (D == 4)
-      displace_draw_kernel<4><<<n, DRAW_THREADS, 0, st>>>(a);
-    else
-      displace_draw_kernel<0><<<n, DRAW_THREADS, 0, st>>>(a);
-    c->launches++;
-    if (c->profile & 2) {
-      cudaEventRecord(rd.b, st);
-      c->recs.push_back(rd);
-    }
-    CU(c, cudaGetLastError(), "displace_draw launch");
-    v_in = v_out;
-    cur ^= 1;
   }
 
   // ---- outputs back to the host ----
@@ -619,9 +696,14 @@ void mps_destroy(mps_ctx* c) {
   cudaStreamSynchronize(c->stream);
   for (auto& s : c->sites)
     if (s.owned && s.data) cudaFree(s.data);
-  c->v0.release();
-  c->v1.release();
-  c->cbuf.release();
+  for (int l = 0; l < mps_ctx::MAX_LANES; ++l) {
+    c->lv0[l].release();
+    c->lv1[l].release();
+    c->lcbuf[l].release();
+    if (c->lane_st[l]) cudaStreamDestroy(c->lane_st[l]);
+    if (c->join_ev[l]) cudaEventDestroy(c->join_ev[l]);
+  }
+  if (c->fork_ev) cudaEventDestroy(c->fork_ev);
   c->ones.release();
   c->alpha_d.release();
   c->disp_d.release();
@@ -651,6 +733,14 @@ int mps_site_gemm_cfg(const void* V, const void* G, void* C, int n, int K, int N
 
 int mps_site_gemm(const void* V, const void* G, void* C, int n, int K, int N, int64_t ldc, uint64_t stream) {
   return mps_site_gemm_cfg(V, G, C, n, K, N, ldc, stream, -1, 3);
+}
+
+int mps_set_lanes(mps_ctx* c, int lanes) {
+  if (!c) return MPS_ERR_VALIDATION;
+  if (lanes < 1 || lanes > mps_ctx::MAX_LANES)
+    return fail(c, MPS_ERR_VALIDATION, "lanes must lie in [1, %d], got %d", mps_ctx::MAX_LANES, lanes);
+  c->lanes = lanes;
+  return MPS_OK;
 }
 
 int mps_set_gemm_mode(mps_ctx* c, int mode) {

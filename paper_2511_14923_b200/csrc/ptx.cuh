@@ -78,6 +78,14 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
 
+// Programmatic dependent launch (sm_90+): a kernel launched with the programmatic-
+// serialization attribute may start while its predecessor drains; it must call
+// griddep_wait() before touching anything the predecessor writes or reads-then-we-write.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // D(8x8) += A(8x4, row) * B(4x8, col), FP64.  Fragments (PTX ISA, mma.m8n8k4 .f64):
 //   a: row = lane>>2, col = lane&3;  b: row = lane&3, col = lane>>2;
 //   c0,c1: row = lane>>2, col = 2*(lane&3) + {0,1}.

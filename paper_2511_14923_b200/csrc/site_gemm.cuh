@@ -68,17 +68,25 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
   const int m0 = blockIdx.x * Cfg::BM;
   const int n0r = blockIdx.y * Cfg::BN_R;
 
-  auto issue = [&](int kt) {  // one k-stage: the V tile + B_GROUPS Gamma boxes
+  auto issue_g = [&](int kt) {  // one k-stage: expect the whole stage, load the B_GROUPS Gamma boxes
     const int s = kt % Cfg::STAGES;
-    uint8_t* As = smem + s * Cfg::STAGE_BYTES;
-    uint8_t* Bs = As + Cfg::A_BYTES;
+    uint8_t* Bs = smem + s * Cfg::STAGE_BYTES + Cfg::A_BYTES;
     mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
-    tma_load_2d(As, &tmap_v, kt * 16, m0, &full[s]);
 #pragma unroll
     for (int gi = 0; gi < Cfg::B_GROUPS; ++gi)
       tma_load_2d(Bs + gi * (Cfg::BK_C * 128), &tmap_g, n0r + gi * 16, kt * Cfg::BK_C, &full[s]);
   };
+  auto issue_v = [&](int kt) {  // the V tile of the stage (written by the previous kernel)
+    const int s = kt % Cfg::STAGES;
+    tma_load_2d(smem + s * Cfg::STAGE_BYTES, &tmap_v, kt * 16, m0, &full[s]);
+  };
+  auto issue = [&](int kt) {
+    issue_g(kt);
+    issue_v(kt);
+  };
 
+  // PDL: let the next kernel's CTAs launch into SMs this grid's tail leaves idle
+  griddep_launch_dependents();
   if (threadIdx.x == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -87,7 +95,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     fence_barrier_init();
     prefetch_tmap(&tmap_v);
     prefetch_tmap(&tmap_g);
-    for (int kt = 0; kt < Cfg::STAGES && kt < KT; ++kt) issue(kt);
+    // Gamma is resident input: prefetch the first stages while the predecessor drains
+    for (int kt = 0; kt < Cfg::STAGES && kt < KT; ++kt) issue_g(kt);
+    griddep_wait();  // predecessor (draw of the previous mode) complete: V valid, C free to overwrite
+    for (int kt = 0; kt < Cfg::STAGES && kt < KT; ++kt) issue_v(kt);
   }
   __syncthreads();
 
@@ -177,17 +188,25 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
   const int m0 = blockIdx.x * Cfg::BM;
   const int n0r = blockIdx.y * Cfg::BN_R;
 
-  auto issue = [&](int kt) {
+  auto issue_g = [&](int kt) {  // one k-stage: expect the whole stage, load the B_GROUPS Gamma boxes
     const int s = kt % Cfg::STAGES;
-    uint8_t* As = smem + s * Cfg::STAGE_BYTES;
-    uint8_t* Bs = As + Cfg::A_BYTES;
+    uint8_t* Bs = smem + s * Cfg::STAGE_BYTES + Cfg::A_BYTES;
     mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
-    tma_load_2d(As, &tmap_v, kt * 16, m0, &full[s]);
 #pragma unroll
     for (int gi = 0; gi < Cfg::B_GROUPS; ++gi)
       tma_load_2d(Bs + gi * (Cfg::BK_C * 128), &tmap_g, n0r + gi * 16, kt * Cfg::BK_C, &full[s]);
   };
+  auto issue_v = [&](int kt) {  // the V tile of the stage (written by the previous kernel)
+    const int s = kt % Cfg::STAGES;
+    tma_load_2d(smem + s * Cfg::STAGE_BYTES, &tmap_v, kt * 16, m0, &full[s]);
+  };
+  auto issue = [&](int kt) {
+    issue_g(kt);
+    issue_v(kt);
+  };
 
+  // PDL: let the next kernel's CTAs launch into SMs this grid's tail leaves idle
+  griddep_launch_dependents();
   if (threadIdx.x == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -196,7 +215,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     fence_barrier_init();
     prefetch_tmap(&tmap_v);
     prefetch_tmap(&tmap_g);
-    for (int kt = 0; kt < Cfg::STAGES && kt < KT; ++kt) issue(kt);
+    // Gamma is resident input: prefetch the first stages while the predecessor drains
+    for (int kt = 0; kt < Cfg::STAGES && kt < KT; ++kt) issue_g(kt);
+    griddep_wait();  // predecessor (draw of the previous mode) complete: V valid, C free to overwrite
+    for (int kt = 0; kt < Cfg::STAGES && kt < KT; ++kt) issue_v(kt);
   }
   __syncthreads();
 

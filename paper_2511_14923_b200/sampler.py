@@ -162,6 +162,14 @@ class MpsSampler:
                                      _ptr(status), 0 if stream is None else int(stream))
         _native.check(rc, self.ctx)
 
+    def set_lanes(self, lanes: int):
+        """Concurrent row-block chains per call (mps_set_lanes); results do not depend on it."""
+        _native.check(self.L.mps_set_lanes(self.ctx, int(lanes)), self.ctx)
+
+    def set_gemm_mode(self, mode: int):
+        """K1 complex product: 3 (3M, default) or 4 (4M)."""
+        _native.check(self.L.mps_set_gemm_mode(self.ctx, int(mode)), self.ctx)
+
     def profile(self, mask: int = 3):
         """Time kernel launches live with CUDA events (mask bit 0: K1, bit 1: K2+K3)."""
         _native.check(self.L.mps_profile(self.ctx, int(mask)), self.ctx)

@@ -308,7 +308,7 @@ def test_staged_and_global_draw_agree():
     _check_parity(sites, res, stream_uniforms(2, 0, N, M), alpha=alpha_stream(2, 0, N, M, 0.5))
 
 
-@pytest.mark.parametrize("mode,cfg_id", [(m, c) for m in (3, 4) for c in range(-2, 6 if m == 3 else 5)])
+@pytest.mark.parametrize("mode,cfg_id", [(m, c) for m in (3, 4) for c in range(-2, 7 if m == 3 else 6)])
 def test_gemm_configs_bit_identical(cfg_id, mode):
     """Within a product mode every tile config (and the autotuner's pick) gives the same bits."""
     L = _native.lib()
@@ -344,3 +344,40 @@ def test_chain_parity_both_modes(c2_sites, mode):
         _native.check(eng.L.mps_set_gemm_mode(eng.ctx, mode), eng.ctx)
         res = eng.sample(cfg, return_marginals=True)
     _check_parity(c2_sites, res, stream_uniforms(12, 0, N, M), alpha=alpha_stream(12, 0, N, M, 0.5))
+
+
+def test_lane_count_invariance(c2_sites):
+    """Splitting a micro-batch into concurrent row-block chains changes nothing (bitwise)."""
+    N = 520
+    outs = []
+    with MpsSampler(MPS(c2_sites)) as eng:
+        for lanes in (1, 2, 3, 4):
+            eng.set_lanes(lanes)
+            outs.append(eng.sample(MpsSamplerConfig(N=N, seed=3, alpha_sigma=0.5, batch_size=N),
+                                   return_marginals=True))
+    for o in outs[1:]:
+        assert np.array_equal(o["counts"], outs[0]["counts"])
+        assert np.array_equal(o["marginals"], outs[0]["marginals"])
+        assert np.array_equal(o["status"], outs[0]["status"])
+
+
+def test_lanes_with_stage_state(c2_sites):
+    """Lanes also split state_in / state_out row blocks correctly (pipeline stage path)."""
+    N, M, cut = 256, 16, 5
+    mps = MPS(c2_sites)
+    cfg = MpsSamplerConfig(N=N, seed=8, alpha_sigma=0.5, batch_size=N)
+    with MpsSampler(mps) as eng:
+        eng.set_lanes(1)
+        full = eng.sample(cfg)
+    counts = torch.empty((N, M), dtype=torch.int32, device="cuda")
+    status = torch.zeros(N, dtype=torch.uint8, device="cuda")
+    state = torch.empty((N, mps.bond_dims[cut]), dtype=torch.complex128, device="cuda")
+    with MpsSampler(mps, sites_range=(0, cut)) as s0, MpsSampler(mps, sites_range=(cut, M)) as s1:
+        s0.set_lanes(4)
+        s1.set_lanes(2)
+        for e in (s0, s1):
+            e.set_streams(8, 0.5)
+        s0.run(0, N, counts, state_out=state, status=status)
+        s1.run(0, N, counts, state_in=state, status=status)
+    torch.cuda.synchronize()
+    assert np.array_equal(counts.cpu().numpy(), full["counts"])
