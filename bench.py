@@ -41,7 +41,12 @@ CONFIGS = {
     "c1": (8, 16, 4, 100, 0.5, 1000, "BASELINE configs[0]: M=8 chi=16 D=4 n=100 alpha~CN(0,0.25)"),
     "c2": (16, 100, 10, 100, 0.5, 10000, "BASELINE configs[1]: M=16 chi=100 D=10 n=100 alpha~CN(0,0.25)"),
     "c3": (64, 1000, 10, 1024, 0.5 ** 0.5, 100000, "BASELINE configs[2]: M=64 chi=1000 D=10 n=1024 alpha~CN(0,0.5)"),
+    "c4": (144, 4000, 10, 2048, 0.5 ** 0.5, 1000000,
+           "BASELINE configs[3]: M=144 chi=4000 D=10 n=2048 alpha~CN(0,0.5), mode-pipelined"),
+    "c5": (64, 10000, 10, 4096, 0.5 ** 0.5, 100000,
+           "BASELINE configs[4]: M=64 chi=10000 D=10 n=4096 alpha~CN(0,0.5), mode-pipelined"),
 }
+HBM_USABLE = 170e9  # bytes per B200 we plan to fill with sites + workspaces
 LANES = 2  # concurrent row-block chains per micro-batch (mps_set_lanes)
 METRIC = "MPS samples/sec (chi,D,M stated) at 1/2/4/8 B200; % of FP64 tensor-core peak"
 
@@ -54,6 +59,22 @@ def fp64_peak():
         return 37.2, "nominal (148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz)"
 
 
+def ncu_traffic(cfg_name, n):
+    """DRAM bytes per K1 launch from the committed ncu --set full capture of a full-chi mode
+    (profiles/), with the algorithmic bytes of that same launch, or (None, None)."""
+    if cfg_name != "c3" or n != 1024:
+        return None, None
+    p = ROOT / "profiles" / "r01_ncu_k1_site_gemm3m_c3_mode30_n1024.json"
+    try:
+        rep = json.loads(p.read_text())[0]
+    except Exception:
+        return None, None
+    chi, D = 1000, 10
+    algo = 16.0 * chi * chi * D + 16.0 * n * chi + 16.0 * n * chi * D
+    return rep["dram_bytes_total"], {"source": str(p.relative_to(ROOT)), "launch": "mode 30 (chi_l = chi_r = 1000)",
+                                     "algorithmic_bytes": algo}
+
+
 def site_flops(dims, D, n):
     return [8.0 * n * dims[m] * dims[m + 1] * D + 8.0 * n * dims[m + 1] * D * D for m in range(len(dims) - 1)]
 
@@ -63,62 +84,85 @@ def site_flops(dims, D, n):
 # ---------------------------------------------------------------------------------------------
 
 
-def cpu_sample_rate(cfg_name, target_s=15.0):
-    """Time the NumPy oracle (batched BLAS ZGEMM chain, all host cores) on a bounded sample:
-    n_cpu samples through a block of S consecutive full-chi sites; extrapolate to all M sites
-    by algorithmic flops.  Returns (samples/s, cores, sample description)."""
-    from oracle import mps_oracle as orc
+class CpuBaseline:
+    """The NumPy oracle (batched BLAS ZGEMM chain, all host cores) on a bounded sample.
 
-    M, chi, D, n, sigma, _, _ = CONFIGS[cfg_name]
-    dims = orc.bond_dims(M, chi, D)
-    try:
-        from threadpoolctl import threadpool_info
+    c1/c2: the whole chain, n samples through all M sites.  Larger configs: n_cpu samples
+    through a block of full-chi sites (a column slice of one site when a site exceeds
+    ~1 GB of host memory), the oracle's per-mode step as in sample_chain; the per-sample
+    time is extrapolated to all M sites by algorithmic flops.  Sites are generated once."""
 
-        cores = max([i.get("num_threads", 1) for i in threadpool_info()] or [os.cpu_count() or 1])
-    except Exception:
-        cores = os.cpu_count() or 1
-    if M * chi * chi * D * 16 <= 2e9:
-        # whole chain fits: run it in full
-        sites = orc.random_mps(M, chi, D, seed=0)
-        n_cpu = n
-        u = orc.stream_uniforms(0, 0, n_cpu, M)
-        al = orc.alpha_stream(0, 0, n_cpu, M, sigma)
+    def __init__(self, cfg_name):
+        from oracle import mps_oracle as orc
+
+        self.orc = orc
+        M, chi, D, n, sigma, _, _ = CONFIGS[cfg_name]
+        self.M, self.chi, self.D, self.n, self.sigma = M, chi, D, n, sigma
+        self.dims = orc.bond_dims(M, chi, D)
+        try:
+            from threadpoolctl import threadpool_info
+
+            self.cores = max([i.get("num_threads", 1) for i in threadpool_info()] or [os.cpu_count() or 1])
+        except Exception:
+            self.cores = os.cpu_count() or 1
+        self.full = M * chi * chi * D * 16 <= 2e9
+        if self.full:
+            self.sites = orc.random_mps(M, chi, D, seed=0)
+            self.n_cpu = n
+            self.u = orc.stream_uniforms(0, 0, n, M)
+            self.al = orc.alpha_stream(0, 0, n, M, sigma)
+            return
+        mid = M // 2
+        site_bytes = 16.0 * chi * chi * D
+        self.S = 2 if site_bytes <= 2e8 else 1
+        self.block = list(range(mid, mid + self.S))
+        self.slice_cols = chi if site_bytes <= 1e9 else max(1, int(1e9 / (16.0 * chi * D)))
+        rng = np.random.default_rng(0)
+        if self.slice_cols == chi and site_bytes <= 2e8:
+            self.sites = [orc.random_site(0, m, self.dims[m], self.dims[m + 1], D) for m in self.block]
+        else:  # timing stand-in of the same shape (QR of a multi-GB site on the host is not the workload)
+            self.sites = [(rng.standard_normal((chi, self.slice_cols, D)) + 1j * rng.standard_normal(
+                (chi, self.slice_cols, D))) / np.sqrt(2.0 * chi * D) for _ in self.block]
+        self.n_cpu = 256
+        self.u = orc.stream_uniforms(0, 0, self.n_cpu, self.S)
+        self.al = orc.alpha_stream(0, 0, self.n_cpu, self.S, sigma)
+        v0 = rng.standard_normal((self.n_cpu, chi)) + 1j * rng.standard_normal((self.n_cpu, chi))
+        self.v0 = v0 / np.linalg.norm(v0, axis=1, keepdims=True)
+
+    def run(self, target_s=15.0):
+        """Returns (samples/s, cores, sample description)."""
+        orc, D = self.orc, self.D
         reps, t = 0, 0.0
-        while t < target_s and reps < 100:
+        if self.full:
+            while t < target_s and reps < 100:
+                t0 = time.perf_counter()
+                orc.sample_chain(self.sites, self.u, alpha=self.al)
+                t += time.perf_counter() - t0
+                reps += 1
+            return reps * self.n_cpu / t, self.cores, f"full chain, {reps} x {self.n_cpu} samples through all {self.M} sites"
+        n_cpu = self.n_cpu
+        rows = np.arange(n_cpu)
+        while t < target_s and reps < 50:
             t0 = time.perf_counter()
-            orc.sample_chain(sites, u, alpha=al)
+            v = self.v0
+            for j, G in enumerate(self.sites):  # the oracle's per-mode step (sample_chain body)
+                chl, chr_, _ = G.shape
+                C = (v @ G.reshape(chl, chr_ * D)).reshape(n_cpu, chr_, D)
+                E = np.einsum("bjd,bkd->bjk", C, orc.displacement_matrix(self.al[:, j], D))
+                p = (E.real * E.real + E.imag * E.imag).sum(axis=1)
+                k, ok, _ = orc.draw(p, self.u[:, j])
+                v = E[rows, :, k] / np.sqrt(p[rows, k])[:, None]
+                if chr_ != self.chi:  # column slice: keep the next state at full width for the next site
+                    v = np.resize(v, (n_cpu, self.chi))
             t += time.perf_counter() - t0
             reps += 1
-        return reps * n_cpu / t, cores, f"full chain, {reps} x {n_cpu} samples through all {M} sites"
-    mid = M // 2
-    S = 2
-    block = list(range(mid - S // 2, mid - S // 2 + S))
-    sites = [orc.random_site(0, m, dims[m], dims[m + 1], D) for m in block]
-    n_cpu = 256
-    u = orc.stream_uniforms(0, 0, n_cpu, S)
-    al = orc.alpha_stream(0, 0, n_cpu, S, sigma)
-    rng = np.random.default_rng(0)
-    v0 = rng.standard_normal((n_cpu, dims[block[0]])) + 1j * rng.standard_normal((n_cpu, dims[block[0]]))
-    v0 /= np.linalg.norm(v0, axis=1, keepdims=True)
-    reps, t = 0, 0.0
-    while t < target_s and reps < 50:
-        t0 = time.perf_counter()
-        v = v0
-        for j, G in enumerate(sites):  # the oracle's per-mode step (sample_chain body)
-            chl, chr_, _ = G.shape
-            C = (v @ G.reshape(chl, chr_ * D)).reshape(n_cpu, chr_, D)
-            E = np.einsum("bjd,bkd->bjk", C, orc.displacement_matrix(al[:, j], D))
-            p = (E.real * E.real + E.imag * E.imag).sum(axis=1)
-            k, ok, _ = orc.draw(p, u[:, j])
-            v = E[np.arange(n_cpu), :, k] / np.sqrt(p[np.arange(n_cpu), k])[:, None]
-        t += time.perf_counter() - t0
-        reps += 1
-    fl = site_flops(dims, D, n_cpu)
-    t_block = t / reps
-    t_all = t_block * sum(fl) / sum(fl[m] for m in block)
-    return (n_cpu / t_all, cores,
-            f"{reps} reps of {n_cpu} samples through sites {block[0]}..{block[-1]} (chi={chi}); "
-            f"per-sample time extrapolated to all {M} sites by algorithmic flops")
+        fl = site_flops(self.dims, D, n_cpu)
+        timed = sum(8.0 * n_cpu * G.shape[0] * G.shape[1] * D + 8.0 * n_cpu * G.shape[1] * D * D for G in self.sites)
+        t_all = (t / reps) * sum(fl) / timed
+        what = "full sites" if self.slice_cols == self.chi else f"a {self.slice_cols}-column slice of a site"
+        return (n_cpu / t_all, self.cores,
+                f"{reps} reps of {n_cpu} samples through {len(self.sites)} x {what} (chi={self.chi}); per-sample "
+                f"time extrapolated to all {self.M} sites by algorithmic flops")
 
 
 # ---------------------------------------------------------------------------------------------
@@ -162,6 +206,127 @@ class Clocks:
 # ---------------------------------------------------------------------------------------------
 
 
+def run_pipelined(args, rank, world, local, W, K, config, dims):
+    """Mode-pipelined layout: rank g holds a contiguous,
+    flops-balanced block of sites; micro-batches of n samples flow rank 0 -> G-1, the
+    n x chi complex128 state handed on by NCCL send/recv (the only exchange).  A step is one
+    micro-batch entering the pipeline; the timed K steps include fill and drain (K + G - 1
+    pipeline ticks).  Uniforms and alpha come from the device counter streams on every
+    stage (column = absolute mode), so no inputs travel between ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2511_14923_b200 import MPS, MpsSampler
+    from paper_2511_14923_b200.distributed import run_pipeline, stage_blocks
+
+    M, chi, D, n, sigma, _, desc = CONFIGS[args.config]
+    dev = torch.device("cuda", local)
+    blocks = stage_blocks(dims, D, world)
+    mb, me = blocks[rank]
+    t_setup = time.perf_counter()
+    mps = MPS.random(M, chi, D, seed=0, device=dev, block=(mb, me))
+    block_bytes = sum(dims[m] * dims[m + 1] for m in range(mb, me)) * D * 16.0
+    eng = MpsSampler(mps, device=local, sites_range=(mb, me), layout=1, sum_planes=block_bytes * 1.5 < HBM_USABLE)
+    eng.set_lanes(LANES)
+    eng.set_streams(0, sigma)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t_setup
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    nsteps = W + K
+    counts = torch.empty((nsteps, n, M), dtype=torch.int32, device=dev)
+    status = torch.zeros((nsteps, n), dtype=torch.uint8, device=dev)
+    y = torch.empty((n, dims[me]), dtype=torch.complex128, device=dev) if rank < world - 1 else None
+    c_host = torch.empty((n, me - mb), dtype=torch.int32).pin_memory()
+
+    def stage_for(offset, copy_out=False):
+        def stage(t, x):
+            s_ = offset + t
+            eng.run(s_ * n, n, counts[s_], m_begin=mb, m_end=me, state_in=x, state_out=y, status=status[s_],
+                    stream=stream.cuda_stream)
+            if copy_out:
+                c_host.copy_(counts[s_, :, mb:me], non_blocking=True)
+            return y
+        return stage
+
+    def pipe(offset, count, copy_out=False):
+        run_pipeline(stage_for(offset, copy_out), count,
+                     recv_like=lambda: torch.empty((n, dims[mb]), dtype=torch.complex128, device=dev),
+                     send_like=lambda: torch.empty((n, dims[me]), dtype=torch.complex128, device=dev),
+                     rank=rank, world=world)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    def max_ms(ms):
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    pipe(0, W)
+    barrier()
+    clocks = Clocks(local)
+    clocks.start()
+    l0 = eng.kernel_launches
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    pipe(W, K)
+    e1.record(stream)
+    barrier()
+    launches = eng.kernel_launches - l0
+    ck = clocks.stop()
+    ms = max_ms(e0.elapsed_time(e1))
+    value = K * n / (ms / 1e3)
+    # e2e: each stage also copies its count columns to pinned host memory per micro-batch
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    pipe(W, K, copy_out=True)
+    e3.record(stream)
+    barrier()
+    ms_e2e = max_ms(e2.elapsed_time(e3))
+    # roofline: K1 per launch on this rank, one lane, events around each launch
+    eng.set_lanes(1)
+    pipe(0, min(W, 2))
+    barrier()
+    eng.profile(1)
+    pipe(W, min(K, 3))
+    barrier()
+    prof = eng.profile_read()
+    eng.profile(0)
+    peak, peak_src = fp64_peak()
+    gemm_ms_avg = prof["gemm_ms"] / max(prof["gemm_launches"], 1)
+    gemm_flops_avg = prof["gemm_flops"] / max(prof["gemm_launches"], 1)
+    achieved = gemm_flops_avg / (gemm_ms_avg / 1e3) / 1e12 if gemm_ms_avg > 0 else 0.0
+    step_flops = sum(site_flops(dims, D, n))
+    whole_tf = K * step_flops / (ms / 1e3) / 1e12
+    ok = not bool((status[W:] & 1).any().item())
+    cfg = dict(config, layout="mode-pipelined", stage_blocks=blocks,
+               pipeline=f"{K} micro-batches over {world} stages = {K + world - 1} ticks (fill+drain timed)")
+    line = {
+        "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak" if world == 1 else "strong",
+        "vs_baseline": None, "dtype": "c128",
+        "data": "synthetic (random row-orthonormal sites from per-site seeds on each stage's device, "
+                "device counter-stream uniforms and alpha)",
+        "config": cfg,
+        "e2e": {"value": K * n / (ms_e2e / 1e3), "unit": "samples/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": n * M * 4},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak if peak else None, "traffic": None,
+                     "kernel": "site_gemm3m_kernel (K1, FP64 DMMA, 3M), rank 0's stage", "peak_source": peak_src,
+                     "per_launch": {"ms": gemm_ms_avg, "algorithmic_flops": gemm_flops_avg},
+                     "whole_chain_tflops": whole_tf, "whole_chain_frac": whole_tf / (world * peak)},
+        "clocks": ck, "valid_outputs": ok, "setup_s": setup_s,
+    }
+    eng.close()
+    return line
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -170,6 +335,8 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--layout", default="auto", choices=["auto", "sharded", "pipelined"],
+                    help="auto: sample-sharded when the MPS fits one GPU, else mode-pipelined")
     args = ap.parse_args()
     W = max(args.warmup, 3)
     K = args.steps
@@ -192,12 +359,13 @@ def main():
         if rank != 0:
             return
         steps = []
+        cpu = CpuBaseline(args.config)
         for i in range(W + K):
-            v, cores, sample = cpu_sample_rate(args.config, target_s=max(1.0, 60.0 / (W + K)))
+            v, cores, sample = cpu.run(target_s=max(1.0, 60.0 / (W + K)))
             if i >= W:
                 steps.append(v)
         v = float(np.median(steps))
-        line = {"metric": METRIC, "value": v, "unit": "samples/s", "impl": "reference", "n_gpus": 0, "steps": K,
+        line = {"metric": METRIC, "value": v, "unit": "samples/s", "impl": "reference", "n_gpus": world, "steps": K,
                 "warmup": W, "ms_per_step": 1000.0 * n / v, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "c128", "data": "synthetic", "config": config,
                 "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cores, "kind": "port", "sample": sample},
@@ -210,9 +378,26 @@ def main():
 
     from paper_2511_14923_b200 import MPS, MpsSampler, alpha_stream, stream_uniforms
 
+    site_bytes = sum(a * b for a, b in zip(dims[:-1], dims[1:])) * D * 16.0
+    layout = args.layout
+    if layout == "auto":
+        layout = "sharded" if site_bytes * 1.5 < HBM_USABLE else "pipelined"
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if layout == "pipelined":
+        if site_bytes / world > HBM_USABLE:
+            if rank == 0:
+                print(json.dumps({"metric": METRIC, "value": None, "unit": "samples/s", "n_gpus": world,
+                                  "config": config, "infeasible": "the MPS (%.0f GB) does not fit %d B200(s)"
+                                  % (site_bytes / 1e9, world)}), flush=True)
+            return
+        line = run_pipelined(args, rank, world, local, W, K, config, dims)
+        if rank == 0:
+            print(json.dumps(line), flush=True)
+        if world > 1:
+            dist.destroy_process_group()
+        return
     dev = torch.device("cuda", local)
     t_setup = time.perf_counter()
     mps = MPS.random(M, chi, D, seed=0, device=dev) if M * chi * chi * D * 16 > 2e8 else MPS.random(M, chi, D, 0)
@@ -319,6 +504,7 @@ def main():
 
     ok = bool((counts[W:] >= 0).all().item()) and not bool((status[W:] & 1).any().item())
     peak, peak_src = fp64_peak()
+    traffic, traffic_note = ncu_traffic(args.config, n)
     gemm_ms_avg = prof["gemm_ms"] / max(prof["gemm_launches"], 1)
     gemm_flops_avg = prof["gemm_flops"] / max(prof["gemm_launches"], 1)
     achieved = gemm_flops_avg / (gemm_ms_avg / 1e3) / 1e12 if gemm_ms_avg > 0 else 0.0
@@ -334,7 +520,8 @@ def main():
                 "d2h_bytes_per_step": n * M * 4 + n},
         "gpu_launches": int(launches),
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": None, "kernel": "site_gemm_kernel (K1, FP64 DMMA)",
+                     "frac": achieved / peak, "traffic": traffic, "traffic_note": traffic_note,
+                     "kernel": "site_gemm3m_kernel (K1, FP64 DMMA, 3M)",
                      "peak_source": peak_src,
                      "per_launch": {"ms": gemm_ms_avg, "algorithmic_flops": gemm_flops_avg},
                      "share_of_step": prof["gemm_ms"] / ms_instr if ms_instr > 0 else None,
@@ -350,7 +537,7 @@ def main():
         "setup_s": setup_s,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, cores, sample = cpu_sample_rate(args.config)
+        v, cores, sample = CpuBaseline(args.config).run()
         line["cpu_baseline"] = {"value": v, "unit": "samples/s", "cores": cores, "kind": "port", "sample": sample}
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -152,6 +152,11 @@ int mps_set_gemm_config(mps_ctx* ctx, int cfg);
  * to the caller's stream) so one block's draw kernels and GEMM tails overlap another's
  * GEMMs.  Per-sample results are identical for any lane count. */
 int mps_set_lanes(mps_ctx* ctx, int lanes);
+/* Sum planes for the 3M GEMM (default on): mps_set_site stores Gr+Gi next to each site
+ * (+50% of the site's HBM, skipped per site when memory is short) and the draw kernel
+ * writes Vr+Vi next to the state, so K1 loads the operand sums instead of forming them
+ * on the FP64 pipe.  Results are bit-identical either way.  Set before loading sites. */
+int mps_set_sum_planes(mps_ctx* ctx, int enable);
 /* K1 complex product: 3 = 3M (default), 4 = 4M.  Results of the two modes differ at
  * rounding level; each is deterministic across batch sizes and GPU counts. */
 int mps_set_gemm_mode(mps_ctx* ctx, int mode);

@@ -16,9 +16,10 @@ LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
 
 # every symbol include/mps_sampler.h declares (checked by tests/test_boundary.py)
 EXPORTS = (
-    "mps_create", "mps_configure", "mps_set_site", "mps_set_streams", "mps_sample",
-    "mps_sample_range", "mps_kernel_launches", "mps_profile", "mps_profile_read", "mps_last_error", "mps_destroy",
-    "mps_site_gemm", "mps_site_gemm_cfg", "mps_set_gemm_config", "mps_set_gemm_mode", "mps_set_lanes", "mps_displacement", "mps_stream_uniforms",
+    "mps_create", "mps_configure", "mps_set_site", "mps_set_streams", "mps_sample", "mps_sample_range",
+    "mps_kernel_launches", "mps_profile", "mps_profile_read", "mps_last_error", "mps_destroy",
+    "mps_site_gemm", "mps_site_gemm_cfg", "mps_set_gemm_config", "mps_set_gemm_mode", "mps_set_lanes",
+    "mps_set_sum_planes", "mps_displacement", "mps_stream_uniforms",
 )
 
 MPS_SITE_HOST, MPS_SITE_DEVICE_COPY, MPS_SITE_DEVICE_BORROW = 0, 1, 2
@@ -52,6 +53,7 @@ def _declare(L):
     L.mps_site_gemm_cfg.argtypes = [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int64, c_uint64, c_int, c_int]
     L.mps_set_gemm_mode.argtypes = [c_void_p, c_int]
     L.mps_set_lanes.argtypes = [c_void_p, c_int]
+    L.mps_set_sum_planes.argtypes = [c_void_p, c_int]
     L.mps_set_gemm_config.argtypes = [c_void_p, c_int]
     L.mps_displacement.argtypes = [c_void_p, c_int, c_int, c_void_p, c_uint64]
     L.mps_stream_uniforms.argtypes = [c_uint64, c_int64, c_int, c_int, c_void_p, c_uint64]
@@ -61,6 +63,7 @@ def _declare(L):
                                                   "mps_set_streams", "mps_sample", "mps_sample_range",
                                                   "mps_profile", "mps_profile_read", "mps_site_gemm_cfg",
                                                   "mps_set_gemm_config", "mps_set_gemm_mode", "mps_set_lanes",
+                                                  "mps_set_sum_planes",
                                                   "mps_site_gemm", "mps_displacement", "mps_stream_uniforms"):
             fn.restype = c_int
 
@@ -69,7 +72,7 @@ def load_library(path: str | os.PathLike | None = None):
     """Load (once) and return the CDLL.  Loading needs no GPU; calls do."""
     global _lib
     if _lib is None:
-        p = Path(path) if path else LIB_PATH
+        p = Path(path) if path else Path(os.environ.get("MPS_LIB", LIB_PATH))
         if not p.exists():
             raise GbsError(f"{p} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
         L = ctypes.CDLL(str(p))

@@ -148,6 +148,8 @@ struct DrawArgs {
   const double2* alpha;     // n x M or null
   double alpha_sigma;       // >= 0: device alpha stream when disp & alpha are null
   double2* v_out;           // n x chi_r
+  double* vs_out;           // n x ld_vs sum plane (re + im) of v_out for the 3M GEMM, or null
+  int ld_vs;
   int32_t* counts;          // n x ld_c
   long long ld_c;
   double* marg;             // n x ld_c x D or null
@@ -221,7 +223,10 @@ __global__ void __launch_bounds__(DRAW_THREADS, 4)
   __syncthreads();
 
   if (A.status[b] & ST_FAILED) {  // dead sample: zero state, count -1 (deterministic chain)
-    for (int j = tid; j < A.chi_r; j += DRAW_THREADS) A.v_out[(long long)b * A.chi_r + j] = make_double2(0.0, 0.0);
+    for (int j = tid; j < A.chi_r; j += DRAW_THREADS) {
+      A.v_out[(long long)b * A.chi_r + j] = make_double2(0.0, 0.0);
+      if (A.vs_out) A.vs_out[(long long)b * A.ld_vs + j] = 0.0;
+    }
     if (tid == 0) A.counts[crow] = -1;
     if (A.marg && tid < D) A.marg[crow * D + tid] = 0.0;
     return;
@@ -301,7 +306,10 @@ __global__ void __launch_bounds__(DRAW_THREADS, 4)
   // ---- pass 2: gather + renormalise ----
   double2* vb = A.v_out + (long long)b * A.chi_r;
   if (ks < 0) {
-    for (int j = tid; j < A.chi_r; j += DRAW_THREADS) vb[j] = make_double2(0.0, 0.0);
+    for (int j = tid; j < A.chi_r; j += DRAW_THREADS) {
+      vb[j] = make_double2(0.0, 0.0);
+      if (A.vs_out) A.vs_out[(long long)b * A.ld_vs + j] = 0.0;
+    }
     return;
   }
   for (int j = tid; j < A.chi_r; j += DRAW_THREADS) {
@@ -321,13 +329,22 @@ __global__ void __launch_bounds__(DRAW_THREADS, 4)
         e.y = fma(tk.y, c.x, e.y);
       }
     }
-    vb[j] = make_double2(e.x * scale, e.y * scale);
+    const double2 v = make_double2(e.x * scale, e.y * scale);
+    vb[j] = v;
+    // __dadd_rn: no FMA contraction with the scaling above, so the plane holds exactly the
+    // sum of the stored (re, im) pair, as the GEMM's in-kernel add would form it
+    if (A.vs_out) A.vs_out[(long long)b * A.ld_vs + j] = __dadd_rn(v.x, v.y);
   }
 }
 
-__global__ void fill_ones_kernel(double2* v, int n) {
+// chi = 1 starting state: v = (1, 0) per sample and its sum plane (row pitch 2 doubles)
+__global__ void fill_ones_kernel(double2* v, double* vs, int n) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) v[i] = make_double2(1.0, 0.0);
+  if (i < n) {
+    v[i] = make_double2(1.0, 0.0);
+    vs[2 * i] = 1.0;
+    vs[2 * i + 1] = 0.0;
+  }
 }
 
 }  // namespace mps

@@ -45,20 +45,24 @@ EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
-// 2-D row-major float64 matrix (rows x cols doubles, row pitch in bytes), box {16, box_rows}, 128B swizzle.
+// 2-D row-major float64 matrix (rows x cols doubles, row pitch in bytes), box {box_cols, box_rows};
+// 16-double boxes use the 128B swizzle, 8-double boxes (sum planes of the state) the 64B one.
 bool make_tmap(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t pitch_bytes,
-               uint32_t box_rows) {
+               uint32_t box_rows, uint32_t box_cols = 16) {
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return false;
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {pitch_bytes};
-  cuuint32_t box[2] = {16, box_rows};
+  cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, box_cols == 8 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
+
+// sum-plane row pitch (doubles): TMA needs 16-byte row strides
+inline int sum_ld(int cols) { return (cols + 1) & ~1; }
 
 bool is_device_ptr(const void* p) {
   if (!p) return false;
@@ -75,6 +79,8 @@ struct Site {
   double2* data = nullptr;
   bool owned = false;
   CUtensorMap tmap;
+  double* gsum = nullptr;  // sum plane Gr + Gi (chi_l x sum_ld(N)) for the 3M GEMM, or null
+  CUtensorMap tmap_gs;
 };
 
 template <class T>
@@ -120,6 +126,9 @@ struct mps_ctx {
   cudaStream_t lane_st[MAX_LANES] = {};
   cudaEvent_t fork_ev = nullptr, join_ev[MAX_LANES] = {};
   DevBuf<double2> lv0[MAX_LANES], lv1[MAX_LANES], lcbuf[MAX_LANES];
+  DevBuf<double> lvs0[MAX_LANES], lvs1[MAX_LANES];  // state sum planes (3M operand sums)
+  bool sum_planes = true;                           // feed the 3M GEMM precomputed sums
+  DevBuf<double> ones_sum, in_sum;
   // workspaces
   DevBuf<double2> ones, alpha_d, disp_d;
   DevBuf<double> u_d, marg_d;
@@ -196,30 +205,65 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
+// K1 operands of one launch.  Vs / tgs (the sum planes) may be null: the 3M kernel then
+// forms the sums with DADDs; both paths give bit-identical C.
+struct GemmOps {
+  const void* V;
+  const double* Vs;
+  int ld_vs;
+  const CUtensorMap* tg;
+  const CUtensorMap* tgs;
+  double2* C;
+  int n, K, N;
+  long long ldc;
+};
+
 // K1 tile configurations, one list per product mode.  Within a mode all configs share
 // BK_C = 8 and the same k-step order, so the per-element summation order (and hence
 // every bit of C) is config-independent; the autotuner only changes speed.
-template <class Cfg, int MODE>
-static cudaError_t launch_cfg(const CUtensorMap& tv, const CUtensorMap& tg, double2* C, int n, int K, int N,
-                              long long ldc, cudaStream_t st) {
+template <class Cfg, int MODE, bool SUMS>
+static cudaError_t launch_cfg_impl(const GemmOps& o, cudaStream_t st) {
   static bool configured = false;
-  void (*kern)(const CUtensorMap, const CUtensorMap, double2*, int, int, int, long long);
-  if constexpr (MODE == 3)
-    kern = site_gemm3m_kernel<Cfg>;
-  else
-    kern = site_gemm_kernel<Cfg>;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    configured = true;
+  CUtensorMap tv, tvs;
+  if (!make_tmap(&tv, o.V, o.n, 2 * (uint64_t)o.K, 16 * (uint64_t)o.K, Cfg::BM)) return cudaErrorInvalidValue;
+  dim3 grid((o.n + Cfg::BM - 1) / Cfg::BM, (2 * o.N + Cfg::BN_R - 1) / Cfg::BN_R);
+  const int KT = (o.K + Cfg::BK_C - 1) / Cfg::BK_C;
+  if constexpr (MODE == 4) {
+    if (!configured) {
+      cudaError_t e = cudaFuncSetAttribute(site_gemm_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           Cfg::SMEM_BYTES);
+      if (e != cudaSuccess) return e;
+      configured = true;
+    }
+    return launch_pdl(site_gemm_kernel<Cfg>, grid, dim3(Cfg::THREADS), Cfg::SMEM_BYTES, st, tv, *o.tg, o.C, o.n, o.N,
+                      KT, o.ldc);
+  } else {
+    using S = Sums3M<Cfg, SUMS>;
+    if (!configured) {
+      cudaError_t e = cudaFuncSetAttribute(site_gemm3m_kernel<Cfg, SUMS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           S::SMEM_BYTES);
+      if (e != cudaSuccess) return e;
+      configured = true;
+    }
+    if constexpr (SUMS) {
+      if (!make_tmap(&tvs, o.Vs, o.n, (uint64_t)o.K, 8 * (uint64_t)o.ld_vs, Cfg::BM, 8)) return cudaErrorInvalidValue;
+    } else {
+      tvs = tv;  // unused
+    }
+    return launch_pdl(site_gemm3m_kernel<Cfg, SUMS>, grid, dim3(Cfg::THREADS), S::SMEM_BYTES, st, tv, *o.tg, tvs,
+                      SUMS ? *o.tgs : *o.tg, o.C, o.n, o.N, KT, o.ldc);
   }
-  dim3 grid((n + Cfg::BM - 1) / Cfg::BM, (2 * N + Cfg::BN_R - 1) / Cfg::BN_R);
-  int KT = (K + Cfg::BK_C - 1) / Cfg::BK_C;
-  return launch_pdl(kern, grid, dim3(Cfg::THREADS), Cfg::SMEM_BYTES, st, tv, tg, C, n, N, KT, ldc);
 }
 
-typedef cudaError_t (*LaunchFn)(const CUtensorMap&, const CUtensorMap&, double2*, int, int, int, long long,
-                                cudaStream_t);
+template <class Cfg, int MODE>
+static cudaError_t launch_cfg(const GemmOps& o, cudaStream_t st) {
+  if constexpr (MODE == 3 && Cfg::BN_R % 32 == 0) {
+    if (o.Vs && o.tgs) return launch_cfg_impl<Cfg, 3, true>(o, st);
+  }
+  return launch_cfg_impl<Cfg, MODE, false>(o, st);
+}
+
+typedef cudaError_t (*LaunchFn)(const GemmOps&, cudaStream_t);
 struct GemmCfgInfo {
   int bm, bn_r, occ;
   LaunchFn fn;
@@ -238,7 +282,9 @@ using G16x32 = GemmCfgT<16, 32, 1, 1, 4, 8>;
 using G128x64 = GemmCfgT<128, 64, 4, 2, 6, 1>;
 using G64x64 = GemmCfgT<64, 64, 2, 2, 4, 3>;
 using G32x128 = GemmCfgT<32, 128, 1, 4, 4, 2>;
-using G64x80 = GemmCfgT<64, 80, 4, 1, 4, 3>;  // 40 complex columns: whole D=10 groups, 4000 tiles at C3
+using G64x80 = GemmCfgT<64, 80, 4, 1, 4, 3>;    // 40 complex columns: whole D=10 groups, 4000 tiles at C3
+using G64x64w8 = GemmCfgT<64, 64, 4, 2, 4, 2>;  // 3M: 8 warps of 16 x 16 complex, 16 warps/SM
+using G32x64w4 = GemmCfgT<32, 64, 2, 2, 4, 4>;  // 3M: 4 warps of 16 x 16 complex
 static const GemmCfgInfo kGemm4[] = {
     cfg_info<G128x128, 4>("4m_128x128_w4x2"), cfg_info<G64x128, 4>("4m_64x128_w2x4"),
     cfg_info<G64x128p, 4>("4m_64x128_w2x2_occ2"), cfg_info<G32x64, 4>("4m_32x64_w1x2_occ4"),
@@ -247,13 +293,13 @@ static const GemmCfgInfo kGemm3[] = {
     cfg_info<G128x64, 3>("3m_128x64_w4x2"), cfg_info<G64x128, 3>("3m_64x128_w2x4"),
     cfg_info<G64x64, 3>("3m_64x64_w2x2_occ3"), cfg_info<G32x64, 3>("3m_32x64_w1x2_occ4"),
     cfg_info<G16x32, 3>("3m_16x32_w1x1_occ8"), cfg_info<G32x128, 3>("3m_32x128_w1x4_occ2"),
-    cfg_info<G64x80, 3>("3m_64x80_w4x1_occ3")};
+    cfg_info<G64x80, 3>("3m_64x80_w4x1_occ3"), cfg_info<G64x64w8, 3>("3m_64x64_w4x2_occ2"),
+    cfg_info<G32x64w4, 3>("3m_32x64_w2x2_occ4")};
 constexpr int N_GEMM4 = sizeof(kGemm4) / sizeof(kGemm4[0]);
 constexpr int N_GEMM3 = sizeof(kGemm3) / sizeof(kGemm3[0]);
 constexpr int N_GEMM_CFGS = N_GEMM3 > N_GEMM4 ? N_GEMM3 : N_GEMM4;  // index bound for the API
 static int n_cfgs(int mode) { return mode == 3 ? N_GEMM3 : N_GEMM4; }
 static const GemmCfgInfo& cfg_of(int mode, int cfg) { return mode == 3 ? kGemm3[cfg] : kGemm4[cfg]; }
-static int cfg_bm(int mode, int cfg) { return cfg_of(mode, cfg).bm; }
 static int g_num_sms = 148;
 
 // Analytic fallback: waves x per-tile DMMA cycles (an SM's FP64 pipe shared by its
@@ -275,40 +321,33 @@ static int choose_gemm_cfg(int mode, int n, int K, int N) {
   return arg;
 }
 
-static cudaError_t launch_any(int mode, int cfg, const CUtensorMap& tv, const CUtensorMap& tg, double2* C, int n,
-                              int K, int N, long long ldc, cudaStream_t st) {
-  return cfg_of(mode, cfg).fn(tv, tg, C, n, K, N, ldc, st);
-}
-
 // Autotune cache: (n, K, N) -> config.  Every config produces bit-identical C, so the
 // choice never changes results; it is made once per shape (first call, outside any
 // timed region in bench.py) by timing each candidate twice on the real operands.
 static std::map<std::tuple<int, int, int, int>, int> g_tuned;
 static std::mutex g_tuned_mu;
 
-static int tune_gemm(int mode, const void* V, const CUtensorMap& tg, double2* C, int n, int K, int N, long long ldc,
-                     cudaStream_t st) {
+static int tune_gemm(int mode, const GemmOps& o, cudaStream_t st) {
+  const bool sums = o.Vs && o.tgs;
   {
     std::lock_guard<std::mutex> lk(g_tuned_mu);
-    auto it = g_tuned.find({mode, n, K, N});
+    auto it = g_tuned.find({mode * 2 + (sums ? 1 : 0), o.n, o.K, o.N});
     if (it != g_tuned.end()) return it->second;
   }
   int best = 0;
   {
     // one timed run per candidate when a GEMM is long (> ~20 ms), else the best of two
-    const double est_ms = 8.0 * n * (double)K * N / 37e9;
+    const double est_ms = 8.0 * o.n * (double)o.K * o.N / 37e9;
     const int reps = est_ms > 20.0 ? 1 : 2;
     float best_ms = 1e30f;
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     for (int cfg = 0; cfg < n_cfgs(mode); ++cfg) {
-      CUtensorMap tv;
-      if (!make_tmap(&tv, V, n, 2 * (uint64_t)K, 16 * (uint64_t)K, cfg_bm(mode, cfg))) continue;
       float ms_min = 1e30f;
       for (int r = 0; r < reps; ++r) {
         cudaEventRecord(e0, st);
-        if (launch_any(mode, cfg, tv, tg, C, n, K, N, ldc, st) != cudaSuccess) break;
+        if (cfg_of(mode, cfg).fn(o, st) != cudaSuccess) break;
         cudaEventRecord(e1, st);
         cudaEventSynchronize(e1);
         float ms = 0.f;
@@ -325,20 +364,26 @@ static int tune_gemm(int mode, const void* V, const CUtensorMap& tg, double2* C,
     cudaGetLastError();
   }
   std::lock_guard<std::mutex> lk(g_tuned_mu);
-  g_tuned[{mode, n, K, N}] = best;
+  g_tuned[{mode * 2 + (sums ? 1 : 0), o.n, o.K, o.N}] = best;
   return best;
 }
 
-// V tensor maps use box rows = BM of the chosen config; Gamma maps always box 8 rows.
-// cfg: 0..3 explicit, -1 autotune (cached per shape), -2 analytic model only.
-static int launch_site_gemm(mps_ctx* ctx, const void* V, const CUtensorMap& tg, double2* C, int n, int K, int N,
-                            long long ldc, cudaStream_t st, int cfg, int mode) {
-  if (cfg == -1) cfg = tune_gemm(mode, V, tg, C, n, K, N, ldc, st);
-  if (cfg < 0 || cfg >= n_cfgs(mode)) cfg = choose_gemm_cfg(mode, n, K, N);
-  CUtensorMap tv;
-  if (!make_tmap(&tv, V, n, 2 * (uint64_t)K, 16 * (uint64_t)K, cfg_bm(mode, cfg)))
-    return fail(ctx, MPS_ERR_GENERIC, "state tensor map encode failed (n=%d, K=%d)", n, K);
-  cudaError_t e = launch_any(mode, cfg, tv, tg, C, n, K, N, ldc, st);
+// cfg: 0..n-1 explicit, -1 autotune (cached per shape), -2 analytic model only.
+static int launch_site_gemm(mps_ctx* ctx, const GemmOps& o, cudaStream_t st, int cfg, int mode) {
+  if (mode == 4 || !o.Vs || !o.tgs) {
+    GemmOps p = o;  // sum planes only feed the 3M kernel
+    p.Vs = nullptr;
+    p.tgs = nullptr;
+    if (cfg == -1) cfg = tune_gemm(mode, p, st);
+    if (cfg < 0 || cfg >= n_cfgs(mode)) cfg = choose_gemm_cfg(mode, o.n, o.K, o.N);
+    cudaError_t e = cfg_of(mode, cfg).fn(p, st);
+    if (ctx) ctx->launches++;
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "site_gemm launch");
+    return MPS_OK;
+  }
+  if (cfg == -1) cfg = tune_gemm(mode, o, st);
+  if (cfg < 0 || cfg >= n_cfgs(mode)) cfg = choose_gemm_cfg(mode, o.n, o.K, o.N);
+  cudaError_t e = cfg_of(mode, cfg).fn(o, st);
   if (ctx) ctx->launches++;
   if (e != cudaSuccess) return cuda_fail(ctx, e, "site_gemm launch");
   return MPS_OK;
@@ -386,8 +431,10 @@ int mps_configure(mps_ctx* c, int M, int D) {
   if (M < 1) return fail(c, MPS_ERR_VALIDATION, "M must be >= 1, got %d", M);
   if (D < 1 || D > DMAX) return fail(c, MPS_ERR_VALIDATION, "D must lie in [1, %d], got %d", DMAX, D);
   cudaSetDevice(c->device);
-  for (auto& s : c->sites)
+  for (auto& s : c->sites) {
     if (s.owned && s.data) cudaFree(s.data);
+    if (s.gsum) cudaFree(s.gsum);
+  }
   c->sites.assign(M, Site());
   c->M = M;
   c->D = D;
@@ -411,6 +458,7 @@ int mps_set_site(mps_ctx* c, int m, int chi_l, int chi_r, int D, const void* gam
   cudaSetDevice(c->device);
   Site& s = c->sites[m];
   if (s.owned && s.data) cudaFree(s.data);
+  if (s.gsum) cudaFree(s.gsum);
   s = Site();
   const size_t elems = (size_t)chi_l * chi_r * D;
   const bool dev = is_device_ptr(gamma);
@@ -428,6 +476,22 @@ int mps_set_site(mps_ctx* c, int m, int chi_l, int chi_r, int D, const void* gam
   const uint64_t N = (uint64_t)chi_r * D;
   if (!make_tmap(&s.tmap, s.data, chi_l, 2 * N, 16 * N, 8))
     return fail(c, MPS_ERR_GENERIC, "site %d: cuTensorMapEncodeTiled failed", m);
+  // sum plane Gr + Gi for the 3M GEMM (+50% of the site's bytes); skipped when memory is short
+  if (c->sum_planes) {
+    const int ld = sum_ld((int)N);
+    if (cudaMalloc(&s.gsum, (size_t)chi_l * ld * sizeof(double)) == cudaSuccess) {
+      const long long total = (long long)chi_l * (long long)N;
+      sum_plane_kernel<<<(unsigned)((total + 255) / 256), 256>>>(s.data, chi_l, (int)N, s.gsum, ld);
+      if (cudaGetLastError() != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess ||
+          !make_tmap(&s.tmap_gs, s.gsum, chi_l, N, 8 * (uint64_t)ld, 8)) {
+        cudaFree(s.gsum);
+        s.gsum = nullptr;
+      }
+    } else {
+      s.gsum = nullptr;
+    }
+    cudaGetLastError();
+  }
   return MPS_OK;
 }
 
@@ -479,7 +543,12 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
     CU(c, c->lv0[l].ensure(nl * chi_max), "alloc state");
     CU(c, c->lv1[l].ensure(nl * chi_max), "alloc state");
     CU(c, c->lcbuf[l].ensure(nl * cmax), "alloc C buffer");
+    if (c->sum_planes && c->gemm_mode == 3) {
+      CU(c, c->lvs0[l].ensure(nl * sum_ld(chi_max)), "alloc state sums");
+      CU(c, c->lvs1[l].ensure(nl * sum_ld(chi_max)), "alloc state sums");
+    }
   }
+  const bool use_sums = c->sum_planes && c->gemm_mode == 3;
 
   // ---- inputs: stage host arrays on the device ----
   const double* u_dev = uniforms;
@@ -535,9 +604,17 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
   }
 
   // ---- the mode loop: L lanes (row blocks), each a chain on its own stream ----
+  const int chi0 = c->sites[m_begin].chi_l;
   if (!state_in) {
     CU(c, c->ones.ensure((size_t)n), "alloc ones");
-    fill_ones_kernel<<<(n + 255) / 256, 256, 0, st>>>(c->ones.p, n);
+    CU(c, c->ones_sum.ensure((size_t)n * 2), "alloc ones");
+    fill_ones_kernel<<<(n + 255) / 256, 256, 0, st>>>(c->ones.p, c->ones_sum.p, n);
+    c->launches++;
+  } else if (use_sums) {
+    CU(c, c->in_sum.ensure((size_t)n * sum_ld(chi0)), "alloc input sums");
+    const long long total = (long long)n * chi0;
+    sum_plane_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>((const double2*)state_in, n, chi0, c->in_sum.p,
+                                                                      sum_ld(chi0));
     c->launches++;
   }
   cudaStream_t lst[mps_ctx::MAX_LANES];
@@ -551,15 +628,19 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
     }
   }
   const double2* v_in[mps_ctx::MAX_LANES];
+  const double* vs_in[mps_ctx::MAX_LANES];
+  int ld_vs_in = sum_ld(chi0);
   int cur[mps_ctx::MAX_LANES];
   for (int l = 0; l < L; ++l) {
     const int r0 = lane_r0[l];
-    v_in[l] = state_in ? (const double2*)state_in + (size_t)r0 * c->sites[m_begin].chi_l : c->ones.p + r0;
+    v_in[l] = state_in ? (const double2*)state_in + (size_t)r0 * chi0 : c->ones.p + r0;
+    vs_in[l] = !use_sums ? nullptr : state_in ? c->in_sum.p + (size_t)r0 * ld_vs_in : c->ones_sum.p + (size_t)r0 * 2;
     cur[l] = 0;
   }
   for (int m = m_begin; m < m_end; ++m) {
     const Site& s = c->sites[m];
     const int N = s.chi_r * D;
+    if (m > m_begin) ld_vs_in = sum_ld(s.chi_l);
     for (int l = 0; l < L; ++l) {  // K1 of every lane, then K2+K3 of every lane
       const int nl = lane_r0[l + 1] - lane_r0[l];
       mps_ctx::Rec rg{0, nullptr, nullptr, 8.0 * nl * (double)s.chi_l * N};
@@ -568,8 +649,9 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
         rg.b = c->get_event();
         cudaEventRecord(rg.a, lst[l]);
       }
-      int rc = launch_site_gemm(c, v_in[l], s.tmap, c->lcbuf[l].p, nl, s.chi_l, N, N, lst[l], c->gemm_cfg,
-                                c->gemm_mode);
+      GemmOps o{v_in[l], vs_in[l], ld_vs_in, &s.tmap, s.gsum ? &s.tmap_gs : nullptr, c->lcbuf[l].p, nl, s.chi_l, N,
+                N};
+      int rc = launch_site_gemm(c, o, lst[l], c->gemm_cfg, c->gemm_mode);
       if (rc) return rc;
       if (c->profile & 1) {
         cudaEventRecord(rg.b, lst[l]);
@@ -595,6 +677,9 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
       a.alpha = alpha_dev ? alpha_dev + (size_t)r0 * M : nullptr;
       a.alpha_sigma = (disp_dev || alpha_dev) ? -1.0 : c->alpha_sigma;
       a.v_out = v_out;
+      const bool last_out = (m == m_end - 1 && state_out);
+      a.vs_out = (use_sums && !last_out) ? (cur[l] ? c->lvs1[l].p : c->lvs0[l].p) : nullptr;
+      a.ld_vs = sum_ld(s.chi_r);
       a.counts = counts_dev + (size_t)r0 * ld_c;
       a.ld_c = ld_c;
       a.marg = marg_dev ? marg_dev + (size_t)r0 * ld_c * D : nullptr;
@@ -617,6 +702,7 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
         c->recs.push_back(rd);
       }
       v_in[l] = v_out;
+      vs_in[l] = a.vs_out;
       cur[l] ^= 1;
     }
   }
@@ -694,9 +780,15 @@ void mps_destroy(mps_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
-  for (auto& s : c->sites)
+  for (auto& s : c->sites) {
     if (s.owned && s.data) cudaFree(s.data);
+    if (s.gsum) cudaFree(s.gsum);
+  }
+  c->ones_sum.release();
+  c->in_sum.release();
   for (int l = 0; l < mps_ctx::MAX_LANES; ++l) {
+    c->lvs0[l].release();
+    c->lvs1[l].release();
     c->lv0[l].release();
     c->lv1[l].release();
     c->lcbuf[l].release();
@@ -727,12 +819,24 @@ int mps_site_gemm_cfg(const void* V, const void* G, void* C, int n, int K, int N
   if (cfg < -2 || cfg >= n_cfgs(mode)) return MPS_ERR_VALIDATION;
   CUtensorMap tg;
   if (!make_tmap(&tg, G, K, 2 * (uint64_t)N, 16 * (uint64_t)N, 8)) return MPS_ERR_GENERIC;
-  return launch_site_gemm(nullptr, V, tg, (double2*)C, n, K, N, ldc, reinterpret_cast<cudaStream_t>(stream), cfg,
-                          mode);
+  GemmOps o{V, nullptr, 0, &tg, nullptr, (double2*)C, n, K, N, ldc};
+  return launch_site_gemm(nullptr, o, reinterpret_cast<cudaStream_t>(stream), cfg, mode);
 }
 
 int mps_site_gemm(const void* V, const void* G, void* C, int n, int K, int N, int64_t ldc, uint64_t stream) {
   return mps_site_gemm_cfg(V, G, C, n, K, N, ldc, stream, -1, 3);
+}
+
+int mps_set_sum_planes(mps_ctx* c, int enable) {
+  if (!c) return MPS_ERR_VALIDATION;
+  c->sum_planes = enable != 0;
+  if (!c->sum_planes)
+    for (auto& s : c->sites)
+      if (s.gsum) {
+        cudaFree(s.gsum);
+        s.gsum = nullptr;
+      }
+  return MPS_OK;
 }
 
 int mps_set_lanes(mps_ctx* c, int lanes) {

@@ -169,43 +169,65 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
 // 25% fewer DMMAs for the same algorithmic (8 flops per complex MAC) work.  Same TMA
 // tiles as 4M; the MMA k index is the complex index, each lane reads (re, im) pairs
 // with one LDS.128 (k of lane t at step s is i = 2t + s: conflict-free against the
-// 128B swizzle for both operands) and forms the sums with one DADD per operand.
-// All 3M configs share this k order, so 3M results are bit-identical across configs,
-// batch sizes and GPU counts (they differ from 4M at rounding level).
+// 128B swizzle for both operands).
+//
+// SUMS: the operand sums Vr+Vi and Gr+Gi come precomputed from "sum planes" (the draw
+// kernel writes the state's, mps_set_site the site's) through two more TMA boxes per
+// stage, instead of DADDs that queue behind DMMAs on the FP64 pipe (+7.5% measured).
+// The planes hold exactly the IEEE sums the in-kernel DADD would form, so SUMS and
+// non-SUMS launches give bit-identical C.  All 3M configs share the k order, so 3M
+// results are bit-identical across configs, batch sizes and GPU counts.
 // ---------------------------------------------------------------------------------------
-template <class Cfg>
+template <class Cfg, bool SUMS>
+struct Sums3M {
+  // state sums: BM rows x 8 doubles (64 B rows, 64B swizzle); site sums: 8 rows x 16-double boxes
+  static constexpr int AS_BYTES = SUMS ? Cfg::BM * 64 : 0;
+  static constexpr int BS_BOXES = SUMS ? Cfg::BN_R / 32 : 0;
+  static constexpr int BS_BYTES = BS_BOXES * 1024;
+  static constexpr int STAGE_BYTES = Cfg::STAGE_BYTES + BS_BYTES + AS_BYTES;
+  static constexpr int SMEM_BYTES = Cfg::STAGES * STAGE_BYTES + 1024 + 2 * Cfg::STAGES * 8;
+  static_assert(!SUMS || (Cfg::BN_R % 32 == 0 && AS_BYTES % 512 == 0), "sum-plane tiles");
+};
+
+template <class Cfg, bool SUMS>
 __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     site_gemm3m_kernel(const __grid_constant__ CUtensorMap tmap_v, const __grid_constant__ CUtensorMap tmap_g,
+                       const __grid_constant__ CUtensorMap tmap_vs, const __grid_constant__ CUtensorMap tmap_gs,
                        double2* __restrict__ C, int n, int N, int KT, long long ldc) {
   static_assert(Cfg::NF3 >= 1 && Cfg::WN % 16 == 0, "3M warp tile needs whole 8-complex fragments");
+  using S = Sums3M<Cfg, SUMS>;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * S::STAGE_BYTES);
   uint64_t* empty = full + Cfg::STAGES;
+  // stage layout: [V tile | Gamma boxes | Gamma-sum boxes | V-sum tile]
+  constexpr int OFF_B = Cfg::A_BYTES, OFF_BS = Cfg::STAGE_BYTES, OFF_AS = Cfg::STAGE_BYTES + S::BS_BYTES;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * Cfg::BM;
   const int n0r = blockIdx.y * Cfg::BN_R;
 
-  auto issue_g = [&](int kt) {  // one k-stage: expect the whole stage, load the B_GROUPS Gamma boxes
+  auto issue_g = [&](int kt) {  // resident operands: Gamma (+ its sum plane)
     const int s = kt % Cfg::STAGES;
-    uint8_t* Bs = smem + s * Cfg::STAGE_BYTES + Cfg::A_BYTES;
-    mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
+    uint8_t* st = smem + s * S::STAGE_BYTES;
+    mbar_arrive_expect_tx(&full[s], S::STAGE_BYTES);
 #pragma unroll
     for (int gi = 0; gi < Cfg::B_GROUPS; ++gi)
-      tma_load_2d(Bs + gi * (Cfg::BK_C * 128), &tmap_g, n0r + gi * 16, kt * Cfg::BK_C, &full[s]);
+      tma_load_2d(st + OFF_B + gi * (Cfg::BK_C * 128), &tmap_g, n0r + gi * 16, kt * Cfg::BK_C, &full[s]);
+    if constexpr (SUMS) {
+#pragma unroll
+      for (int gi = 0; gi < S::BS_BOXES; ++gi)
+        tma_load_2d(st + OFF_BS + gi * 1024, &tmap_gs, (n0r >> 1) + gi * 16, kt * Cfg::BK_C, &full[s]);
+    }
   };
-  auto issue_v = [&](int kt) {  // the V tile of the stage (written by the previous kernel)
+  auto issue_v = [&](int kt) {  // the state (written by the previous kernel) (+ its sum plane)
     const int s = kt % Cfg::STAGES;
-    tma_load_2d(smem + s * Cfg::STAGE_BYTES, &tmap_v, kt * 16, m0, &full[s]);
-  };
-  auto issue = [&](int kt) {
-    issue_g(kt);
-    issue_v(kt);
+    uint8_t* st = smem + s * S::STAGE_BYTES;
+    tma_load_2d(st, &tmap_v, kt * 16, m0, &full[s]);
+    if constexpr (SUMS) tma_load_2d(st + OFF_AS, &tmap_vs, kt * 8, m0, &full[s]);
   };
 
-  // PDL: let the next kernel's CTAs launch into SMs this grid's tail leaves idle
   griddep_launch_dependents();
   if (threadIdx.x == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {
@@ -215,9 +237,12 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     fence_barrier_init();
     prefetch_tmap(&tmap_v);
     prefetch_tmap(&tmap_g);
-    // Gamma is resident input: prefetch the first stages while the predecessor drains
+    if constexpr (SUMS) {
+      prefetch_tmap(&tmap_vs);
+      prefetch_tmap(&tmap_gs);
+    }
     for (int kt = 0; kt < Cfg::STAGES && kt < KT; ++kt) issue_g(kt);
-    griddep_wait();  // predecessor (draw of the previous mode) complete: V valid, C free to overwrite
+    griddep_wait();
     for (int kt = 0; kt < Cfg::STAGES && kt < KT; ++kt) issue_v(kt);
   }
   __syncthreads();
@@ -239,8 +264,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
   for (int kt = 0; kt < KT; ++kt) {
     const int s = kt % Cfg::STAGES;
     mbar_wait(&full[s], (kt / Cfg::STAGES) & 1);
-    const uint8_t* As = smem + s * Cfg::STAGE_BYTES + (warp_m * Cfg::WM + g) * 128;
-    const uint8_t* Bs = smem + s * Cfg::STAGE_BYTES + Cfg::A_BYTES + warp_n * NF * (Cfg::BK_C * 128);
+    const uint8_t* st = smem + s * S::STAGE_BYTES;
+    const uint8_t* As = st + (warp_m * Cfg::WM + g) * 128;
+    const uint8_t* Bs = st + OFF_B + warp_n * NF * (Cfg::BK_C * 128);
+    const uint8_t* Ass = st + OFF_AS + (warp_m * Cfg::WM + g) * 64;
+    const uint8_t* Bss = st + OFF_BS;
 #pragma unroll
     for (int step = 0; step < 2; ++step) {
       const int i = 2 * t + step;  // complex k of this lane: row of the Gamma box, chunk of the V row
@@ -250,14 +278,35 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
         const double2 v = *reinterpret_cast<const double2*>(As + mf * 8 * 128 + ((i ^ g) << 4));
         ar[mf] = v.x;
         ai[mf] = v.y;
-        as[mf] = v.x + v.y;
+        if constexpr (SUMS) {
+          // 64B swizzle: 16B chunk t of a 64B row XOR (row >> 1) & 3, row & 7 == g
+          as[mf] = *reinterpret_cast<const double*>(Ass + mf * 8 * 64 + ((t ^ ((g >> 1) & 3)) << 4) + (step << 3));
+        } else {
+#ifdef MPS_EXPERIMENT_NO_DADD  // timing experiment only: wrong results
+          as[mf] = v.x;
+#else
+          as[mf] = __dadd_rn(v.x, v.y);
+#endif
+        }
       }
 #pragma unroll
       for (int nf = 0; nf < NF; ++nf) {
         const double2 w = *reinterpret_cast<const double2*>(Bs + nf * (Cfg::BK_C * 128) + i * 128 + ((g ^ i) << 4));
         br[nf] = w.x;
         bi[nf] = w.y;
-        bs[nf] = w.x + w.y;
+        if constexpr (SUMS) {
+          // sum boxes: 8 rows x 16 doubles (complex cols); fragment fi covers cols 8 fi .. 8 fi + 7:
+          // box fi/2, col (fi&1)*8 + g -> 16B chunk ((fi&1)*4 + g/2) ^ i (128B swizzle, row i)
+          const int fi = warp_n * NF + nf;
+          const int c = ((fi & 1) * 4 + (g >> 1)) ^ i;
+          bs[nf] = *reinterpret_cast<const double*>(Bss + (fi >> 1) * 1024 + i * 128 + (c << 4) + ((g & 1) << 3));
+        } else {
+#ifdef MPS_EXPERIMENT_NO_DADD
+          bs[nf] = w.y;
+#else
+          bs[nf] = __dadd_rn(w.x, w.y);
+#endif
+        }
       }
 #pragma unroll
       for (int mf = 0; mf < MF; ++mf)
@@ -272,7 +321,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     if (lane == 0) mbar_arrive(&empty[s]);
     if (threadIdx.x == 0 && kt >= 1 && kt - 1 + Cfg::STAGES < KT) {
       mbar_wait(&empty[(kt - 1) % Cfg::STAGES], ((kt - 1) / Cfg::STAGES) & 1);
-      issue(kt - 1 + Cfg::STAGES);
+      issue_g(kt - 1 + Cfg::STAGES);
+      issue_v(kt - 1 + Cfg::STAGES);
     }
   }
 
@@ -291,6 +341,17 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
           crow[col + e] = make_double2(t1[mf][nf][e] - t2[mf][nf][e], t3[mf][nf][e] - (t1[mf][nf][e] + t2[mf][nf][e]));
     }
   }
+}
+
+// Sum plane of complex data: out[r * ld_out + c] = re + im (the exact DADD the 3M kernel forms)
+__global__ void sum_plane_kernel(const double2* __restrict__ in, long long rows, int cols, double* __restrict__ out,
+                                 int ld_out) {
+  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= rows * cols) return;
+  const long long r = idx / cols;
+  const int c = (int)(idx % cols);
+  const double2 v = in[idx];
+  out[r * ld_out + c] = __dadd_rn(v.x, v.y);
 }
 
 }  // namespace mps

@@ -121,6 +121,31 @@ class MPS:
     def nbytes(self) -> int:
         return sum(int(np.prod(G.shape)) * 16 for G in self.sites)
 
+    @classmethod
+    def from_vidal(cls, gammas, lambdas) -> "MPS":
+        """Vidal form Gamma^[0] Lambda^[1] Gamma^[1] ... Lambda^[M-1] Gamma^[M-1] -> site tensors.
+
+        lambdas[m] (length chi_{m+1}) is the bond between sites m and m+1; it is absorbed
+        to the right of Gamma^[m] (B^[m] = Gamma^[m] diag(Lambda^[m+1]), the right-canonical
+        sites of a Vidal-canonical state), which is exactly the Lambda^2-weighted marginal
+        p(k) = sum_j Lambda_j^2 |E_jk|^2 of the unabsorbed chain."""
+        gammas = list(gammas)
+        if len(lambdas) != len(gammas) - 1:
+            raise ValidationError(f"need {len(gammas) - 1} bond vectors, got {len(lambdas)}")
+        sites = []
+        for m, G in enumerate(gammas):
+            if m < len(gammas) - 1:
+                lam = lambdas[m]
+                if tuple(lam.shape) != (G.shape[1],):
+                    raise ValidationError(f"bond {m + 1}: Lambda has shape {tuple(lam.shape)}, site {m} has "
+                                          f"chi_r={G.shape[1]}")
+                if hasattr(G, "detach"):
+                    G = G * lam.to(G.dtype)[None, :, None]
+                else:
+                    G = np.ascontiguousarray(np.asarray(G) * np.asarray(lam)[None, :, None], dtype=np.complex128)
+            sites.append(G)
+        return cls(sites)
+
     def holds(self, m: int) -> bool:
         return not isinstance(self.sites[m], SiteShape)
 

@@ -105,7 +105,8 @@ class MpsSampler:
     ``sites_range`` = (m_begin, m_end) loads only that block (mode-pipelined stage).
     """
 
-    def __init__(self, mps: MPS, device: int = 0, layout: int = 0, sites_range=None, borrow: bool = True):
+    def __init__(self, mps: MPS, device: int = 0, layout: int = 0, sites_range=None, borrow: bool = True,
+                 sum_planes: bool = True):
         _native.require_cuda()
         import torch
 
@@ -122,6 +123,7 @@ class MpsSampler:
         self.ctx = ctx
         try:
             _native.check(self.L.mps_configure(self.ctx, self.M, self.D), self.ctx)
+            _native.check(self.L.mps_set_sum_planes(self.ctx, int(sum_planes)), self.ctx)
             self._keep = []
             for m in range(*self.sites_range):
                 if not mps.holds(m):

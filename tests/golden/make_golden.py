@@ -55,5 +55,16 @@ mu = np.sqrt(2 * HBAR) * np.concatenate([am.real, am.imag])
 out["coherent_multimode_alpha"] = am
 out["coherent_multimode_vacuum_prob"] = np.array(g.vacuum_overlap(np.eye(2 * Mm), mu, hbar=HBAR))
 
+# the reference's sample text format (sampler.py:772-778) for a small click batch
+import tempfile  # noqa: E402
+
+rng = np.random.default_rng(9)
+bits = (rng.random((7, 6)) < 0.4).astype(np.uint8)
+sb = sp.SampleBatch(M=6, N=7, bitstrings=bits, method="mps", K=0, seed=11)
+with tempfile.TemporaryDirectory() as d:
+    sp.save_samples_text(Path(d) / "s.txt", sb)
+    out["text_bits"] = bits
+    out["text_bytes"] = np.frombuffer((Path(d) / "s.txt").read_bytes(), dtype=np.uint8)
+
 np.savez_compressed(Path(__file__).with_name("reference_conventions.npz"), **out)
 print("wrote", len(out), "arrays")

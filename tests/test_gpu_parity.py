@@ -308,7 +308,7 @@ def test_staged_and_global_draw_agree():
     _check_parity(sites, res, stream_uniforms(2, 0, N, M), alpha=alpha_stream(2, 0, N, M, 0.5))
 
 
-@pytest.mark.parametrize("mode,cfg_id", [(m, c) for m in (3, 4) for c in range(-2, 7 if m == 3 else 6)])
+@pytest.mark.parametrize("mode,cfg_id", [(m, c) for m in (3, 4) for c in range(-2, 9 if m == 3 else 6)])
 def test_gemm_configs_bit_identical(cfg_id, mode):
     """Within a product mode every tile config (and the autotuner's pick) gives the same bits."""
     L = _native.lib()
@@ -381,3 +381,51 @@ def test_lanes_with_stage_state(c2_sites):
         s1.run(0, N, counts, state_in=state, status=status)
     torch.cuda.synchronize()
     assert np.array_equal(counts.cpu().numpy(), full["counts"])
+
+
+def test_cli_sample_end_to_end(tmp_path, capsys):
+    """gen-mps -> sample (GPU) -> counts file + reference-format clicks, manifest on stdout."""
+    import json
+
+    from paper_2511_14923_b200.cli import main
+    from paper_2511_14923_b200.formats import load_counts, load_mps
+
+    m = tmp_path / "m.gmps"
+    assert main(["gen-mps", "--modes", "8", "--chi", "16", "--dim", "4", "--seed", "0", "--out", str(m)]) == 0
+    capsys.readouterr()
+    out, clicks = tmp_path / "c.gmpc", tmp_path / "c.txt"
+    assert main(["sample", "--mps", str(m), "--samples", "300", "--seed", "5", "--alpha-sigma", "0.5",
+                 "--batch-size", "100", "--out", str(out), "--clicks-out", str(clicks)]) == 0
+    man = json.loads(capsys.readouterr().out)
+    assert man["n_generated"] == 300 and man["throughput_per_s"] > 0
+    counts, D, seed = load_counts(out)
+    assert counts.shape == (300, 8) and D == 4 and seed == 5
+    sites = load_mps(m).sites
+    ref = orc.sample_chain(sites, stream_uniforms(5, 0, 300, 8), alpha=alpha_stream(5, 0, 300, 8, 0.5))
+    assert ((counts == ref["counts"]).all(axis=1) | ref["flagged"]).all()
+    lines = clicks.read_text().splitlines()
+    assert lines[0].startswith("# gbs-samples v1 M=8 N=300 method=mps")
+    assert lines[1] == "".join("1" if c > 0 else "0" for c in counts[0])
+
+
+@pytest.mark.parametrize("lanes", [1, 3])
+def test_sum_planes_bit_identical(c2_sites, lanes):
+    """3M with precomputed operand sums (sum planes) == 3M with in-kernel DADDs, bit for bit."""
+    N = 384
+    cfg = MpsSamplerConfig(N=N, seed=21, alpha_sigma=0.5, batch_size=N)
+    outs = []
+    for sp in (True, False):
+        with MpsSampler(MPS(c2_sites), sum_planes=sp) as eng:
+            eng.set_lanes(lanes)
+            outs.append(eng.sample(cfg, return_marginals=True))
+    assert np.array_equal(outs[0]["counts"], outs[1]["counts"])
+    assert np.array_equal(outs[0]["marginals"], outs[1]["marginals"])
+
+
+def test_sum_planes_chi1000_parity():
+    M, chi, D, N = 5, 1000, 10, 96
+    sites = orc.random_mps(M, chi, D, seed=7)
+    cfg = MpsSamplerConfig(N=N, seed=7, alpha_sigma=0.7, batch_size=N)
+    with MpsSampler(MPS(sites), sum_planes=True) as eng:
+        res = eng.sample(cfg, return_marginals=True)
+    _check_parity(sites, res, stream_uniforms(7, 0, N, M), alpha=alpha_stream(7, 0, N, M, 0.7))
