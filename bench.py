@@ -59,6 +59,15 @@ def fp64_peak():
         return 37.2, "nominal (148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz)"
 
 
+def measured_bf16():
+    for p in (ROOT / "MEASURED_PEAKS.json",):
+        try:
+            return float(json.loads(p.read_text())["bf16_tflops"]), "measured (MEASURED_PEAKS.json)"
+        except Exception:
+            pass
+    return 1590.0, "fallback (B200_PROFILING.md)"
+
+
 def ncu_traffic(cfg_name, n):
     """DRAM bytes per K1 launch from the committed ncu --set full capture of a full-chi mode
     (profiles/), with the algorithmic bytes of that same launch, or (None, None)."""
@@ -225,6 +234,8 @@ def run_pipelined(args, rank, world, local, W, K, config, dims):
     mb, me = blocks[rank]
     t_setup = time.perf_counter()
     mps = MPS.random(M, chi, D, seed=0, device=dev, block=(mb, me))
+    if args.dtype == "c64":
+        mps = mps.astype("complex64")
     block_bytes = sum(dims[m] * dims[m + 1] for m in range(mb, me)) * D * 16.0
     eng = MpsSampler(mps, device=local, sites_range=(mb, me), layout=1, sum_planes=block_bytes * 1.5 < HBM_USABLE)
     eng.set_lanes(LANES)
@@ -236,7 +247,8 @@ def run_pipelined(args, rank, world, local, W, K, config, dims):
     nsteps = W + K
     counts = torch.empty((nsteps, n, M), dtype=torch.int32, device=dev)
     status = torch.zeros((nsteps, n), dtype=torch.uint8, device=dev)
-    y = torch.empty((n, dims[me]), dtype=torch.complex128, device=dev) if rank < world - 1 else None
+    cdt = torch.complex64 if args.dtype == "c64" else torch.complex128
+    y = torch.empty((n, dims[me]), dtype=cdt, device=dev) if rank < world - 1 else None
     c_host = torch.empty((n, me - mb), dtype=torch.int32).pin_memory()
 
     def stage_for(offset, copy_out=False):
@@ -251,8 +263,8 @@ def run_pipelined(args, rank, world, local, W, K, config, dims):
 
     def pipe(offset, count, copy_out=False):
         run_pipeline(stage_for(offset, copy_out), count,
-                     recv_like=lambda: torch.empty((n, dims[mb]), dtype=torch.complex128, device=dev),
-                     send_like=lambda: torch.empty((n, dims[me]), dtype=torch.complex128, device=dev),
+                     recv_like=lambda: torch.empty((n, dims[mb]), dtype=cdt, device=dev),
+                     send_like=lambda: torch.empty((n, dims[me]), dtype=cdt, device=dev),
                      rank=rank, world=world)
 
     def barrier():
@@ -301,6 +313,17 @@ def run_pipelined(args, rank, world, local, W, K, config, dims):
     gemm_ms_avg = prof["gemm_ms"] / max(prof["gemm_launches"], 1)
     gemm_flops_avg = prof["gemm_flops"] / max(prof["gemm_launches"], 1)
     achieved = gemm_flops_avg / (gemm_ms_avg / 1e3) / 1e12 if gemm_ms_avg > 0 else 0.0
+    kernel_name = "site_gemm3m_kernel (K1, FP64 DMMA, 3M)"
+    bound_note = None
+    if args.dtype == "c64":
+        # tcgen05 kind::tf32 executes 3 passes (hi.hi, hi.lo, lo.hi) of the real-doubled
+        # product = 24 tensor flops per complex MAC; the roofline is the dense TF32 rate,
+        # half the measured dense bf16 rate (MEASURED_PEAKS.json)
+        bf16, src = measured_bf16()
+        achieved, peak = 3.0 * achieved, bf16 / 2.0
+        peak_src = f"dense TF32 = 1/2 of {src} bf16 {bf16:.0f} TFLOP/s"
+        kernel_name = "c64_gemm_kernel (K1, tcgen05 kind::tf32, 3xTF32)"
+        bound_note = "achieved counts executed tensor flops (3 passes x 8 per complex MAC)"
     step_flops = sum(site_flops(dims, D, n))
     whole_tf = K * step_flops / (ms / 1e3) / 1e12
     ok = not bool((status[W:] & 1).any().item())
@@ -309,7 +332,7 @@ def run_pipelined(args, rank, world, local, W, K, config, dims):
     line = {
         "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak" if world == 1 else "strong",
-        "vs_baseline": None, "dtype": "c128",
+        "vs_baseline": None, "dtype": args.dtype,
         "data": "synthetic (random row-orthonormal sites from per-site seeds on each stage's device, "
                 "device counter-stream uniforms and alpha)",
         "config": cfg,
@@ -335,6 +358,8 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dtype", default="c128", choices=["c128", "c64"],
+                    help="c64: complex64 chain, K1 on tcgen05 (3xTF32), parity 1e-4")
     ap.add_argument("--layout", default="auto", choices=["auto", "sharded", "pipelined"],
                     help="auto: sample-sharded when the MPS fits one GPU, else mode-pipelined")
     args = ap.parse_args()
@@ -401,6 +426,8 @@ def main():
     dev = torch.device("cuda", local)
     t_setup = time.perf_counter()
     mps = MPS.random(M, chi, D, seed=0, device=dev) if M * chi * chi * D * 16 > 2e8 else MPS.random(M, chi, D, 0)
+    if args.dtype == "c64":
+        mps = mps.astype("complex64")
     eng = MpsSampler(mps, device=local)
     eng.set_lanes(LANES)
     torch.cuda.synchronize()
@@ -505,15 +532,28 @@ def main():
     ok = bool((counts[W:] >= 0).all().item()) and not bool((status[W:] & 1).any().item())
     peak, peak_src = fp64_peak()
     traffic, traffic_note = ncu_traffic(args.config, n)
+    if args.dtype == "c64":
+        traffic, traffic_note = None, None
     gemm_ms_avg = prof["gemm_ms"] / max(prof["gemm_launches"], 1)
     gemm_flops_avg = prof["gemm_flops"] / max(prof["gemm_launches"], 1)
     achieved = gemm_flops_avg / (gemm_ms_avg / 1e3) / 1e12 if gemm_ms_avg > 0 else 0.0
+    kernel_name = "site_gemm3m_kernel (K1, FP64 DMMA, 3M)"
+    bound_note = None
+    if args.dtype == "c64":
+        # tcgen05 kind::tf32 executes 3 passes (hi.hi, hi.lo, lo.hi) of the real-doubled
+        # product = 24 tensor flops per complex MAC; the roofline is the dense TF32 rate,
+        # half the measured dense bf16 rate (MEASURED_PEAKS.json)
+        bf16, src = measured_bf16()
+        achieved, peak = 3.0 * achieved, bf16 / 2.0
+        peak_src = f"dense TF32 = 1/2 of {src} bf16 {bf16:.0f} TFLOP/s"
+        kernel_name = "c64_gemm_kernel (K1, tcgen05 kind::tf32, 3xTF32)"
+        bound_note = "achieved counts executed tensor flops (3 passes x 8 per complex MAC)"
     step_flops = sum(site_flops(dims, D, n))
     whole_tf = world * K * step_flops / (ms / 1e3) / 1e12
 
     line = {
         "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": K, "warmup": W,
-        "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+        "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
         "data": "synthetic (random row-orthonormal sites from seeds, counter-stream uniforms and alpha)",
         "config": config,
         "e2e": {"value": e2e, "unit": "samples/s", "h2d_bytes_per_step": n * M * (8 + 16) + n,
@@ -521,14 +561,15 @@ def main():
         "gpu_launches": int(launches),
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_note": traffic_note,
-                     "kernel": "site_gemm3m_kernel (K1, FP64 DMMA, 3M)",
+                     "kernel": kernel_name, "note": bound_note,
                      "peak_source": peak_src,
                      "per_launch": {"ms": gemm_ms_avg, "algorithmic_flops": gemm_flops_avg},
                      "share_of_step": prof["gemm_ms"] / ms_instr if ms_instr > 0 else None,
                      "timing": "K1 launches bracketed by CUDA events on their stream in an instrumented "
                                "repeat of the K timed steps with one lane (events would defeat PDL and "
                                "lane overlap in the clean run)",
-                     "whole_chain_tflops": whole_tf, "whole_chain_frac": whole_tf / (world * peak),
+                     "whole_chain_tflops": whole_tf,
+                     "whole_chain_frac": (3.0 if args.dtype == "c64" else 1.0) * whole_tf / (world * peak),
                      "displace_draw": {"ms_per_launch": prof["draw_ms"] / max(prof["draw_launches"], 1),
                                        "achieved_gbs": (prof["draw_bytes"] / (prof["draw_ms"] / 1e3) / 1e9)
                                        if prof["draw_ms"] > 0 else None}},

@@ -67,8 +67,9 @@ extern "C" {
 #define MPS_SITE_DEVICE_COPY 1   /* gamma is device memory: copied */
 #define MPS_SITE_DEVICE_BORROW 2 /* gamma is device memory: borrowed, caller keeps it alive */
 
-/* dtype */
+/* dtype (all sites of a context share it; state_in / state_out use the same type) */
 #define MPS_C128 0
+#define MPS_C64 1   /* complex64 chain: K1 on tcgen05 (3xTF32), draw in fp64, parity 1e-4 */
 
 /* per-sample status bits written to `status` */
 #define MPS_STATUS_FAILED 1      /* step norm sum_k p(k) not finite / not positive */
@@ -160,6 +161,17 @@ int mps_set_sum_planes(mps_ctx* ctx, int enable);
 /* K1 complex product: 3 = 3M (default), 4 = 4M.  Results of the two modes differ at
  * rounding level; each is deterministic across batch sizes and GPU counts. */
 int mps_set_gemm_mode(mps_ctx* ctx, int mode);
+/* complex64 K1 on the tcgen05 tensor cores (kind::tf32, 3xTF32 split, fp32 accumulate):
+ * C (n x N complex64) = V (n x K complex64) . G (K x N complex64).  Test/benchmark entry:
+ * builds the hi/lo operand planes in temporary memory on every call. */
+int mps_site_gemm_c64(const void* V, const void* G, void* C, int n, int K, int N, uint64_t stream);
+/* The pieces of it: tf32 hi / lo planes of a complex64 state (rows x cols -> rows x ld fp32,
+ * ld >= 2 cols, ld % 4 == 0) and of a complex64 site (K x N -> B_r^T, 2N x ld), and the
+ * GEMM on prepared planes. */
+int mps_c64_state_planes(const void* V, int rows, int cols, float* hi, float* lo, int ld, uint64_t stream);
+int mps_c64_site_planes(const void* G, int K, int N, float* hi, float* lo, int ld, uint64_t stream);
+int mps_c64_gemm_planes(const float* ahi, const float* alo, const float* bhi, const float* blo, int ld, void* C,
+                        int n, int K, int N, uint64_t stream);
 /* D x D truncated displacement matrices for `count` alphas: out[count][D][D] */
 int mps_displacement(const void* alpha, int count, int D, void* out, uint64_t stream);
 /* Uniforms of samples first..first+count-1 (count x M float64), bit-equal to

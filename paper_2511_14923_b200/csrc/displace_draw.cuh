@@ -13,6 +13,7 @@
 #pragma once
 #include <cstdint>
 
+#include "c64_gemm.cuh"
 #include "ptx.cuh"
 
 namespace mps {
@@ -150,6 +151,14 @@ struct DrawArgs {
   double2* v_out;           // n x chi_r
   double* vs_out;           // n x ld_vs sum plane (re + im) of v_out for the 3M GEMM, or null
   int ld_vs;
+  // complex64 chain (C64 instantiation): C in fp32, next state as tf32 hi/lo planes of the
+  // interleaved state (n x ld_a) or, for a stage's last mode, complex64 into v_out32
+  const float2* C32;
+  float2* v_out32;
+  float* a_hi;
+  float* a_lo;
+  int ld_a;
+  double tie_eps;           // |cdf - u| band that flags a draw (1e-10 c128, 1e-4 c64)
   int32_t* counts;          // n x ld_c
   long long ld_c;
   double* marg;             // n x ld_c x D or null
@@ -185,7 +194,43 @@ __device__ __forceinline__ double2 disp_row(const double2* T, int D, int k, cons
 // (L2 hits: the row was touched microseconds earlier).  128 threads and <= 128 regs
 // keep 4 CTAs per SM so one CTA's serial sections (D(alpha), the draw) hide behind
 // the others' streaming.
-template <int DT>
+// C element loads for both precisions (the c64 chain computes the draw in fp64 too)
+template <bool C64>
+__device__ __forceinline__ double2 load_c(const DrawArgs& A, long long idx) {
+  if constexpr (C64) {
+    const float2 v = A.C32[idx];
+    return make_double2((double)v.x, (double)v.y);
+  } else {
+    return A.C[idx];
+  }
+}
+
+// next-state store: c128 state (+ its 3M sum plane), or c64 as tf32 hi/lo planes / complex64
+template <bool C64>
+__device__ __forceinline__ void store_state(const DrawArgs& A, int b, int j, double2 v) {
+  if constexpr (C64) {
+    const float re = (float)v.x, im = (float)v.y;
+    if (A.v_out32) {
+      A.v_out32[(long long)b * A.chi_r + j] = make_float2(re, im);
+    } else {
+      float h, l;
+      const long long o = (long long)b * A.ld_a + 2 * j;
+      split_tf32(re, h, l);
+      A.a_hi[o] = h;
+      A.a_lo[o] = l;
+      split_tf32(im, h, l);
+      A.a_hi[o + 1] = h;
+      A.a_lo[o + 1] = l;
+    }
+  } else {
+    A.v_out[(long long)b * A.chi_r + j] = v;
+    // __dadd_rn: no FMA contraction with the scaling, so the plane holds exactly the sum of
+    // the stored (re, im) pair, as the GEMM's in-kernel add would form it
+    if (A.vs_out) A.vs_out[(long long)b * A.ld_vs + j] = __dadd_rn(v.x, v.y);
+  }
+}
+
+template <int DT, bool C64>
 __global__ void __launch_bounds__(DRAW_THREADS, 4)
     displace_draw_kernel(DrawArgs A) {
   __shared__ double2 T[DMAX * DMAX];
@@ -201,7 +246,7 @@ __global__ void __launch_bounds__(DRAW_THREADS, 4)
   const unsigned long long gi = (unsigned long long)(A.first_index + b);
   const long long crow = (long long)b * A.ld_c + A.m;
 
-  const double2* Cb = A.C + (long long)b * A.ldc;
+  const long long cbase = (long long)b * A.ldc;
 
   // ---- displacement matrix for (b, m): inputs only, so it runs before the PDL wait and
   //      overlaps the tail of the site GEMM that produces C ----
@@ -223,10 +268,7 @@ __global__ void __launch_bounds__(DRAW_THREADS, 4)
   __syncthreads();
 
   if (A.status[b] & ST_FAILED) {  // dead sample: zero state, count -1 (deterministic chain)
-    for (int j = tid; j < A.chi_r; j += DRAW_THREADS) {
-      A.v_out[(long long)b * A.chi_r + j] = make_double2(0.0, 0.0);
-      if (A.vs_out) A.vs_out[(long long)b * A.ld_vs + j] = 0.0;
-    }
+    for (int j = tid; j < A.chi_r; j += DRAW_THREADS) store_state<C64>(A, b, j, make_double2(0.0, 0.0));
     if (tid == 0) A.counts[crow] = -1;
     if (A.marg && tid < D) A.marg[crow * D + tid] = 0.0;
     return;
@@ -241,7 +283,7 @@ __global__ void __launch_bounds__(DRAW_THREADS, 4)
     double2 c[DR];
 #pragma unroll
     for (int d = 0; d < DR; ++d)
-      if (DT || d < D) c[d] = Cb[(long long)j * D + d];
+      if (DT || d < D) c[d] = load_c<C64>(A, cbase + (long long)j * D + d);
 #pragma unroll
     for (int k = 0; k < DR; ++k) {
       if (!DT && k >= D) break;
@@ -287,7 +329,7 @@ __global__ void __launch_bounds__(DRAW_THREADS, 4)
       }
       ksel = cnt < D - 1 ? cnt : D - 1;
       while (ksel > 0 && !(p_s[ksel] > 0.0)) --ksel;
-      if (mind <= TIE_EPS) st |= ST_FLAGGED;
+      if (mind <= A.tie_eps) st |= ST_FLAGGED;
     }
     A.status[b] = st;
     A.counts[crow] = ksel;
@@ -304,24 +346,20 @@ __global__ void __launch_bounds__(DRAW_THREADS, 4)
   }
 
   // ---- pass 2: gather + renormalise ----
-  double2* vb = A.v_out + (long long)b * A.chi_r;
   if (ks < 0) {
-    for (int j = tid; j < A.chi_r; j += DRAW_THREADS) {
-      vb[j] = make_double2(0.0, 0.0);
-      if (A.vs_out) A.vs_out[(long long)b * A.ld_vs + j] = 0.0;
-    }
+    for (int j = tid; j < A.chi_r; j += DRAW_THREADS) store_state<C64>(A, b, j, make_double2(0.0, 0.0));
     return;
   }
   for (int j = tid; j < A.chi_r; j += DRAW_THREADS) {
     double2 e;
     if (ident) {
-      e = Cb[(long long)j * D + ks];
+      e = load_c<C64>(A, cbase + (long long)j * D + ks);
     } else {
       e = make_double2(0.0, 0.0);
 #pragma unroll
       for (int d = 0; d < DR; ++d) {
         if (!DT && d >= D) break;
-        const double2 c = Cb[(long long)j * D + d];
+        const double2 c = load_c<C64>(A, cbase + (long long)j * D + d);
         const double2 tk = lds_c128(&T[ks * D + d]);
         e.x = fma(tk.x, c.x, e.x);
         e.x = fma(-tk.y, c.y, e.x);
@@ -329,11 +367,16 @@ __global__ void __launch_bounds__(DRAW_THREADS, 4)
         e.y = fma(tk.y, c.x, e.y);
       }
     }
-    const double2 v = make_double2(e.x * scale, e.y * scale);
-    vb[j] = v;
-    // __dadd_rn: no FMA contraction with the scaling above, so the plane holds exactly the
-    // sum of the stored (re, im) pair, as the GEMM's in-kernel add would form it
-    if (A.vs_out) A.vs_out[(long long)b * A.ld_vs + j] = __dadd_rn(v.x, v.y);
+    store_state<C64>(A, b, j, make_double2(e.x * scale, e.y * scale));
+  }
+}
+
+// chi = 1 complex64 starting state as tf32 planes (row pitch 4 floats): (1, 0, 0, 0) / zeros
+__global__ void fill_ones_planes_kernel(float* hi, float* lo, int n) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < 4 * n) {
+    hi[i] = (i % 4 == 0) ? 1.0f : 0.0f;
+    lo[i] = 0.0f;
   }
 }
 

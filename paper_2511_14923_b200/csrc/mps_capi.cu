@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "../../include/mps_sampler.h"
+#include "c64_gemm.cuh"
 #include "displace_draw.cuh"
 #include "site_gemm.cuh"
 
@@ -48,18 +49,23 @@ EncodeTiledFn get_encode_fn() {
 // 2-D row-major float64 matrix (rows x cols doubles, row pitch in bytes), box {box_cols, box_rows};
 // 16-double boxes use the 128B swizzle, 8-double boxes (sum planes of the state) the 64B one.
 bool make_tmap(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t pitch_bytes,
-               uint32_t box_rows, uint32_t box_cols = 16) {
+               uint32_t box_rows, uint32_t box_cols = 16, bool fp32 = false) {
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return false;
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {pitch_bytes};
   cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, box_cols == 8 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+  const uint32_t box_bytes = box_cols * (fp32 ? 4 : 8);
+  CUresult r = enc(map, fp32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   box_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
+
+// fp32 plane row pitch (floats): TMA needs 16-byte row strides
+inline int plane_ld(int cols_fp32) { return (cols_fp32 + 3) & ~3; }
 
 // sum-plane row pitch (doubles): TMA needs 16-byte row strides
 inline int sum_ld(int cols) { return (cols + 1) & ~1; }
@@ -81,6 +87,21 @@ struct Site {
   CUtensorMap tmap;
   double* gsum = nullptr;  // sum plane Gr + Gi (chi_l x sum_ld(N)) for the 3M GEMM, or null
   CUtensorMap tmap_gs;
+  bool loaded = false;
+  // complex64 sites: only the tcgen05 operand planes are kept (B_r^T hi / lo, 2N x ld fp32)
+  float* bhi = nullptr;
+  float* blo = nullptr;
+  int ld = 0;
+  void release() {
+    if (owned && data) cudaFree(data);
+    if (gsum) cudaFree(gsum);
+    if (bhi) cudaFree(bhi);
+    if (blo) cudaFree(blo);
+    data = nullptr;
+    gsum = nullptr;
+    bhi = blo = nullptr;
+    loaded = false;
+  }
 };
 
 template <class T>
@@ -128,6 +149,10 @@ struct mps_ctx {
   DevBuf<double2> lv0[MAX_LANES], lv1[MAX_LANES], lcbuf[MAX_LANES];
   DevBuf<double> lvs0[MAX_LANES], lvs1[MAX_LANES];  // state sum planes (3M operand sums)
   bool sum_planes = true;                           // feed the 3M GEMM precomputed sums
+  int dtype = -1;                                   // MPS_C128 / MPS_C64, fixed by the first site
+  DevBuf<float> la_hi[2][MAX_LANES], la_lo[2][MAX_LANES];  // c64 state planes (ping-pong)
+  DevBuf<float2> lc32[MAX_LANES];                   // c64 C buffer
+  DevBuf<float> ones_hi, ones_lo, in_hi, in_lo;
   DevBuf<double> ones_sum, in_sum;
   // workspaces
   DevBuf<double2> ones, alpha_d, disp_d;
@@ -389,6 +414,32 @@ static int launch_site_gemm(mps_ctx* ctx, const GemmOps& o, cudaStream_t st, int
   return MPS_OK;
 }
 
+// ---- complex64 K1 (tcgen05, 3xTF32) --------------------------------------------------------
+using C64Big = C64Cfg<256, 2>;
+
+// C (n x N complex64) = A planes (n x ld fp32, hi/lo of the interleaved state) . B_r planes
+static cudaError_t launch_c64_gemm(const float* ahi, const float* alo, const float* bhi, const float* blo, int ld,
+                                   float* C, int n, int K, int N, long long ldc_f, cudaStream_t st) {
+  using Cfg = C64Big;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(c64_gemm_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Cfg::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  CUtensorMap tah, tal, tbh, tbl;
+  const uint64_t cols = 2 * (uint64_t)K, pitch = 4 * (uint64_t)ld;
+  if (!make_tmap(&tah, ahi, n, cols, pitch, Cfg::BM, 32, true) || !make_tmap(&tal, alo, n, cols, pitch, Cfg::BM, 32, true) ||
+      !make_tmap(&tbh, bhi, 2 * (uint64_t)N, cols, pitch, Cfg::BN, 32, true) ||
+      !make_tmap(&tbl, blo, 2 * (uint64_t)N, cols, pitch, Cfg::BN, 32, true))
+    return cudaErrorInvalidValue;
+  dim3 grid((n + Cfg::BM - 1) / Cfg::BM, (2 * N + Cfg::BN - 1) / Cfg::BN);
+  const int KB = (int)((cols + Cfg::BK - 1) / Cfg::BK);
+  return launch_pdl(c64_gemm_kernel<Cfg>, grid, dim3(Cfg::THREADS), Cfg::SMEM_BYTES, st, tah, tal, tbh, tbl, C, n,
+                    2 * N, KB, ldc_f);
+}
+
 extern "C" {
 
 int mps_create(int n_dev, const int* dev_ids, int layout, mps_ctx** out) {
@@ -431,11 +482,9 @@ int mps_configure(mps_ctx* c, int M, int D) {
   if (M < 1) return fail(c, MPS_ERR_VALIDATION, "M must be >= 1, got %d", M);
   if (D < 1 || D > DMAX) return fail(c, MPS_ERR_VALIDATION, "D must lie in [1, %d], got %d", DMAX, D);
   cudaSetDevice(c->device);
-  for (auto& s : c->sites) {
-    if (s.owned && s.data) cudaFree(s.data);
-    if (s.gsum) cudaFree(s.gsum);
-  }
+  for (auto& s : c->sites) s.release();
   c->sites.assign(M, Site());
+  c->dtype = -1;
   c->M = M;
   c->D = D;
   return MPS_OK;
@@ -447,21 +496,56 @@ int mps_set_site(mps_ctx* c, int m, int chi_l, int chi_r, int D, const void* gam
   if (m < 0 || m >= c->M) return fail(c, MPS_ERR_VALIDATION, "site index %d outside [0, %d)", m, c->M);
   if (D != c->D) return fail(c, MPS_ERR_VALIDATION, "site %d: D=%d but the chain has D=%d", m, D, c->D);
   if (chi_l < 1 || chi_r < 1) return fail(c, MPS_ERR_VALIDATION, "site %d: bond dims must be >= 1", m);
-  if (dtype != MPS_C128) return fail(c, MPS_ERR_VALIDATION, "site %d: only complex128 (dtype 0) is supported", m);
+  if (dtype != MPS_C128 && dtype != MPS_C64)
+    return fail(c, MPS_ERR_VALIDATION, "site %d: dtype %d is neither complex128 (0) nor complex64 (1)", m, dtype);
+  if (c->dtype >= 0 && c->dtype != dtype)
+    return fail(c, MPS_ERR_VALIDATION, "site %d: dtype %d differs from the chain's %d", m, dtype, c->dtype);
   if (!gamma) return fail(c, MPS_ERR_VALIDATION, "site %d: null tensor", m);
-  if (m > 0 && c->sites[m - 1].data && c->sites[m - 1].chi_r != chi_l)
+  if (m > 0 && c->sites[m - 1].loaded && c->sites[m - 1].chi_r != chi_l)
     return fail(c, MPS_ERR_VALIDATION, "site %d: chi_l=%d != chi_r=%d of site %d", m, chi_l, c->sites[m - 1].chi_r,
                 m - 1);
-  if (m + 1 < c->M && c->sites[m + 1].data && c->sites[m + 1].chi_l != chi_r)
+  if (m + 1 < c->M && c->sites[m + 1].loaded && c->sites[m + 1].chi_l != chi_r)
     return fail(c, MPS_ERR_VALIDATION, "site %d: chi_r=%d != chi_l=%d of site %d", m, chi_r, c->sites[m + 1].chi_l,
                 m + 1);
   cudaSetDevice(c->device);
   Site& s = c->sites[m];
-  if (s.owned && s.data) cudaFree(s.data);
-  if (s.gsum) cudaFree(s.gsum);
+  s.release();
   s = Site();
   const size_t elems = (size_t)chi_l * chi_r * D;
   const bool dev = is_device_ptr(gamma);
+  if (dtype == MPS_C64) {
+    // keep only the tcgen05 operand planes of B_r^T (2N x ld fp32, hi / lo)
+    const int N = chi_r * D, ld = plane_ld(2 * chi_l);
+    const float2* src = (const float2*)gamma;
+    float2* tmp = nullptr;
+    if (!dev) {
+      CU(c, cudaMalloc(&tmp, elems * sizeof(float2)), "cudaMalloc(site staging)");
+      CU(c, cudaMemcpy(tmp, gamma, elems * sizeof(float2), cudaMemcpyHostToDevice), "copy site");
+      src = tmp;
+    }
+    cudaError_t e1 = cudaMalloc(&s.bhi, (size_t)2 * N * ld * sizeof(float));
+    cudaError_t e2 = e1 == cudaSuccess ? cudaMalloc(&s.blo, (size_t)2 * N * ld * sizeof(float)) : e1;
+    if (e2 != cudaSuccess) {
+      if (tmp) cudaFree(tmp);
+      s.release();
+      return cuda_fail(c, e2, "cudaMalloc(c64 site planes)");
+    }
+    const long long t = (long long)2 * N * ld;
+    c64_site_planes_kernel<<<(unsigned)((t + 255) / 256), 256>>>(src, chi_l, N, s.bhi, s.blo, ld);
+    cudaError_t e3 = cudaGetLastError();
+    if (e3 == cudaSuccess) e3 = cudaDeviceSynchronize();
+    if (tmp) cudaFree(tmp);
+    if (e3 != cudaSuccess) {
+      s.release();
+      return cuda_fail(c, e3, "c64 site planes");
+    }
+    s.ld = ld;
+    s.chi_l = chi_l;
+    s.chi_r = chi_r;
+    s.loaded = true;
+    c->dtype = MPS_C64;
+    return MPS_OK;
+  }
   if (flags == MPS_SITE_DEVICE_BORROW) {
     if (!dev) return fail(c, MPS_ERR_VALIDATION, "site %d: BORROW needs a device pointer", m);
     s.data = (double2*)gamma;
@@ -473,6 +557,8 @@ int mps_set_site(mps_ctx* c, int m, int chi_l, int chi_r, int D, const void* gam
   }
   s.chi_l = chi_l;
   s.chi_r = chi_r;
+  s.loaded = true;
+  c->dtype = MPS_C128;
   const uint64_t N = (uint64_t)chi_r * D;
   if (!make_tmap(&s.tmap, s.data, chi_l, 2 * N, 16 * N, 8))
     return fail(c, MPS_ERR_GENERIC, "site %d: cuTensorMapEncodeTiled failed", m);
@@ -516,7 +602,7 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
   if (!counts) return fail(c, MPS_ERR_VALIDATION, "counts output is required");
   if (ld_c < c->M || (uniforms && ld_u < c->M)) return fail(c, MPS_ERR_VALIDATION, "row strides must be >= M");
   for (int m = m_begin; m < m_end; ++m)
-    if (!c->sites[m].data) return fail(c, MPS_ERR_VALIDATION, "site %d not loaded", m);
+    if (!c->sites[m].loaded) return fail(c, MPS_ERR_VALIDATION, "site %d not loaded", m);
   for (int m = m_begin + 1; m < m_end; ++m)
     if (c->sites[m].chi_l != c->sites[m - 1].chi_r)
       return fail(c, MPS_ERR_VALIDATION, "bond mismatch between sites %d and %d", m - 1, m);
@@ -538,8 +624,17 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
   int L = std::max(1, std::min(c->lanes, n / 64));
   int lane_r0[mps_ctx::MAX_LANES + 1];
   for (int l = 0; l <= L; ++l) lane_r0[l] = (int)((long long)n * l / L);
+  const bool c64 = c->dtype == MPS_C64;
   for (int l = 0; l < L; ++l) {
     const size_t nl = (size_t)(lane_r0[l + 1] - lane_r0[l]);
+    if (c64) {
+      for (int w = 0; w < 2; ++w) {
+        CU(c, c->la_hi[w][l].ensure(nl * plane_ld(2 * chi_max)), "alloc c64 state planes");
+        CU(c, c->la_lo[w][l].ensure(nl * plane_ld(2 * chi_max)), "alloc c64 state planes");
+      }
+      CU(c, c->lc32[l].ensure(nl * cmax), "alloc c64 C buffer");
+      continue;
+    }
     CU(c, c->lv0[l].ensure(nl * chi_max), "alloc state");
     CU(c, c->lv1[l].ensure(nl * chi_max), "alloc state");
     CU(c, c->lcbuf[l].ensure(nl * cmax), "alloc C buffer");
@@ -548,7 +643,7 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
       CU(c, c->lvs1[l].ensure(nl * sum_ld(chi_max)), "alloc state sums");
     }
   }
-  const bool use_sums = c->sum_planes && c->gemm_mode == 3;
+  const bool use_sums = !c64 && c->sum_planes && c->gemm_mode == 3;
 
   // ---- inputs: stage host arrays on the device ----
   const double* u_dev = uniforms;
@@ -605,7 +700,21 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
 
   // ---- the mode loop: L lanes (row blocks), each a chain on its own stream ----
   const int chi0 = c->sites[m_begin].chi_l;
-  if (!state_in) {
+  if (c64) {
+    if (!state_in) {
+      CU(c, c->ones_hi.ensure((size_t)n * 4), "alloc ones");
+      CU(c, c->ones_lo.ensure((size_t)n * 4), "alloc ones");
+      fill_ones_planes_kernel<<<(4 * n + 255) / 256, 256, 0, st>>>(c->ones_hi.p, c->ones_lo.p, n);
+    } else {
+      const int ld0 = plane_ld(2 * chi0);
+      CU(c, c->in_hi.ensure((size_t)n * ld0), "alloc input planes");
+      CU(c, c->in_lo.ensure((size_t)n * ld0), "alloc input planes");
+      const long long t = (long long)n * ld0;
+      split_planes_kernel<<<(unsigned)((t + 255) / 256), 256, 0, st>>>((const float2*)state_in, n, chi0, c->in_hi.p,
+                                                                        c->in_lo.p, ld0);
+    }
+    c->launches++;
+  } else if (!state_in) {
     CU(c, c->ones.ensure((size_t)n), "alloc ones");
     CU(c, c->ones_sum.ensure((size_t)n * 2), "alloc ones");
     fill_ones_kernel<<<(n + 255) / 256, 256, 0, st>>>(c->ones.p, c->ones_sum.p, n);
@@ -631,11 +740,18 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
   const double* vs_in[mps_ctx::MAX_LANES];
   int ld_vs_in = sum_ld(chi0);
   int cur[mps_ctx::MAX_LANES];
+  const float *a_hi[mps_ctx::MAX_LANES], *a_lo[mps_ctx::MAX_LANES];  // c64 state planes in
   for (int l = 0; l < L; ++l) {
     const int r0 = lane_r0[l];
+    cur[l] = 0;
+    if (c64) {
+      const int ld0 = state_in ? plane_ld(2 * chi0) : 4;
+      a_hi[l] = (state_in ? c->in_hi.p : c->ones_hi.p) + (size_t)r0 * ld0;
+      a_lo[l] = (state_in ? c->in_lo.p : c->ones_lo.p) + (size_t)r0 * ld0;
+      continue;
+    }
     v_in[l] = state_in ? (const double2*)state_in + (size_t)r0 * chi0 : c->ones.p + r0;
     vs_in[l] = !use_sums ? nullptr : state_in ? c->in_sum.p + (size_t)r0 * ld_vs_in : c->ones_sum.p + (size_t)r0 * 2;
-    cur[l] = 0;
   }
   for (int m = m_begin; m < m_end; ++m) {
     const Site& s = c->sites[m];
@@ -649,10 +765,17 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
         rg.b = c->get_event();
         cudaEventRecord(rg.a, lst[l]);
       }
-      GemmOps o{v_in[l], vs_in[l], ld_vs_in, &s.tmap, s.gsum ? &s.tmap_gs : nullptr, c->lcbuf[l].p, nl, s.chi_l, N,
-                N};
-      int rc = launch_site_gemm(c, o, lst[l], c->gemm_cfg, c->gemm_mode);
-      if (rc) return rc;
+      if (c64) {
+        cudaError_t e = launch_c64_gemm(a_hi[l], a_lo[l], s.bhi, s.blo, s.ld, (float*)c->lc32[l].p, nl, s.chi_l, N,
+                                        2LL * N, lst[l]);
+        c->launches++;
+        if (e != cudaSuccess) return cuda_fail(c, e, "c64 site_gemm launch");
+      } else {
+        GemmOps o{v_in[l], vs_in[l], ld_vs_in, &s.tmap, s.gsum ? &s.tmap_gs : nullptr, c->lcbuf[l].p, nl, s.chi_l, N,
+                  N};
+        int rc = launch_site_gemm(c, o, lst[l], c->gemm_cfg, c->gemm_mode);
+        if (rc) return rc;
+      }
       if (c->profile & 1) {
         cudaEventRecord(rg.b, lst[l]);
         c->recs.push_back(rg);
@@ -660,10 +783,17 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
     }
     for (int l = 0; l < L; ++l) {
       const int r0 = lane_r0[l], nl = lane_r0[l + 1] - r0;
-      double2* v_out = (m == m_end - 1 && state_out) ? (double2*)state_out + (size_t)r0 * s.chi_r
-                                                      : (cur[l] ? c->lv1[l].p : c->lv0[l].p);
+      const bool last_out = (m == m_end - 1 && state_out);
+      double2* v_out = c64 ? nullptr
+                           : last_out ? (double2*)state_out + (size_t)r0 * s.chi_r : (cur[l] ? c->lv1[l].p : c->lv0[l].p);
       DrawArgs a;
-      a.C = c->lcbuf[l].p;
+      a.C = c64 ? nullptr : c->lcbuf[l].p;
+      a.C32 = c64 ? c->lc32[l].p : nullptr;
+      a.v_out32 = (c64 && last_out) ? (float2*)state_out + (size_t)r0 * s.chi_r : nullptr;
+      a.a_hi = (c64 && !last_out) ? c->la_hi[cur[l]][l].p : nullptr;
+      a.a_lo = (c64 && !last_out) ? c->la_lo[cur[l]][l].p : nullptr;
+      a.ld_a = plane_ld(2 * s.chi_r);
+      a.tie_eps = c64 ? 1e-4 : TIE_EPS;
       a.ldc = N;
       a.chi_r = s.chi_r;
       a.D = D;
@@ -677,7 +807,6 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
       a.alpha = alpha_dev ? alpha_dev + (size_t)r0 * M : nullptr;
       a.alpha_sigma = (disp_dev || alpha_dev) ? -1.0 : c->alpha_sigma;
       a.v_out = v_out;
-      const bool last_out = (m == m_end - 1 && state_out);
       a.vs_out = (use_sums && !last_out) ? (cur[l] ? c->lvs1[l].p : c->lvs0[l].p) : nullptr;
       a.ld_vs = sum_ld(s.chi_r);
       a.counts = counts_dev + (size_t)r0 * ld_c;
@@ -692,8 +821,13 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
         cudaEventRecord(rd.a, lst[l]);
       }
       {
-        void (*dk)(DrawArgs) = (D == 10) ? displace_draw_kernel<10> : (D == 4) ? displace_draw_kernel<4>
-                                                                                 : displace_draw_kernel<0>;
+        void (*dk)(DrawArgs);
+        if (c64)
+          dk = (D == 10) ? displace_draw_kernel<10, true> : (D == 4) ? displace_draw_kernel<4, true>
+                                                                     : displace_draw_kernel<0, true>;
+        else
+          dk = (D == 10) ? displace_draw_kernel<10, false> : (D == 4) ? displace_draw_kernel<4, false>
+                                                                      : displace_draw_kernel<0, false>;
         CU(c, launch_pdl(dk, dim3(nl), dim3(DRAW_THREADS), 0, lst[l], a), "displace_draw launch");
       }
       c->launches++;
@@ -703,6 +837,8 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
       }
       v_in[l] = v_out;
       vs_in[l] = a.vs_out;
+      a_hi[l] = a.a_hi;
+      a_lo[l] = a.a_lo;
       cur[l] ^= 1;
     }
   }
@@ -780,10 +916,17 @@ void mps_destroy(mps_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
-  for (auto& s : c->sites) {
-    if (s.owned && s.data) cudaFree(s.data);
-    if (s.gsum) cudaFree(s.gsum);
-  }
+  for (auto& s : c->sites) s.release();
+  for (int w = 0; w < 2; ++w)
+    for (int l = 0; l < mps_ctx::MAX_LANES; ++l) {
+      c->la_hi[w][l].release();
+      c->la_lo[w][l].release();
+    }
+  for (int l = 0; l < mps_ctx::MAX_LANES; ++l) c->lc32[l].release();
+  c->ones_hi.release();
+  c->ones_lo.release();
+  c->in_hi.release();
+  c->in_lo.release();
   c->ones_sum.release();
   c->in_sum.release();
   for (int l = 0; l < mps_ctx::MAX_LANES; ++l) {
@@ -825,6 +968,58 @@ int mps_site_gemm_cfg(const void* V, const void* G, void* C, int n, int K, int N
 
 int mps_site_gemm(const void* V, const void* G, void* C, int n, int K, int N, int64_t ldc, uint64_t stream) {
   return mps_site_gemm_cfg(V, G, C, n, K, N, ldc, stream, -1, 3);
+}
+
+int mps_c64_state_planes(const void* V, int rows, int cols, float* hi, float* lo, int ld, uint64_t stream) {
+  if (!V || !hi || !lo || rows < 1 || cols < 1 || ld < 2 * cols || ld % 4) return MPS_ERR_VALIDATION;
+  const long long t = (long long)rows * ld;
+  split_planes_kernel<<<(unsigned)((t + 255) / 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      (const float2*)V, rows, cols, hi, lo, ld);
+  return cudaGetLastError() == cudaSuccess ? MPS_OK : MPS_ERR_GENERIC;
+}
+
+int mps_c64_site_planes(const void* G, int K, int N, float* hi, float* lo, int ld, uint64_t stream) {
+  if (!G || !hi || !lo || K < 1 || N < 1 || ld < 2 * K || ld % 4) return MPS_ERR_VALIDATION;
+  const long long t = (long long)2 * N * ld;
+  c64_site_planes_kernel<<<(unsigned)((t + 255) / 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      (const float2*)G, K, N, hi, lo, ld);
+  return cudaGetLastError() == cudaSuccess ? MPS_OK : MPS_ERR_GENERIC;
+}
+
+int mps_c64_gemm_planes(const float* ahi, const float* alo, const float* bhi, const float* blo, int ld, void* C, int n,
+                        int K, int N, uint64_t stream) {
+  if (!ahi || !alo || !bhi || !blo || !C || n < 1 || K < 1 || N < 1 || ld < 2 * K || ld % 4)
+    return MPS_ERR_VALIDATION;
+  return launch_c64_gemm(ahi, alo, bhi, blo, ld, (float*)C, n, K, N, 2LL * N, reinterpret_cast<cudaStream_t>(stream)) ==
+                 cudaSuccess
+             ? MPS_OK
+             : MPS_ERR_GENERIC;
+}
+
+int mps_site_gemm_c64(const void* V, const void* G, void* C, int n, int K, int N, uint64_t stream) {
+  if (!V || !G || !C || n < 1 || K < 1 || N < 1) return MPS_ERR_VALIDATION;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int ld = plane_ld(2 * K);
+  float *ahi = nullptr, *alo = nullptr, *bhi = nullptr, *blo = nullptr;
+  const size_t a_bytes = (size_t)n * ld * 4, b_bytes = (size_t)2 * N * ld * 4;
+  if (cudaMallocAsync(&ahi, a_bytes, st) != cudaSuccess || cudaMallocAsync(&alo, a_bytes, st) != cudaSuccess ||
+      cudaMallocAsync(&bhi, b_bytes, st) != cudaSuccess || cudaMallocAsync(&blo, b_bytes, st) != cudaSuccess) {
+    cudaGetLastError();
+    return MPS_ERR_RESOURCE;
+  }
+  const long long at = (long long)n * ld, bt = (long long)2 * N * ld;
+  split_planes_kernel<<<(unsigned)((at + 255) / 256), 256, 0, st>>>((const float2*)V, n, K, ahi, alo, ld);
+  c64_site_planes_kernel<<<(unsigned)((bt + 255) / 256), 256, 0, st>>>((const float2*)G, K, N, bhi, blo, ld);
+  cudaError_t e = launch_c64_gemm(ahi, alo, bhi, blo, ld, (float*)C, n, K, N, 2LL * N, st);
+  cudaFreeAsync(ahi, st);
+  cudaFreeAsync(alo, st);
+  cudaFreeAsync(bhi, st);
+  cudaFreeAsync(blo, st);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return MPS_ERR_GENERIC;
+  }
+  return cudaGetLastError() == cudaSuccess ? MPS_OK : MPS_ERR_GENERIC;
 }
 
 int mps_set_sum_planes(mps_ctx* c, int enable) {

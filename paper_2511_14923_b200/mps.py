@@ -89,8 +89,11 @@ class MPS:
             shape = tuple(G.shape)
             if len(shape) != 3:
                 raise ValidationError(f"site {m}: expected (chi_l, chi_r, D), got shape {shape}")
-            if str(G.dtype) not in ("complex128", "torch.complex128"):
-                raise ValidationError(f"site {m}: dtype {G.dtype} is not complex128")
+            dt = str(G.dtype).replace("torch.", "")
+            if dt not in ("complex128", "complex64"):
+                raise ValidationError(f"site {m}: dtype {G.dtype} is neither complex128 nor complex64")
+            if m > 0 and dt != self.dtype:
+                raise ValidationError(f"site {m}: dtype {dt} differs from site 0's {self.dtype}")
             if D is None:
                 D = shape[2]
             elif shape[2] != D:
@@ -100,6 +103,25 @@ class MPS:
             prev = shape[1]
         if self.sites[0].shape[0] != 1:
             raise ValidationError("chi_0 must be 1")
+
+    @property
+    def dtype(self) -> str:
+        """"complex128" or "complex64" (all sites share it)."""
+        return str(self.sites[0].dtype).replace("torch.", "")
+
+    def astype(self, dtype: str) -> "MPS":
+        """Copy with every materialised site cast to complex64 / complex128."""
+        out = []
+        for G in self.sites:
+            if isinstance(G, SiteShape):
+                out.append(SiteShape(G.shape, dtype))
+            elif hasattr(G, "detach"):
+                import torch
+
+                out.append(G.to(getattr(torch, dtype)))
+            else:
+                out.append(np.ascontiguousarray(G, dtype=dtype))
+        return MPS(out)
 
     @property
     def M(self) -> int:

@@ -125,12 +125,14 @@ class MpsSampler:
             _native.check(self.L.mps_configure(self.ctx, self.M, self.D), self.ctx)
             _native.check(self.L.mps_set_sum_planes(self.ctx, int(sum_planes)), self.ctx)
             self._keep = []
+            self.dtype = mps.dtype
+            dcode = _native.MPS_C64 if self.dtype == "complex64" else _native.MPS_C128
             for m in range(*self.sites_range):
                 if not mps.holds(m):
                     raise ValidationError(f"site {m} is in this context's range but not materialised")
                 G = mps.sites[m]
                 if isinstance(G, np.ndarray):
-                    G = np.ascontiguousarray(G, dtype=np.complex128)
+                    G = np.ascontiguousarray(G, dtype=self.dtype)
                     flags = _native.MPS_SITE_HOST
                 else:
                     G = G.contiguous()
@@ -138,8 +140,7 @@ class MpsSampler:
                     if borrow:
                         self._keep.append(G)
                 chl, chr_, D = (int(s) for s in G.shape)
-                _native.check(self.L.mps_set_site(self.ctx, m, chl, chr_, D, _ptr(G), flags, _native.MPS_C128),
-                              self.ctx)
+                _native.check(self.L.mps_set_site(self.ctx, m, chl, chr_, D, _ptr(G), flags, dcode), self.ctx)
         except Exception:
             self.close()
             raise

@@ -94,7 +94,9 @@ def test_mps_container_validation():
     with pytest.raises(ValidationError):
         MPS([sites[0], sites[2]])  # bond mismatch
     with pytest.raises(ValidationError):
-        MPS([s.astype(np.complex64) for s in sites])
+        MPS([s.real.copy() for s in sites])  # real dtype
+    with pytest.raises(ValidationError):
+        MPS([sites[0].astype(np.complex64)] + sites[1:])  # mixed dtypes
     with pytest.raises(ValidationError):
         MPS(sites[1:])  # chi_0 != 1
 

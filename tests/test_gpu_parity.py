@@ -429,3 +429,84 @@ def test_sum_planes_chi1000_parity():
     with MpsSampler(MPS(sites), sum_planes=True) as eng:
         res = eng.sample(cfg, return_marginals=True)
     _check_parity(sites, res, stream_uniforms(7, 0, N, M), alpha=alpha_stream(7, 0, N, M, 0.7))
+
+
+# ------------------------------------------------------------------ complex64 (tcgen05)
+
+
+@pytest.mark.parametrize("n,K,N", [(1, 1, 4), (100, 16, 40), (130, 37, 90), (257, 250, 2500), (1024, 1000, 10000)])
+def test_site_gemm_c64_tcgen05_vs_fp64(n, K, N):
+    """3xTF32 tcgen05 complex GEMM vs an fp64 product of the same complex64 inputs."""
+    L = _native.lib()
+    g = torch.Generator(device="cuda").manual_seed(n + 3 * K)
+    V = torch.randn(n, K, dtype=torch.complex64, device="cuda", generator=g)
+    G = torch.randn(K, N, dtype=torch.complex64, device="cuda", generator=g)
+    C = torch.full((n, N), complex(np.nan, np.nan), dtype=torch.complex64, device="cuda")
+    assert L.mps_site_gemm_c64(V.data_ptr(), G.data_ptr(), C.data_ptr(), n, K, N, 0) == 0
+    torch.cuda.synchronize()
+    ref = V.to(torch.complex128) @ G.to(torch.complex128)
+    err = (C.to(torch.complex128) - ref).abs().max().item()
+    scale = (V.abs().max() * G.abs().max()).item() * np.sqrt(K)
+    assert err <= 2e-5 * scale, (err, scale)
+
+
+C64_TOL = 1e-4  # north star: marginals within 1e-4 in complex64
+
+
+def _check_parity_c64(sites64, res, u, alpha=None):
+    """c64 chain vs the c128 oracle on the same (complex64-rounded) sites."""
+    sites = [np.asarray(s, dtype=np.complex128) for s in sites64]
+    ref_forced = orc.sample_chain(sites, u, alpha=alpha, forced=res["counts"], return_marginals=True)
+    err = np.abs(res["marginals"] - ref_forced["marginals"]).max()
+    assert err <= C64_TOL, f"max |p_gpu - p_cpu| = {err}"
+    free = orc.sample_chain(sites, u, alpha=alpha)
+    flagged = (res["status"] & _native.MPS_STATUS_FLAGGED) != 0
+    mism = (res["counts"] != free["counts"]).any(axis=1)
+    assert not (mism & ~flagged).any(), "c64 counts differ on samples not flagged within 1e-4 of a CDF boundary"
+    return err
+
+
+@pytest.mark.parametrize("name,M,chi,D,N,n", [("c1", 8, 16, 4, 400, 100), ("c2", 16, 100, 10, 400, 100),
+                                              ("chi1000", 5, 1000, 10, 128, 128)])
+def test_c64_chain_parity(name, M, chi, D, N, n):
+    sites = [s.astype(np.complex64) for s in orc.random_mps(M, chi, D, seed=3)]
+    cfg = MpsSamplerConfig(N=N, seed=4, alpha_sigma=0.5, batch_size=n)
+    with MpsSampler(MPS(sites)) as eng:
+        assert eng.dtype == "complex64"
+        res = eng.sample(cfg, return_marginals=True)
+    err = _check_parity_c64(sites, res, stream_uniforms(4, 0, N, M), alpha=alpha_stream(4, 0, N, M, 0.5))
+    assert err < 1e-5  # in practice 3xTF32 lands ~1e-6 from the fp64 chain
+
+
+def test_c64_lane_and_batch_invariance(c2_sites):
+    sites = [s.astype(np.complex64) for s in c2_sites]
+    outs = []
+    with MpsSampler(MPS(sites)) as eng:
+        for lanes, B in ((1, 300), (3, 300), (2, 64)):
+            eng.set_lanes(lanes)
+            outs.append(eng.sample(MpsSamplerConfig(N=300, seed=2, alpha_sigma=0.5, batch_size=B),
+                                   return_marginals=True))
+    for o in outs[1:]:
+        assert np.array_equal(o["counts"], outs[0]["counts"])
+        assert np.array_equal(o["marginals"], outs[0]["marginals"])
+
+
+def test_c64_stage_split(c2_sites):
+    N, M, cut = 200, 16, 6
+    sites = [s.astype(np.complex64) for s in c2_sites]
+    mps = MPS(sites)
+    cfg = MpsSamplerConfig(N=N, seed=5, alpha_sigma=0.5, batch_size=N)
+    with MpsSampler(mps) as eng:
+        full = eng.sample(cfg)
+    counts = torch.empty((N, M), dtype=torch.int32, device="cuda")
+    status = torch.zeros(N, dtype=torch.uint8, device="cuda")
+    state = torch.empty((N, mps.bond_dims[cut]), dtype=torch.complex64, device="cuda")
+    with MpsSampler(mps, sites_range=(0, cut)) as s0, MpsSampler(mps, sites_range=(cut, M)) as s1:
+        for e in (s0, s1):
+            e.set_streams(5, 0.5)
+        s0.run(0, N, counts, state_out=state, status=status)
+        s1.run(0, N, counts, state_in=state, status=status)
+    torch.cuda.synchronize()
+    # the hand-off rounds the state to complex64 exactly as the in-context chain stores it
+    # before splitting into tf32 planes, so the split chain reproduces the full one
+    assert np.array_equal(counts.cpu().numpy(), full["counts"])

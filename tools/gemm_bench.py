@@ -44,5 +44,20 @@ for name in sys.argv[1:] or list(SHAPES):
             err = ((C - ref).abs().max() / ref.abs().max()).item()
             print(json.dumps({"shape": name, "mode": mode, "cfg": cfg, "ms": ms, "tflops": flops / ms / 1e9,
                               "rel_err": err}), flush=True)
-    del V, G, C, ref
+    # complex64 on tcgen05 (3xTF32), planes prepared once, GEMM timed alone
+    ld = (2 * K + 3) & ~3
+    V32, G32 = V.to(torch.complex64), G.to(torch.complex64)
+    ahi = torch.empty(n, ld, device="cuda"); alo = torch.empty_like(ahi)
+    bhi = torch.empty(2 * N, ld, device="cuda"); blo = torch.empty_like(bhi)
+    C32 = torch.empty(n, N, dtype=torch.complex64, device="cuda")
+    assert L.mps_c64_state_planes(V32.data_ptr(), n, K, ahi.data_ptr(), alo.data_ptr(), ld, 0) == 0
+    assert L.mps_c64_site_planes(G32.data_ptr(), K, N, bhi.data_ptr(), blo.data_ptr(), ld, 0) == 0
+    ms = timeit(lambda: L.mps_c64_gemm_planes(ahi.data_ptr(), alo.data_ptr(), bhi.data_ptr(), blo.data_ptr(), ld,
+                                              C32.data_ptr(), n, K, N, 0))
+    err = ((C32.to(torch.complex128) - ref).abs().max() / ref.abs().max()).item()
+    print(json.dumps({"shape": name, "mode": "c64_tcgen05_3xtf32", "ms": ms, "tflops": flops / ms / 1e9,
+                      "rel_err": err}), flush=True)
+    ms = timeit(lambda: torch.matmul(V32, G32, out=C32))
+    print(json.dumps({"shape": name, "cfg": "cublas_c64", "ms": ms, "tflops": flops / ms / 1e9}), flush=True)
+    del V, G, C, ref, ahi, alo, bhi, blo, V32, G32, C32
     torch.cuda.empty_cache()
