@@ -238,7 +238,7 @@ def run_pipelined(args, rank, world, local, W, K, config, dims):
         mps = mps.astype("complex64")
     block_bytes = sum(dims[m] * dims[m + 1] for m in range(mb, me)) * D * 16.0
     eng = MpsSampler(mps, device=local, sites_range=(mb, me), layout=1, sum_planes=block_bytes * 1.5 < HBM_USABLE)
-    eng.set_lanes(LANES)
+    eng.set_lanes(args.lanes)
     eng.set_streams(0, sigma)
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t_setup
@@ -358,6 +358,7 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--lanes", type=int, default=LANES, help="concurrent row-block chains per micro-batch")
     ap.add_argument("--dtype", default="c128", choices=["c128", "c64"],
                     help="c64: complex64 chain, K1 on tcgen05 (3xTF32), parity 1e-4")
     ap.add_argument("--layout", default="auto", choices=["auto", "sharded", "pipelined"],
@@ -429,7 +430,7 @@ def main():
     if args.dtype == "c64":
         mps = mps.astype("complex64")
     eng = MpsSampler(mps, device=local)
-    eng.set_lanes(LANES)
+    eng.set_lanes(args.lanes)
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t_setup
     stream = torch.cuda.Stream(dev)  # explicit stream: events and kernels share it
@@ -493,7 +494,7 @@ def main():
     prof_draw = eng.profile_read()
     prof.update({k: v for k, v in prof_draw.items() if k.startswith("draw")})
     eng.profile(0)
-    eng.set_lanes(LANES)
+    eng.set_lanes(args.lanes)
     ms = e0.elapsed_time(e1)
     if world > 1:
         t = torch.tensor([ms], device=dev)

@@ -230,10 +230,29 @@ __device__ __forceinline__ void store_state(const DrawArgs& A, int b, int j, dou
   }
 }
 
+// complex64 chain: the einsum and the marginal partials run in fp32 (twice the fp64 rate;
+// ~1e-7 relative, far inside the 1e-4 c64 bar); the draw itself stays in fp64.
+template <int DT>
+__device__ __forceinline__ float2 disp_row_f(const float2* T, int D, int k, const float2* c) {
+  float2 e = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int d = 0; d < (DT ? DT : DMAX); ++d) {
+    if (!DT && d >= D) break;
+    float2 tk;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(tk.x), "=f"(tk.y) : "r"(smem_u32(&T[k * D + d])));
+    e.x = fmaf(tk.x, c[d].x, e.x);
+    e.x = fmaf(-tk.y, c[d].y, e.x);
+    e.y = fmaf(tk.x, c[d].y, e.y);
+    e.y = fmaf(tk.y, c[d].x, e.y);
+  }
+  return e;
+}
+
 template <int DT, bool C64>
-__global__ void __launch_bounds__(DRAW_THREADS, 4)
+__global__ void __launch_bounds__(DRAW_THREADS, C64 ? 8 : 4)
     displace_draw_kernel(DrawArgs A) {
   __shared__ double2 T[DMAX * DMAX];
+  __shared__ float2 Tf[C64 ? DMAX * DMAX : 1];
   __shared__ double red[DRAW_THREADS / 32][DMAX];
   __shared__ double p_s[DMAX];
   __shared__ int k_s;
@@ -264,6 +283,10 @@ __global__ void __launch_bounds__(DRAW_THREADS, 4)
       __syncwarp();
     }
   }
+  if constexpr (C64) {
+    __syncthreads();
+    for (int e = tid; e < D * D; e += DRAW_THREADS) Tf[e] = make_float2((float)T[e].x, (float)T[e].y);
+  }
   griddep_wait();  // the GEMM (and transitively the previous draw) is complete: C, status valid
   __syncthreads();
 
@@ -276,28 +299,54 @@ __global__ void __launch_bounds__(DRAW_THREADS, 4)
 
   // ---- pass 1: partial marginals ----
   constexpr int DR = DT ? DT : DMAX;
-  double acc[DR];
+  if constexpr (C64) {
+    float acc[DR];
 #pragma unroll
-  for (int k = 0; k < DR; ++k) acc[k] = 0.0;
-  for (int j = tid; j < A.chi_r; j += DRAW_THREADS) {
-    double2 c[DR];
+    for (int k = 0; k < DR; ++k) acc[k] = 0.f;
+    for (int j = tid; j < A.chi_r; j += DRAW_THREADS) {
+      float2 c[DR];
 #pragma unroll
-    for (int d = 0; d < DR; ++d)
-      if (DT || d < D) c[d] = load_c<C64>(A, cbase + (long long)j * D + d);
+      for (int d = 0; d < DR; ++d)
+        if (DT || d < D) c[d] = A.C32[cbase + (long long)j * D + d];
+#pragma unroll
+      for (int k = 0; k < DR; ++k) {
+        if (!DT && k >= D) break;
+        const float2 e = ident ? c[k] : disp_row_f<DT>(Tf, D, k, c);
+        acc[k] = fmaf(e.x, e.x, fmaf(e.y, e.y, acc[k]));
+      }
+    }
 #pragma unroll
     for (int k = 0; k < DR; ++k) {
       if (!DT && k >= D) break;
-      const double2 e = ident ? c[k] : disp_row<DT>(T, D, k, c);
-      acc[k] = fma(e.x, e.x, fma(e.y, e.y, acc[k]));
+      float v = acc[k];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) red[warp][k] = (double)v;
     }
-  }
+  } else {
+    double acc[DR];
 #pragma unroll
-  for (int k = 0; k < DR; ++k) {
-    if (!DT && k >= D) break;
-    double v = acc[k];
+    for (int k = 0; k < DR; ++k) acc[k] = 0.0;
+    for (int j = tid; j < A.chi_r; j += DRAW_THREADS) {
+      double2 c[DR];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) red[warp][k] = v;
+      for (int d = 0; d < DR; ++d)
+        if (DT || d < D) c[d] = load_c<C64>(A, cbase + (long long)j * D + d);
+#pragma unroll
+      for (int k = 0; k < DR; ++k) {
+        if (!DT && k >= D) break;
+        const double2 e = ident ? c[k] : disp_row<DT>(T, D, k, c);
+        acc[k] = fma(e.x, e.x, fma(e.y, e.y, acc[k]));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < DR; ++k) {
+      if (!DT && k >= D) break;
+      double v = acc[k];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) red[warp][k] = v;
+    }
   }
   __syncthreads();
   if (tid < D) {  // fixed order over warps
@@ -348,6 +397,23 @@ __global__ void __launch_bounds__(DRAW_THREADS, 4)
   // ---- pass 2: gather + renormalise ----
   if (ks < 0) {
     for (int j = tid; j < A.chi_r; j += DRAW_THREADS) store_state<C64>(A, b, j, make_double2(0.0, 0.0));
+    return;
+  }
+  if constexpr (C64) {
+    const float fs = (float)scale;
+    for (int j = tid; j < A.chi_r; j += DRAW_THREADS) {
+      float2 e;
+      if (ident) {
+        e = A.C32[cbase + (long long)j * D + ks];
+      } else {
+        float2 c[DR];
+#pragma unroll
+        for (int d = 0; d < DR; ++d)
+          if (DT || d < D) c[d] = A.C32[cbase + (long long)j * D + d];
+        e = disp_row_f<DT>(Tf, D, ks, c);
+      }
+      store_state<true>(A, b, j, make_double2(e.x * fs, e.y * fs));
+    }
     return;
   }
   for (int j = tid; j < A.chi_r; j += DRAW_THREADS) {
