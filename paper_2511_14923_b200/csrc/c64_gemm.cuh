@@ -50,6 +50,30 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
+// multicast variants for a 2-CTA cluster sharing the B tile
+__device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::
+                   "r"(smem_u32(bar)),
+               "h"(mask)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_mc(void* smem_dst, const CUtensorMap* map, int x, int y, uint64_t* bar,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -84,7 +108,11 @@ struct C64Cfg {
   static constexpr int THREADS = 192;
 };
 
-template <class Cfg>
+// MC: launched as 2-CTA clusters along M; the two CTAs (same N tile) each fetch half of the
+// B rows and multicast them to both, so each SM pulls 64 KiB instead of 96 KiB per stage
+// from L2 (the kernel is L2-bandwidth-bound without it).  A slot is refilled only after
+// both CTAs' MMAs released it (empty barriers count 2, commits multicast to the pair).
+template <class Cfg, bool MC>
 __global__ void __launch_bounds__(Cfg::THREADS, 1)
     c64_gemm_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
                     const __grid_constant__ CUtensorMap tm_bhi, const __grid_constant__ CUtensorMap tm_blo,
@@ -99,11 +127,12 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * Cfg::BM, n0 = blockIdx.y * Cfg::BN;
 
+  const uint32_t crank = MC ? cluster_ctarank() : 0;
   griddep_launch_dependents();
   if (threadIdx.x == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], MC ? 2 : 1);
     }
     mbar_init(tmem_full, 1);
     fence_barrier_init();
@@ -119,6 +148,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (MC) cluster_sync_all();  // peer barriers initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -132,8 +162,16 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
         tma_load_2d(st, &tm_ahi, kb * Cfg::BK, m0, &full[s]);
         tma_load_2d(st + Cfg::A_BYTES, &tm_alo, kb * Cfg::BK, m0, &full[s]);
-        tma_load_2d(st + 2 * Cfg::A_BYTES, &tm_bhi, kb * Cfg::BK, n0, &full[s]);
-        tma_load_2d(st + 2 * Cfg::A_BYTES + Cfg::B_BYTES, &tm_blo, kb * Cfg::BK, n0, &full[s]);
+        if constexpr (MC) {  // my half of the B rows, multicast to both CTAs of the pair
+          const int half = Cfg::BN / 2;
+          const uint32_t boff = crank * half * Cfg::BK * 4;
+          tma_load_2d_mc(st + 2 * Cfg::A_BYTES + boff, &tm_bhi, kb * Cfg::BK, n0 + crank * half, &full[s], 0x3);
+          tma_load_2d_mc(st + 2 * Cfg::A_BYTES + Cfg::B_BYTES + boff, &tm_blo, kb * Cfg::BK, n0 + crank * half,
+                         &full[s], 0x3);
+        } else {
+          tma_load_2d(st + 2 * Cfg::A_BYTES, &tm_bhi, kb * Cfg::BK, n0, &full[s]);
+          tma_load_2d(st + 2 * Cfg::A_BYTES + Cfg::B_BYTES, &tm_blo, kb * Cfg::BK, n0, &full[s]);
+        }
       }
     }
   } else if (warp == 1) {
@@ -154,7 +192,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           umma_tf32(tmem, dah, dbl, idesc, 1u);
           umma_tf32(tmem, dal, dbh, idesc, 1u);
         }
-        umma_commit(&empty[s]);  // smem slot free once these MMAs have read it
+        if constexpr (MC)
+          umma_commit_mc(&empty[s], 0x3);  // the slot is free for both CTAs' producers
+        else
+          umma_commit(&empty[s]);  // smem slot free once these MMAs have read it
       }
       umma_commit(tmem_full);  // accumulator complete
     }
@@ -171,11 +212,15 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       tmem_ld_32x32b_x32(tmem + ((uint32_t)(32 * q) << 16) + c0, r);
       const int col = n0 + c0;
       if (row < n) {
-        if (col + 32 <= N2) {
+        if (col + 32 <= N2 && (ldc & 3) == 0) {  // rows 16-B aligned: vector stores
 #pragma unroll
           for (int j = 0; j < 32; j += 4)
             *reinterpret_cast<float4*>(crow + col + j) = make_float4(
                 __uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+        } else if (col + 32 <= N2) {  // ldc = 2N is even: complex (8-B) stores are always aligned
+#pragma unroll
+          for (int j = 0; j < 32; j += 2)
+            *reinterpret_cast<float2*>(crow + col + j) = make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1]));
         } else {
 #pragma unroll
           for (int j = 0; j < 32; ++j)
@@ -186,6 +231,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     tc_fence_before();
   }
   __syncthreads();
+  if constexpr (MC) cluster_sync_all();  // no CTA leaves while its peer may still signal it
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)Cfg::TMEM_COLS));

@@ -418,26 +418,60 @@ static int launch_site_gemm(mps_ctx* ctx, const GemmOps& o, cudaStream_t st, int
 using C64Big = C64Cfg<256, 2>;
 
 // C (n x N complex64) = A planes (n x ld fp32, hi/lo of the interleaved state) . B_r planes
+// multicast pairs are used when there are >= 2 M tiles (MPS_C64_NO_MULTICAST=1 disables them)
+static bool c64_multicast_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MPS_C64_NO_MULTICAST");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 static cudaError_t launch_c64_gemm(const float* ahi, const float* alo, const float* bhi, const float* blo, int ld,
                                    float* C, int n, int K, int N, long long ldc_f, cudaStream_t st) {
   using Cfg = C64Big;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(c64_gemm_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(c64_gemm_kernel<Cfg, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          Cfg::SMEM_BYTES);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(c64_gemm_kernel<Cfg, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               Cfg::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     configured = true;
   }
+  const int mtiles = (n + Cfg::BM - 1) / Cfg::BM;
+  const bool mc = c64_multicast_enabled() && mtiles >= 2;
   CUtensorMap tah, tal, tbh, tbl;
   const uint64_t cols = 2 * (uint64_t)K, pitch = 4 * (uint64_t)ld;
+  const uint32_t brows = mc ? Cfg::BN / 2 : Cfg::BN;
   if (!make_tmap(&tah, ahi, n, cols, pitch, Cfg::BM, 32, true) || !make_tmap(&tal, alo, n, cols, pitch, Cfg::BM, 32, true) ||
-      !make_tmap(&tbh, bhi, 2 * (uint64_t)N, cols, pitch, Cfg::BN, 32, true) ||
-      !make_tmap(&tbl, blo, 2 * (uint64_t)N, cols, pitch, Cfg::BN, 32, true))
+      !make_tmap(&tbh, bhi, 2 * (uint64_t)N, cols, pitch, brows, 32, true) ||
+      !make_tmap(&tbl, blo, 2 * (uint64_t)N, cols, pitch, brows, 32, true))
     return cudaErrorInvalidValue;
-  dim3 grid((n + Cfg::BM - 1) / Cfg::BM, (2 * N + Cfg::BN - 1) / Cfg::BN);
   const int KB = (int)((cols + Cfg::BK - 1) / Cfg::BK);
-  return launch_pdl(c64_gemm_kernel<Cfg>, grid, dim3(Cfg::THREADS), Cfg::SMEM_BYTES, st, tah, tal, tbh, tbl, C, n,
-                    2 * N, KB, ldc_f);
+  if (!mc) {
+    dim3 grid(mtiles, (2 * N + Cfg::BN - 1) / Cfg::BN);
+    return launch_pdl(c64_gemm_kernel<Cfg, false>, grid, dim3(Cfg::THREADS), Cfg::SMEM_BYTES, st, tah, tal, tbh, tbl,
+                      C, n, 2 * N, KB, ldc_f);
+  }
+  dim3 grid((mtiles + 1) & ~1, (2 * N + Cfg::BN - 1) / Cfg::BN);  // pairs along M (a padding CTA stores nothing)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(Cfg::THREADS);
+  cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, c64_gemm_kernel<Cfg, true>, tah, tal, tbh, tbl, C, n, 2 * N, KB, ldc_f);
 }
 
 extern "C" {

@@ -434,7 +434,8 @@ def test_sum_planes_chi1000_parity():
 # ------------------------------------------------------------------ complex64 (tcgen05)
 
 
-@pytest.mark.parametrize("n,K,N", [(1, 1, 4), (100, 16, 40), (130, 37, 90), (257, 250, 2500), (1024, 1000, 10000)])
+@pytest.mark.parametrize("n,K,N", [(1, 1, 4), (37, 21, 45), (100, 16, 40), (130, 37, 90), (257, 250, 2500),
+                                   (1024, 1000, 10000)])
 def test_site_gemm_c64_tcgen05_vs_fp64(n, K, N):
     """3xTF32 tcgen05 complex GEMM vs an fp64 product of the same complex64 inputs."""
     L = _native.lib()
@@ -467,7 +468,7 @@ def _check_parity_c64(sites64, res, u, alpha=None):
 
 
 @pytest.mark.parametrize("name,M,chi,D,N,n", [("c1", 8, 16, 4, 400, 100), ("c2", 16, 100, 10, 400, 100),
-                                              ("chi1000", 5, 1000, 10, 128, 128)])
+                                              ("chi1000", 5, 1000, 10, 128, 128), ("odd", 6, 9, 5, 90, 90)])
 def test_c64_chain_parity(name, M, chi, D, N, n):
     sites = [s.astype(np.complex64) for s in orc.random_mps(M, chi, D, seed=3)]
     cfg = MpsSamplerConfig(N=N, seed=4, alpha_sigma=0.5, batch_size=n)
@@ -510,3 +511,20 @@ def test_c64_stage_split(c2_sites):
     # the hand-off rounds the state to complex64 exactly as the in-context chain stores it
     # before splitting into tf32 planes, so the split chain reproduces the full one
     assert np.array_equal(counts.cpu().numpy(), full["counts"])
+
+
+@pytest.mark.parametrize("dtype", ["complex128", "complex64"])
+@pytest.mark.parametrize("M,chi,D,N", [(7, 7, 3, 37), (5, 9, 5, 130), (3, 1, 16, 64), (1, 1, 7, 33), (9, 40, 2, 257)])
+def test_odd_shapes(M, chi, D, N, dtype):
+    """Ragged / odd shapes (odd N = chi_r D, odd K, D up to 16, chi = 1 product states, M = 1):
+    alignment paths of every kernel, both dtypes, against the fp64 oracle."""
+    sites = [s.astype(dtype) for s in orc.random_mps(M, chi, D, seed=M + D)]
+    cfg = MpsSamplerConfig(N=N, seed=M, alpha_sigma=0.4, batch_size=N)
+    with MpsSampler(MPS(sites)) as eng:
+        eng.set_lanes(2)
+        res = eng.sample(cfg, return_marginals=True)
+    u, al = stream_uniforms(M, 0, N, M), alpha_stream(M, 0, N, M, 0.4)
+    if dtype == "complex64":
+        _check_parity_c64(sites, res, u, alpha=al)
+    else:
+        _check_parity(sites, res, u, alpha=al)
