@@ -313,7 +313,8 @@ def run_pipelined(args, rank, world, local, W, K, config, dims):
     gemm_ms_avg = prof["gemm_ms"] / max(prof["gemm_launches"], 1)
     gemm_flops_avg = prof["gemm_flops"] / max(prof["gemm_launches"], 1)
     achieved = gemm_flops_avg / (gemm_ms_avg / 1e3) / 1e12 if gemm_ms_avg > 0 else 0.0
-    kernel_name = "site_gemm3m_kernel (K1, FP64 DMMA, 3M)"
+    kernel_name = {"3m": "site_gemm3m_kernel (K1, FP64 DMMA, 3M)", "4m": "site_gemm_kernel (K1, FP64 DMMA, 4M)",
+                   "ozaki": "ozaki_gemm_kernel (K1, fp64 emulated on INT8 tcgen05, 7 digits)"}[args.gemm]
     bound_note = None
     if args.dtype == "c64":
         # tcgen05 kind::tf32 executes 3 passes (hi.hi, hi.lo, lo.hi) of the real-doubled
@@ -359,6 +360,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--lanes", type=int, default=LANES, help="concurrent row-block chains per micro-batch")
+    ap.add_argument("--gemm", default="3m", choices=["3m", "4m", "ozaki"],
+                    help="complex128 K1: 3M / 4M on the FP64 DMMA pipe, or fp64 emulated on INT8 tcgen05")
     ap.add_argument("--dtype", default="c128", choices=["c128", "c64"],
                     help="c64: complex64 chain, K1 on tcgen05 (3xTF32), parity 1e-4")
     ap.add_argument("--layout", default="auto", choices=["auto", "sharded", "pipelined"],
@@ -373,7 +376,7 @@ def main():
     from paper_2511_14923_b200.mps import bond_dims
 
     dims = bond_dims(M, chi, D)
-    config = {"workload": f"{args.config}: {desc}", "M": M, "chi": chi, "D": D, "n": n,
+    config = {"workload": f"{args.config}: {desc}", "M": M, "chi": chi, "D": D, "n": n, "gemm": args.gemm,
               "alpha": "CN(0,%.3g)" % (sigma * sigma), "sites": "random row-orthonormal, seed 0",
               "layout": "sample-sharded" if world > 1 else "single GPU",
               "l2": "inputs larger than L2 (sites %.2f GB streamed per step)" % (
@@ -431,6 +434,7 @@ def main():
         mps = mps.astype("complex64")
     eng = MpsSampler(mps, device=local)
     eng.set_lanes(args.lanes)
+    eng.set_gemm_mode({"3m": 3, "4m": 4, "ozaki": 8}[args.gemm])
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t_setup
     stream = torch.cuda.Stream(dev)  # explicit stream: events and kernels share it
@@ -538,7 +542,8 @@ def main():
     gemm_ms_avg = prof["gemm_ms"] / max(prof["gemm_launches"], 1)
     gemm_flops_avg = prof["gemm_flops"] / max(prof["gemm_launches"], 1)
     achieved = gemm_flops_avg / (gemm_ms_avg / 1e3) / 1e12 if gemm_ms_avg > 0 else 0.0
-    kernel_name = "site_gemm3m_kernel (K1, FP64 DMMA, 3M)"
+    kernel_name = {"3m": "site_gemm3m_kernel (K1, FP64 DMMA, 3M)", "4m": "site_gemm_kernel (K1, FP64 DMMA, 4M)",
+                   "ozaki": "ozaki_gemm_kernel (K1, fp64 emulated on INT8 tcgen05, 7 digits)"}[args.gemm]
     bound_note = None
     if args.dtype == "c64":
         # tcgen05 kind::tf32 executes 3 passes (hi.hi, hi.lo, lo.hi) of the real-doubled

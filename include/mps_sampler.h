@@ -158,9 +158,22 @@ int mps_set_lanes(mps_ctx* ctx, int lanes);
  * writes Vr+Vi next to the state, so K1 loads the operand sums instead of forming them
  * on the FP64 pipe.  Results are bit-identical either way.  Set before loading sites. */
 int mps_set_sum_planes(mps_ctx* ctx, int enable);
-/* K1 complex product: 3 = 3M (default), 4 = 4M.  Results of the two modes differ at
- * rounding level; each is deterministic across batch sizes and GPU counts. */
+/* K1 complex product: 3 = 3M (default), 4 = 4M, both on the FP64 DMMA pipe; 8 = fp64
+ * emulated on the INT8 tcgen05 tensor cores (Ozaki scheme, 7 digits of 7 bits per operand,
+ * ~1e-13 of the row scales; opt-in).  Results of the modes differ at rounding level; each is
+ * deterministic across batch sizes and GPU counts. */
 int mps_set_gemm_mode(mps_ctx* ctx, int mode);
+/* complex128 K1 emulated on the INT8 tensor cores (Ozaki scheme with S = 5..7 digits):
+ * C (n x N) = V (n x K) . G (K x N), all complex128.  Test/benchmark entry (slices per call). */
+int mps_site_gemm_ozaki(const void* V, const void* G, void* C, int n, int K, int N, int S, uint64_t stream);
+/* Its pieces: int8 digit planes (S stacked planes of rows_pad x ld bytes, ld % 16 == 0) and
+ * exponents of a state (n x K) and of a site's B_r^T (2N rows), and the GEMM on them. */
+int mps_ozaki_state_planes(const void* V, int n, int K, int S, int8_t* planes, int* e, int ld, int n_pad,
+                           uint64_t stream);
+int mps_ozaki_site_planes(const void* G, int K, int N, int S, int8_t* planes, int* e, int ld, int b_pad,
+                          uint64_t stream);
+int mps_ozaki_gemm_planes(const int8_t* a_planes, int n_pad, const int* ea, const int8_t* b_planes, int b_pad,
+                          const int* eb, int ld, void* C, int n, int K, int N, int S, uint64_t stream);
 /* complex64 K1 on the tcgen05 tensor cores (kind::tf32, 3xTF32 split, fp32 accumulate):
  * C (n x N complex64) = V (n x K complex64) . G (K x N complex64).  Test/benchmark entry:
  * builds the hi/lo operand planes in temporary memory on every call. */

@@ -20,7 +20,8 @@ EXPORTS = (
     "mps_kernel_launches", "mps_profile", "mps_profile_read", "mps_last_error", "mps_destroy",
     "mps_site_gemm", "mps_site_gemm_cfg", "mps_set_gemm_config", "mps_set_gemm_mode", "mps_set_lanes",
     "mps_set_sum_planes", "mps_displacement", "mps_stream_uniforms", "mps_site_gemm_c64",
-    "mps_c64_state_planes", "mps_c64_site_planes", "mps_c64_gemm_planes",
+    "mps_c64_state_planes", "mps_c64_site_planes", "mps_c64_gemm_planes", "mps_site_gemm_ozaki",
+    "mps_ozaki_state_planes", "mps_ozaki_site_planes", "mps_ozaki_gemm_planes",
 )
 
 MPS_SITE_HOST, MPS_SITE_DEVICE_COPY, MPS_SITE_DEVICE_BORROW = 0, 1, 2
@@ -56,6 +57,11 @@ def _declare(L):
     L.mps_set_lanes.argtypes = [c_void_p, c_int]
     L.mps_set_sum_planes.argtypes = [c_void_p, c_int]
     L.mps_site_gemm_c64.argtypes = [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_uint64]
+    L.mps_site_gemm_ozaki.argtypes = [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_uint64]
+    L.mps_ozaki_state_planes.argtypes = [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_int, c_int, c_uint64]
+    L.mps_ozaki_site_planes.argtypes = [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_int, c_int, c_uint64]
+    L.mps_ozaki_gemm_planes.argtypes = [c_void_p, c_int, c_void_p, c_void_p, c_int, c_void_p, c_int, c_void_p, c_int,
+                                        c_int, c_int, c_int, c_uint64]
     L.mps_c64_state_planes.argtypes = [c_void_p, c_int, c_int, c_void_p, c_void_p, c_int, c_uint64]
     L.mps_c64_site_planes.argtypes = [c_void_p, c_int, c_int, c_void_p, c_void_p, c_int, c_uint64]
     L.mps_c64_gemm_planes.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_int, c_int, c_int,
@@ -63,17 +69,9 @@ def _declare(L):
     L.mps_set_gemm_config.argtypes = [c_void_p, c_int]
     L.mps_displacement.argtypes = [c_void_p, c_int, c_int, c_void_p, c_uint64]
     L.mps_stream_uniforms.argtypes = [c_uint64, c_int64, c_int, c_int, c_void_p, c_uint64]
-    for name in EXPORTS:
-        fn = getattr(L, name)
-        if fn.restype is ctypes.c_int or name in ("mps_create", "mps_configure", "mps_set_site",
-                                                  "mps_set_streams", "mps_sample", "mps_sample_range",
-                                                  "mps_profile", "mps_profile_read", "mps_site_gemm_cfg",
-                                                  "mps_set_gemm_config", "mps_set_gemm_mode", "mps_set_lanes",
-                                                  "mps_set_sum_planes", "mps_site_gemm_c64",
-                                                  "mps_c64_state_planes", "mps_c64_site_planes",
-                                                  "mps_c64_gemm_planes",
-                                                  "mps_site_gemm", "mps_displacement", "mps_stream_uniforms"):
-            fn.restype = c_int
+    for name in EXPORTS:  # everything else returns an int status (include/mps_sampler.h)
+        if name not in ("mps_kernel_launches", "mps_last_error", "mps_destroy"):
+            getattr(L, name).restype = c_int
 
 
 def load_library(path: str | os.PathLike | None = None):

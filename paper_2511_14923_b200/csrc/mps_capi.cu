@@ -24,6 +24,7 @@
 #include "../../include/mps_sampler.h"
 #include "c64_gemm.cuh"
 #include "displace_draw.cuh"
+#include "ozaki_gemm.cuh"
 #include "site_gemm.cuh"
 
 using namespace mps;
@@ -64,6 +65,36 @@ bool make_tmap(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
   return r == CUDA_SUCCESS;
 }
 
+// int8 digit planes: rows x cols bytes, 32-byte boxes with the 32B swizzle (Ozaki K1)
+bool make_tmap_u8(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t pitch, uint32_t box_rows) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {pitch};
+  cuuint32_t box[2] = {32, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+// S stacked digit planes (plane p at rows [p * rows_pad, (p+1) * rows_pad)) as one 3-D tensor,
+// so a single TMA op brings a {32 B x box_rows x S} box: all digits of a tile for one K step
+bool make_tmap_u8_planes(CUtensorMap* map, const void* base, uint64_t rows_pad, uint64_t cols, uint64_t pitch, int S,
+                         uint32_t box_rows) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {cols, rows_pad, (cuuint64_t)S};
+  cuuint64_t strides[2] = {pitch, pitch * rows_pad};
+  cuuint32_t box[3] = {32, box_rows, (cuuint32_t)S};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // fp32 plane row pitch (floats): TMA needs 16-byte row strides
 inline int plane_ld(int cols_fp32) { return (cols_fp32 + 3) & ~3; }
 
@@ -88,6 +119,10 @@ struct Site {
   double* gsum = nullptr;  // sum plane Gr + Gi (chi_l x sum_ld(N)) for the 3M GEMM, or null
   CUtensorMap tmap_gs;
   bool loaded = false;
+  // Ozaki (int8 tcgen05) digit planes of B_r^T, built on first use in gemm mode 8
+  int8_t* oz = nullptr;
+  int* oz_e = nullptr;
+  int oz_S = 0, oz_ld = 0, oz_pad = 0;
   // complex64 sites: only the tcgen05 operand planes are kept (B_r^T hi / lo, 2N x ld fp32)
   float* bhi = nullptr;
   float* blo = nullptr;
@@ -97,6 +132,10 @@ struct Site {
     if (gsum) cudaFree(gsum);
     if (bhi) cudaFree(bhi);
     if (blo) cudaFree(blo);
+    if (oz) cudaFree(oz);
+    if (oz_e) cudaFree(oz_e);
+    oz = nullptr;
+    oz_e = nullptr;
     data = nullptr;
     gsum = nullptr;
     bhi = blo = nullptr;
@@ -150,6 +189,9 @@ struct mps_ctx {
   DevBuf<double> lvs0[MAX_LANES], lvs1[MAX_LANES];  // state sum planes (3M operand sums)
   bool sum_planes = true;                           // feed the 3M GEMM precomputed sums
   int dtype = -1;                                   // MPS_C128 / MPS_C64, fixed by the first site
+  int oz_S = 7;                                     // Ozaki digits per operand (gemm mode 8)
+  DevBuf<int8_t> loz[MAX_LANES];                    // state digit planes per lane
+  DevBuf<int> loz_e[MAX_LANES];
   DevBuf<float> la_hi[2][MAX_LANES], la_lo[2][MAX_LANES];  // c64 state planes (ping-pong)
   DevBuf<float2> lc32[MAX_LANES];                   // c64 C buffer
   DevBuf<float> ones_hi, ones_lo, in_hi, in_lo;
@@ -414,6 +456,64 @@ static int launch_site_gemm(mps_ctx* ctx, const GemmOps& o, cudaStream_t st, int
   return MPS_OK;
 }
 
+// ---- complex128 K1 emulated on the INT8 tensor cores (Ozaki scheme, gemm mode 8) -----------------
+template <int S>
+static cudaError_t launch_ozaki_s(const int8_t* a_planes, int n_pad, const int* ea, const int8_t* b_planes, int b_pad,
+                                  const int* eb, int ld, double2* C, int n, int K, int N, cudaStream_t st) {
+  using Cfg = OzCfg<S>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(ozaki_gemm_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Cfg::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  CUtensorMap ta, tb;
+  if (!make_tmap_u8_planes(&ta, a_planes, n_pad, 2 * (uint64_t)K, ld, S, Cfg::BM) ||
+      !make_tmap_u8_planes(&tb, b_planes, b_pad, 2 * (uint64_t)K, ld, S, Cfg::BN))
+    return cudaErrorInvalidValue;
+  dim3 grid((n + Cfg::BM - 1) / Cfg::BM, (2 * N + Cfg::BN - 1) / Cfg::BN);
+  const int KB = (2 * K + Cfg::BK - 1) / Cfg::BK;
+  return launch_pdl(ozaki_gemm_kernel<Cfg>, grid, dim3(Cfg::THREADS), Cfg::SMEM_BYTES, st, ta, tb, ea, eb,
+                    (double*)C, n, 2 * N, n_pad, b_pad, KB, 2LL * N);
+}
+
+static cudaError_t launch_ozaki(int S, const int8_t* a_planes, int n_pad, const int* ea, const int8_t* b_planes,
+                                int b_pad, const int* eb, int ld, double2* C, int n, int K, int N, cudaStream_t st) {
+  switch (S) {
+    case 5: return launch_ozaki_s<5>(a_planes, n_pad, ea, b_planes, b_pad, eb, ld, C, n, K, N, st);
+    case 6: return launch_ozaki_s<6>(a_planes, n_pad, ea, b_planes, b_pad, eb, ld, C, n, K, N, st);
+    default: return launch_ozaki_s<7>(a_planes, n_pad, ea, b_planes, b_pad, eb, ld, C, n, K, N, st);
+  }
+}
+
+// digit planes of a state (n x K complex128): S planes of n_pad x ld bytes + n exponents
+static cudaError_t ozaki_slice_state(const double2* V, int n, int K, int S, int8_t* planes, int n_pad, int ld, int* e,
+                                     cudaStream_t st) {
+  ozaki_slice_rows_kernel<<<n, 128, 0, st>>>(V, K, S, planes, (long long)n_pad * ld, ld, e);
+  return cudaGetLastError();
+}
+
+// site digit planes (B_r^T: 2N rows), built once per (site, S)
+static cudaError_t ozaki_prepare_site(Site& s, int D, int S) {
+  if (s.oz && s.oz_S == S) return cudaSuccess;
+  if (s.oz) cudaFree(s.oz);
+  if (s.oz_e) cudaFree(s.oz_e);
+  s.oz = nullptr;
+  s.oz_e = nullptr;
+  const int N = s.chi_r * D;
+  s.oz_ld = round_up(2 * s.chi_l, 16);
+  s.oz_pad = round_up(2 * N, 64);
+  cudaError_t e = cudaMalloc(&s.oz, (size_t)S * s.oz_pad * s.oz_ld);
+  if (e == cudaSuccess) e = cudaMalloc(&s.oz_e, (size_t)2 * N * sizeof(int));
+  if (e != cudaSuccess) return e;
+  ozaki_slice_site_kernel<<<2 * N, 128>>>(s.data, s.chi_l, N, S, s.oz, (long long)s.oz_pad * s.oz_ld, s.oz_ld, s.oz_e);
+  e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  s.oz_S = S;
+  return e;
+}
+
 // ---- complex64 K1 (tcgen05, 3xTF32) --------------------------------------------------------
 using C64Big = C64Cfg<256, 2>;
 
@@ -672,12 +772,19 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
     CU(c, c->lv0[l].ensure(nl * chi_max), "alloc state");
     CU(c, c->lv1[l].ensure(nl * chi_max), "alloc state");
     CU(c, c->lcbuf[l].ensure(nl * cmax), "alloc C buffer");
+    if (c->gemm_mode == 8) {
+      CU(c, c->loz[l].ensure((size_t)c->oz_S * round_up((int)nl, 128) * round_up(2 * chi_max, 16)), "alloc digits");
+      CU(c, c->loz_e[l].ensure(nl), "alloc digit exponents");
+    }
     if (c->sum_planes && c->gemm_mode == 3) {
       CU(c, c->lvs0[l].ensure(nl * sum_ld(chi_max)), "alloc state sums");
       CU(c, c->lvs1[l].ensure(nl * sum_ld(chi_max)), "alloc state sums");
     }
   }
   const bool use_sums = !c64 && c->sum_planes && c->gemm_mode == 3;
+  const bool ozaki = !c64 && c->gemm_mode == 8;
+  if (ozaki)
+    for (int m = m_begin; m < m_end; ++m) CU(c, ozaki_prepare_site(c->sites[m], D, c->oz_S), "Ozaki site digits");
 
   // ---- inputs: stage host arrays on the device ----
   const double* u_dev = uniforms;
@@ -804,6 +911,14 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
                                         2LL * N, lst[l]);
         c->launches++;
         if (e != cudaSuccess) return cuda_fail(c, e, "c64 site_gemm launch");
+      } else if (ozaki) {
+        const int n_pad = round_up(nl, 128);
+        CU(c, ozaki_slice_state(v_in[l], nl, s.chi_l, c->oz_S, c->loz[l].p, n_pad, s.oz_ld, c->loz_e[l].p, lst[l]),
+           "Ozaki state digits");
+        cudaError_t e = launch_ozaki(c->oz_S, c->loz[l].p, n_pad, c->loz_e[l].p, s.oz, s.oz_pad, s.oz_e, s.oz_ld,
+                                     c->lcbuf[l].p, nl, s.chi_l, N, lst[l]);
+        c->launches += 2;
+        if (e != cudaSuccess) return cuda_fail(c, e, "Ozaki site_gemm launch");
       } else {
         GemmOps o{v_in[l], vs_in[l], ld_vs_in, &s.tmap, s.gsum ? &s.tmap_gs : nullptr, c->lcbuf[l].p, nl, s.chi_l, N,
                   N};
@@ -956,7 +1071,11 @@ void mps_destroy(mps_ctx* c) {
       c->la_hi[w][l].release();
       c->la_lo[w][l].release();
     }
-  for (int l = 0; l < mps_ctx::MAX_LANES; ++l) c->lc32[l].release();
+  for (int l = 0; l < mps_ctx::MAX_LANES; ++l) {
+    c->lc32[l].release();
+    c->loz[l].release();
+    c->loz_e[l].release();
+  }
   c->ones_hi.release();
   c->ones_lo.release();
   c->in_hi.release();
@@ -1002,6 +1121,61 @@ int mps_site_gemm_cfg(const void* V, const void* G, void* C, int n, int K, int N
 
 int mps_site_gemm(const void* V, const void* G, void* C, int n, int K, int N, int64_t ldc, uint64_t stream) {
   return mps_site_gemm_cfg(V, G, C, n, K, N, ldc, stream, -1, 3);
+}
+
+int mps_site_gemm_ozaki(const void* V, const void* G, void* C, int n, int K, int N, int S, uint64_t stream) {
+  if (!V || !G || !C || n < 1 || K < 1 || N < 1 || S < 5 || S > 7) return MPS_ERR_VALIDATION;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int ld = round_up(2 * K, 16), n_pad = round_up(n, 128), b_pad = round_up(2 * N, 64);
+  int8_t *ap = nullptr, *bp = nullptr;
+  int *ea = nullptr, *eb = nullptr;
+  if (cudaMallocAsync(&ap, (size_t)S * n_pad * ld, st) != cudaSuccess ||
+      cudaMallocAsync(&bp, (size_t)S * b_pad * ld, st) != cudaSuccess ||
+      cudaMallocAsync(&ea, (size_t)n * sizeof(int), st) != cudaSuccess ||
+      cudaMallocAsync(&eb, (size_t)2 * N * sizeof(int), st) != cudaSuccess) {
+    cudaGetLastError();
+    return MPS_ERR_RESOURCE;
+  }
+  ozaki_slice_rows_kernel<<<n, 128, 0, st>>>((const double2*)V, K, S, ap, (long long)n_pad * ld, ld, ea);
+  ozaki_slice_site_kernel<<<2 * N, 128, 0, st>>>((const double2*)G, K, N, S, bp, (long long)b_pad * ld, ld, eb);
+  cudaError_t e = launch_ozaki(S, ap, n_pad, ea, bp, b_pad, eb, ld, (double2*)C, n, K, N, st);
+  cudaFreeAsync(ap, st);
+  cudaFreeAsync(bp, st);
+  cudaFreeAsync(ea, st);
+  cudaFreeAsync(eb, st);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return MPS_ERR_GENERIC;
+  }
+  return cudaGetLastError() == cudaSuccess ? MPS_OK : MPS_ERR_GENERIC;
+}
+
+int mps_ozaki_state_planes(const void* V, int n, int K, int S, int8_t* planes, int* e, int ld, int n_pad,
+                           uint64_t stream) {
+  if (!V || !planes || !e || n < 1 || K < 1 || S < 5 || S > 7 || ld < 2 * K || ld % 16 || n_pad < n)
+    return MPS_ERR_VALIDATION;
+  return ozaki_slice_state((const double2*)V, n, K, S, planes, n_pad, ld, e, reinterpret_cast<cudaStream_t>(stream)) ==
+                 cudaSuccess
+             ? MPS_OK
+             : MPS_ERR_GENERIC;
+}
+
+int mps_ozaki_site_planes(const void* G, int K, int N, int S, int8_t* planes, int* e, int ld, int b_pad,
+                          uint64_t stream) {
+  if (!G || !planes || !e || K < 1 || N < 1 || S < 5 || S > 7 || ld < 2 * K || ld % 16 || b_pad < 2 * N)
+    return MPS_ERR_VALIDATION;
+  ozaki_slice_site_kernel<<<2 * N, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      (const double2*)G, K, N, S, planes, (long long)b_pad * ld, ld, e);
+  return cudaGetLastError() == cudaSuccess ? MPS_OK : MPS_ERR_GENERIC;
+}
+
+int mps_ozaki_gemm_planes(const int8_t* a_planes, int n_pad, const int* ea, const int8_t* b_planes, int b_pad,
+                          const int* eb, int ld, void* C, int n, int K, int N, int S, uint64_t stream) {
+  if (!a_planes || !b_planes || !ea || !eb || !C || n < 1 || K < 1 || N < 1 || S < 5 || S > 7) return MPS_ERR_VALIDATION;
+  return launch_ozaki(S, a_planes, n_pad, ea, b_planes, b_pad, eb, ld, (double2*)C, n, K, N,
+                      reinterpret_cast<cudaStream_t>(stream)) == cudaSuccess
+             ? MPS_OK
+             : MPS_ERR_GENERIC;
 }
 
 int mps_c64_state_planes(const void* V, int rows, int cols, float* hi, float* lo, int ld, uint64_t stream) {
@@ -1078,7 +1252,8 @@ int mps_set_lanes(mps_ctx* c, int lanes) {
 
 int mps_set_gemm_mode(mps_ctx* c, int mode) {
   if (!c) return MPS_ERR_VALIDATION;
-  if (mode != 3 && mode != 4) return fail(c, MPS_ERR_VALIDATION, "gemm mode must be 3 (3M) or 4 (4M), got %d", mode);
+  if (mode != 3 && mode != 4 && mode != 8)
+    return fail(c, MPS_ERR_VALIDATION, "gemm mode must be 3 (3M), 4 (4M) or 8 (Ozaki int8), got %d", mode);
   c->gemm_mode = mode;
   return MPS_OK;
 }

@@ -528,3 +528,48 @@ def test_odd_shapes(M, chi, D, N, dtype):
         _check_parity_c64(sites, res, u, alpha=al)
     else:
         _check_parity(sites, res, u, alpha=al)
+
+
+# ------------------------------------------------------------------ fp64 emulated on INT8 tcgen05 (Ozaki)
+
+
+@pytest.mark.parametrize("S", [6, 7])
+@pytest.mark.parametrize("n,K,N", [(1, 1, 4), (37, 21, 45), (130, 37, 90), (257, 250, 2500), (1024, 1000, 10000)])
+def test_site_gemm_ozaki_vs_torch(n, K, N, S):
+    L = _native.lib()
+    g = torch.Generator(device="cuda").manual_seed(n + 5 * K)
+    V = torch.randn(n, K, dtype=torch.complex128, device="cuda", generator=g)
+    G = torch.randn(K, N, dtype=torch.complex128, device="cuda", generator=g)
+    C = torch.full((n, N), complex(np.nan, np.nan), dtype=torch.complex128, device="cuda")
+    assert L.mps_site_gemm_ozaki(V.data_ptr(), G.data_ptr(), C.data_ptr(), n, K, N, S, 0) == 0
+    torch.cuda.synchronize()
+    ref = V @ G
+    err = (C - ref).abs().max().item()
+    scale = (V.abs().max() * G.abs().max()).item() * np.sqrt(K)
+    assert err <= (2e-13 if S == 7 else 3e-11) * scale, (err, scale)
+
+
+def test_chain_parity_ozaki(c2_sites):
+    N, M = 400, 16
+    cfg = MpsSamplerConfig(N=N, seed=13, alpha_sigma=0.5, batch_size=200)
+    with MpsSampler(MPS(c2_sites)) as eng:
+        eng.set_gemm_mode(8)
+        res = eng.sample(cfg, return_marginals=True)
+    err = _check_parity(c2_sites, res, stream_uniforms(13, 0, N, M), alpha=alpha_stream(13, 0, N, M, 0.5))
+    assert err < 1e-12
+
+
+def test_ozaki_chi1000_and_invariance():
+    M, chi, D, N = 5, 1000, 10, 192
+    sites = orc.random_mps(M, chi, D, seed=9)
+    outs = []
+    with MpsSampler(MPS(sites)) as eng:
+        eng.set_gemm_mode(8)
+        for lanes, B in ((1, 192), (2, 192), (1, 64)):
+            eng.set_lanes(lanes)
+            outs.append(eng.sample(MpsSamplerConfig(N=N, seed=9, alpha_sigma=0.7, batch_size=B),
+                                   return_marginals=True))
+    _check_parity(sites, outs[0], stream_uniforms(9, 0, N, M), alpha=alpha_stream(9, 0, N, M, 0.7))
+    for o in outs[1:]:
+        assert np.array_equal(o["counts"], outs[0]["counts"])
+        assert np.array_equal(o["marginals"], outs[0]["marginals"])
