@@ -360,6 +360,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--lanes", type=int, default=LANES, help="concurrent row-block chains per micro-batch")
+    ap.add_argument("--stream-sites", action="store_true",
+                    help="keep the sites in pinned host memory and stream them into HBM every step")
     ap.add_argument("--gemm", default="3m", choices=["3m", "4m", "ozaki"],
                     help="complex128 K1: 3M / 4M on the FP64 DMMA pipe, or fp64 emulated on INT8 tcgen05")
     ap.add_argument("--dtype", default="c128", choices=["c128", "c64"],
@@ -377,6 +379,7 @@ def main():
 
     dims = bond_dims(M, chi, D)
     config = {"workload": f"{args.config}: {desc}", "M": M, "chi": chi, "D": D, "n": n, "gemm": args.gemm,
+              "sites_in": "host, streamed per step" if args.stream_sites else "HBM",
               "alpha": "CN(0,%.3g)" % (sigma * sigma), "sites": "random row-orthonormal, seed 0",
               "layout": "sample-sharded" if world > 1 else "single GPU",
               "l2": "inputs larger than L2 (sites %.2f GB streamed per step)" % (
@@ -432,7 +435,10 @@ def main():
     mps = MPS.random(M, chi, D, seed=0, device=dev) if M * chi * chi * D * 16 > 2e8 else MPS.random(M, chi, D, 0)
     if args.dtype == "c64":
         mps = mps.astype("complex64")
-    eng = MpsSampler(mps, device=local)
+    if args.stream_sites:  # host-resident sites, streamed per step (PCIe) instead of resident in HBM
+        mps = MPS([G.cpu().numpy() if hasattr(G, "cpu") else G for G in mps.sites])
+        torch.cuda.empty_cache()
+    eng = MpsSampler(mps, device=local, stream_sites=args.stream_sites)
     eng.set_lanes(args.lanes)
     eng.set_gemm_mode({"3m": 3, "4m": 4, "ozaki": 8}[args.gemm])
     torch.cuda.synchronize()

@@ -66,6 +66,10 @@ extern "C" {
 #define MPS_SITE_HOST 0          /* gamma is host memory: copied into context-owned HBM */
 #define MPS_SITE_DEVICE_COPY 1   /* gamma is device memory: copied */
 #define MPS_SITE_DEVICE_BORROW 2 /* gamma is device memory: borrowed, caller keeps it alive */
+#define MPS_SITE_HOST_STREAM 3   /* gamma is host memory, kept there (pinned via cudaHostRegister
+                                    unless already pinned; caller keeps it alive) and streamed
+                                    into a 2-slot HBM ring on a copy stream ahead of each GEMM:
+                                    for MPS larger than the GPU (complex128 only) */
 
 /* dtype (all sites of a context share it; state_in / state_out use the same type) */
 #define MPS_C128 0

@@ -24,7 +24,7 @@ EXPORTS = (
     "mps_ozaki_state_planes", "mps_ozaki_site_planes", "mps_ozaki_gemm_planes",
 )
 
-MPS_SITE_HOST, MPS_SITE_DEVICE_COPY, MPS_SITE_DEVICE_BORROW = 0, 1, 2
+MPS_SITE_HOST, MPS_SITE_DEVICE_COPY, MPS_SITE_DEVICE_BORROW, MPS_SITE_HOST_STREAM = 0, 1, 2, 3
 MPS_C128, MPS_C64 = 0, 1
 MPS_STATUS_FAILED, MPS_STATUS_FLAGGED = 1, 2
 

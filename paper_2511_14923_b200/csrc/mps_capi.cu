@@ -119,6 +119,9 @@ struct Site {
   double* gsum = nullptr;  // sum plane Gr + Gi (chi_l x sum_ld(N)) for the 3M GEMM, or null
   CUtensorMap tmap_gs;
   bool loaded = false;
+  // host-streamed site (MPS_SITE_HOST_STREAM): pinned host copy, uploaded per call into a ring slot
+  const double2* host = nullptr;
+  bool registered = false;  // we cudaHostRegister'ed it (unregister on release)
   // Ozaki (int8 tcgen05) digit planes of B_r^T, built on first use in gemm mode 8
   int8_t* oz = nullptr;
   int* oz_e = nullptr;
@@ -134,6 +137,9 @@ struct Site {
     if (blo) cudaFree(blo);
     if (oz) cudaFree(oz);
     if (oz_e) cudaFree(oz_e);
+    if (registered && host) cudaHostUnregister(const_cast<double2*>(host));
+    host = nullptr;
+    registered = false;
     oz = nullptr;
     oz_e = nullptr;
     data = nullptr;
@@ -190,6 +196,11 @@ struct mps_ctx {
   bool sum_planes = true;                           // feed the 3M GEMM precomputed sums
   int dtype = -1;                                   // MPS_C128 / MPS_C64, fixed by the first site
   int oz_S = 7;                                     // Ozaki digits per operand (gemm mode 8)
+  // host->HBM site streaming: 2-slot ring filled on a copy stream ahead of the GEMMs
+  cudaStream_t copy_st = nullptr;
+  cudaEvent_t slot_ready[2] = {}, slot_free[2][MAX_LANES] = {};
+  DevBuf<double2> sbuf[2];
+  DevBuf<double> ssum[2];
   DevBuf<int8_t> loz[MAX_LANES];                    // state digit planes per lane
   DevBuf<int> loz_e[MAX_LANES];
   DevBuf<float> la_hi[2][MAX_LANES], la_lo[2][MAX_LANES];  // c64 state planes (ping-pong)
@@ -602,6 +613,12 @@ int mps_create(int n_dev, const int* dev_ids, int layout, mps_ctx** out) {
   for (int l = 0; ok && l < mps_ctx::MAX_LANES; ++l)
     ok = cudaStreamCreateWithFlags(&c->lane_st[l], cudaStreamNonBlocking) == cudaSuccess &&
          cudaEventCreateWithFlags(&c->join_ev[l], cudaEventDisableTiming) == cudaSuccess;
+  ok = ok && cudaStreamCreateWithFlags(&c->copy_st, cudaStreamNonBlocking) == cudaSuccess;
+  for (int w = 0; ok && w < 2; ++w) {
+    ok = cudaEventCreateWithFlags(&c->slot_ready[w], cudaEventDisableTiming) == cudaSuccess;
+    for (int l = 0; ok && l < mps_ctx::MAX_LANES; ++l)
+      ok = cudaEventCreateWithFlags(&c->slot_free[w][l], cudaEventDisableTiming) == cudaSuccess;
+  }
   if (!ok) {
     cudaGetLastError();
     delete c;
@@ -647,6 +664,8 @@ int mps_set_site(mps_ctx* c, int m, int chi_l, int chi_r, int D, const void* gam
   s = Site();
   const size_t elems = (size_t)chi_l * chi_r * D;
   const bool dev = is_device_ptr(gamma);
+  if (dtype == MPS_C64 && flags == MPS_SITE_HOST_STREAM)
+    return fail(c, MPS_ERR_VALIDATION, "site %d: host streaming is implemented for complex128 sites", m);
   if (dtype == MPS_C64) {
     // keep only the tcgen05 operand planes of B_r^T (2N x ld fp32, hi / lo)
     const int N = chi_r * D, ld = plane_ld(2 * chi_l);
@@ -678,6 +697,23 @@ int mps_set_site(mps_ctx* c, int m, int chi_l, int chi_r, int D, const void* gam
     s.chi_r = chi_r;
     s.loaded = true;
     c->dtype = MPS_C64;
+    return MPS_OK;
+  }
+  if (flags == MPS_SITE_HOST_STREAM) {
+    if (dev) return fail(c, MPS_ERR_VALIDATION, "site %d: HOST_STREAM needs a host pointer", m);
+    cudaPointerAttributes at;
+    const bool pinned = cudaPointerGetAttributes(&at, gamma) == cudaSuccess && at.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    if (!pinned) {
+      CU(c, cudaHostRegister(const_cast<void*>(gamma), elems * sizeof(double2), cudaHostRegisterReadOnly),
+         "cudaHostRegister(site)");
+      s.registered = true;
+    }
+    s.host = (const double2*)gamma;
+    s.chi_l = chi_l;
+    s.chi_r = chi_r;
+    s.loaded = true;
+    c->dtype = MPS_C128;
     return MPS_OK;
   }
   if (flags == MPS_SITE_DEVICE_BORROW) {
@@ -783,8 +819,11 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
   }
   const bool use_sums = !c64 && c->sum_planes && c->gemm_mode == 3;
   const bool ozaki = !c64 && c->gemm_mode == 8;
-  if (ozaki)
+  if (ozaki) {
+    for (int m = m_begin; m < m_end; ++m)
+      if (c->sites[m].host) return fail(c, MPS_ERR_VALIDATION, "host-streamed sites do not support gemm mode 8");
     for (int m = m_begin; m < m_end; ++m) CU(c, ozaki_prepare_site(c->sites[m], D, c->oz_S), "Ozaki site digits");
+  }
 
   // ---- inputs: stage host arrays on the device ----
   const double* u_dev = uniforms;
@@ -894,8 +933,62 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
     v_in[l] = state_in ? (const double2*)state_in + (size_t)r0 * chi0 : c->ones.p + r0;
     vs_in[l] = !use_sums ? nullptr : state_in ? c->in_sum.p + (size_t)r0 * ld_vs_in : c->ones_sum.p + (size_t)r0 * 2;
   }
+  // host-streamed sites: stage the next two into the ring ahead of their GEMMs (copy stream)
+  std::vector<int> streamed;
+  for (int m = m_begin; m < m_end; ++m)
+    if (c->sites[m].host) streamed.push_back(m);
+  if (!streamed.empty()) {
+    size_t smax = 0, sumax = 0;
+    for (int m : streamed) {
+      smax = std::max(smax, (size_t)c->sites[m].chi_l * c->sites[m].chi_r * D);
+      sumax = std::max(sumax, (size_t)c->sites[m].chi_l * sum_ld(c->sites[m].chi_r * D));
+    }
+    for (int w = 0; w < 2; ++w) {
+      CU(c, c->sbuf[w].ensure(smax), "alloc site ring");
+      if (use_sums) CU(c, c->ssum[w].ensure(sumax), "alloc site ring sums");
+    }
+    CU(c, cudaEventRecord(c->fork_ev, st), "stream fork");
+    CU(c, cudaStreamWaitEvent(c->copy_st, c->fork_ev, 0), "stream fork wait");
+  }
+  auto upload = [&](int k) -> int {  // k-th streamed site of this call into slot k % 2
+    const int m = streamed[k], w = k % 2;
+    const Site& ss = c->sites[m];
+    if (k >= 2)  // the slot's previous occupant must have been consumed by every lane's GEMM
+      for (int l = 0; l < L; ++l) CU(c, cudaStreamWaitEvent(c->copy_st, c->slot_free[w][l], 0), "slot wait");
+    const size_t elems = (size_t)ss.chi_l * ss.chi_r * D;
+    CU(c, cudaMemcpyAsync(c->sbuf[w].p, ss.host, elems * sizeof(double2), cudaMemcpyHostToDevice, c->copy_st),
+       "H2D streamed site");
+    if (use_sums) {
+      const long long tot = (long long)elems;
+      sum_plane_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, c->copy_st>>>(c->sbuf[w].p, ss.chi_l, ss.chi_r * D,
+                                                                             c->ssum[w].p, sum_ld(ss.chi_r * D));
+      c->launches++;
+    }
+    CU(c, cudaEventRecord(c->slot_ready[w], c->copy_st), "slot ready");
+    return MPS_OK;
+  };
+  for (int k = 0; k < (int)streamed.size() && k < 2; ++k)
+    if (int rc = upload(k)) return rc;
+  int next_stream = 0;
+
   for (int m = m_begin; m < m_end; ++m) {
-    const Site& s = c->sites[m];
+    const Site& s0 = c->sites[m];
+    Site sl;  // a streamed site's ring view (its own tensor maps)
+    int slot = -1;
+    if (s0.host) {
+      slot = next_stream % 2;
+      sl = s0;
+      sl.host = nullptr;
+      sl.registered = false;
+      sl.data = c->sbuf[slot].p;
+      sl.gsum = use_sums ? c->ssum[slot].p : nullptr;
+      const uint64_t Nn = (uint64_t)s0.chi_r * D;
+      if (!make_tmap(&sl.tmap, sl.data, s0.chi_l, 2 * Nn, 16 * Nn, 8) ||
+          (sl.gsum && !make_tmap(&sl.tmap_gs, sl.gsum, s0.chi_l, Nn, 8 * (uint64_t)sum_ld((int)Nn), 8)))
+        return fail(c, MPS_ERR_GENERIC, "mode %d: streamed site tensor map failed", m);
+      for (int l = 0; l < L; ++l) CU(c, cudaStreamWaitEvent(lst[l], c->slot_ready[slot], 0), "slot ready wait");
+    }
+    const Site& s = s0.host ? sl : s0;
     const int N = s.chi_r * D;
     if (m > m_begin) ld_vs_in = sum_ld(s.chi_l);
     for (int l = 0; l < L; ++l) {  // K1 of every lane, then K2+K3 of every lane
@@ -929,6 +1022,12 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
         cudaEventRecord(rg.b, lst[l]);
         c->recs.push_back(rg);
       }
+    }
+    if (slot >= 0) {  // the GEMMs of this mode are queued: free the slot for streamed site k+2
+      for (int l = 0; l < L; ++l) CU(c, cudaEventRecord(c->slot_free[slot][l], lst[l]), "slot free");
+      if (next_stream + 2 < (int)streamed.size())
+        if (int rc = upload(next_stream + 2)) return rc;
+      ++next_stream;
     }
     for (int l = 0; l < L; ++l) {
       const int r0 = lane_r0[l], nl = lane_r0[l + 1] - r0;
@@ -996,6 +1095,10 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
       CU(c, cudaEventRecord(c->join_ev[l], lst[l]), "join");
       CU(c, cudaStreamWaitEvent(st, c->join_ev[l], 0), "join wait");
     }
+  }
+  if (!streamed.empty()) {  // the copy stream's work is older than the GEMMs that waited on it
+    CU(c, cudaEventRecord(c->join_ev[0], c->copy_st), "copy join");
+    CU(c, cudaStreamWaitEvent(st, c->join_ev[0], 0), "copy join wait");
   }
 
   // ---- outputs back to the host ----
@@ -1092,6 +1195,14 @@ void mps_destroy(mps_ctx* c) {
     if (c->join_ev[l]) cudaEventDestroy(c->join_ev[l]);
   }
   if (c->fork_ev) cudaEventDestroy(c->fork_ev);
+  for (int w = 0; w < 2; ++w) {
+    c->sbuf[w].release();
+    c->ssum[w].release();
+    if (c->slot_ready[w]) cudaEventDestroy(c->slot_ready[w]);
+    for (int l = 0; l < mps_ctx::MAX_LANES; ++l)
+      if (c->slot_free[w][l]) cudaEventDestroy(c->slot_free[w][l]);
+  }
+  if (c->copy_st) cudaStreamDestroy(c->copy_st);
   c->ones.release();
   c->alpha_d.release();
   c->disp_d.release();

@@ -106,7 +106,9 @@ class MpsSampler:
     """
 
     def __init__(self, mps: MPS, device: int = 0, layout: int = 0, sites_range=None, borrow: bool = True,
-                 sum_planes: bool = True):
+                 sum_planes: bool = True, stream_sites: bool = False):
+        """stream_sites: keep host (numpy) sites in pinned host memory and stream them into a
+        2-slot HBM ring per call (MPS_SITE_HOST_STREAM), for MPS larger than the GPU."""
         _native.require_cuda()
         import torch
 
@@ -133,7 +135,9 @@ class MpsSampler:
                 G = mps.sites[m]
                 if isinstance(G, np.ndarray):
                     G = np.ascontiguousarray(G, dtype=self.dtype)
-                    flags = _native.MPS_SITE_HOST
+                    flags = _native.MPS_SITE_HOST_STREAM if stream_sites else _native.MPS_SITE_HOST
+                    if stream_sites:
+                        self._keep.append(G)  # the library streams from this buffer on every call
                 else:
                     G = G.contiguous()
                     flags = _native.MPS_SITE_DEVICE_BORROW if borrow else _native.MPS_SITE_DEVICE_COPY

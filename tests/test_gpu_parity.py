@@ -573,3 +573,29 @@ def test_ozaki_chi1000_and_invariance():
     for o in outs[1:]:
         assert np.array_equal(o["counts"], outs[0]["counts"])
         assert np.array_equal(o["marginals"], outs[0]["marginals"])
+
+
+@pytest.mark.parametrize("lanes,sums", [(1, True), (2, True), (2, False)])
+def test_host_streamed_sites_bit_identical(c2_sites, lanes, sums):
+    """Sites kept in pinned host memory and streamed into the 2-slot HBM ring per call give the
+    same bits as resident sites."""
+    cfg = MpsSamplerConfig(N=300, seed=17, alpha_sigma=0.5, batch_size=150)
+    outs = []
+    for stream in (False, True):
+        with MpsSampler(MPS(c2_sites), stream_sites=stream, sum_planes=sums) as eng:
+            eng.set_lanes(lanes)
+            outs.append(eng.sample(cfg, return_marginals=True))
+            outs.append(eng.sample(cfg, return_marginals=True))  # the ring is reused across calls
+    for o in outs[1:]:
+        assert np.array_equal(o["counts"], outs[0]["counts"])
+        assert np.array_equal(o["marginals"], outs[0]["marginals"])
+
+
+def test_host_streamed_refusals(c2_sites):
+    sites64 = [s.astype(np.complex64) for s in c2_sites]
+    with pytest.raises(ValidationError):
+        MpsSampler(MPS(sites64), stream_sites=True)
+    with MpsSampler(MPS(c2_sites), stream_sites=True) as eng:
+        eng.set_gemm_mode(8)
+        with pytest.raises(ValidationError):
+            eng.sample(MpsSamplerConfig(N=10, seed=1))
