@@ -49,8 +49,38 @@ EncodeTiledFn get_encode_fn() {
 
 // 2-D row-major float64 matrix (rows x cols doubles, row pitch in bytes), box {box_cols, box_rows};
 // 16-double boxes use the 128B swizzle, 8-double boxes (sum planes of the state) the 64B one.
+// Encoding a tensor map costs microseconds of host time, as much as a launch: small chains
+// (chi ~ 100) re-encode the same few maps every mode, so they are cached by their arguments.
+struct TmapKey {
+  const void* base;
+  uint64_t rows, cols, pitch;
+  uint32_t box_rows, box_cols;
+  int kind;
+  bool operator<(const TmapKey& o) const {
+    return std::tie(base, rows, cols, pitch, box_rows, box_cols, kind) <
+           std::tie(o.base, o.rows, o.cols, o.pitch, o.box_rows, o.box_cols, o.kind);
+  }
+};
+static std::map<TmapKey, CUtensorMap> g_tmap_cache;
+static std::mutex g_tmap_mu;
+
+static bool tmap_cached(CUtensorMap* map, const TmapKey& k) {
+  std::lock_guard<std::mutex> lk(g_tmap_mu);
+  auto it = g_tmap_cache.find(k);
+  if (it == g_tmap_cache.end()) return false;
+  *map = it->second;
+  return true;
+}
+static void tmap_store(const CUtensorMap& map, const TmapKey& k) {
+  std::lock_guard<std::mutex> lk(g_tmap_mu);
+  if (g_tmap_cache.size() > 4096) g_tmap_cache.clear();  // buffers get reallocated: keep it bounded
+  g_tmap_cache[k] = map;
+}
+
 bool make_tmap(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t pitch_bytes,
                uint32_t box_rows, uint32_t box_cols = 16, bool fp32 = false) {
+  const TmapKey key{base, rows, cols, pitch_bytes, box_rows, box_cols, fp32 ? 1 : 0};
+  if (tmap_cached(map, key)) return true;
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return false;
   cuuint64_t dims[2] = {cols, rows};
@@ -62,7 +92,9 @@ bool make_tmap(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
                    const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    box_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
+  if (r != CUDA_SUCCESS) return false;
+  tmap_store(*map, key);
+  return true;
 }
 
 // int8 digit planes: rows x cols bytes, 32-byte boxes with the 32B swizzle (Ozaki K1)
