@@ -103,7 +103,7 @@ struct C64Cfg {
   static constexpr int A_BYTES = BM * BK * 4;  // 16 KiB per plane
   static constexpr int B_BYTES = BN * BK * 4;
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 2 * STAGES * 8 + 8 + 16;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 2 * STAGES * 8 + 5 * 8 + 16;
   static constexpr int TMEM_COLS = BN;  // fp32 accumulator, BN <= 256 (power of 2)
   static constexpr int THREADS = 192;
 };
@@ -235,6 +235,149 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)Cfg::TMEM_COLS));
+  }
+}
+
+// Persistent variant: grid = min(tiles, SMs); CTA c walks tiles c, c + G, ... (m fastest).  Two
+// TMEM accumulators (2 x BN columns): the MMA warp fills one while the epilogue warps drain the
+// other, so a tile's epilogue overlaps the next tile's mainloop; the TMA ring runs across tiles.
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, 1)
+    c64_gemm_persistent_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
+                               const __grid_constant__ CUtensorMap tm_bhi, const __grid_constant__ CUtensorMap tm_blo,
+                               float* __restrict__ C, int n, int N2, int KB, long long ldc) {
+  static_assert(2 * Cfg::BN <= 512, "two accumulators must fit TMEM");
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint64_t* empty = full + Cfg::STAGES;
+  uint64_t* acc_full = empty + Cfg::STAGES;  // [2]
+  uint64_t* acc_empty = acc_full + 2;        // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  constexpr uint32_t TMEM_COLS = 2 * Cfg::BN <= 256 ? 256 : 512;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int MT = (n + Cfg::BM - 1) / Cfg::BM;
+  const int ntiles = MT * ((N2 + Cfg::BN - 1) / Cfg::BN);
+  const int my_tiles = (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+
+  griddep_launch_dependents();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < Cfg::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&acc_full[a], 1);
+      mbar_init(&acc_empty[a], 4);  // one arrive per epilogue warp
+    }
+    fence_barrier_init();
+    prefetch_tmap(&tm_ahi);
+    prefetch_tmap(&tm_alo);
+    prefetch_tmap(&tm_bhi);
+    prefetch_tmap(&tm_blo);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer over all (tile, k-block) pairs ----
+      griddep_wait();
+      int g = 0;
+      for (int q = 0; q < my_tiles; ++q) {
+        const int tile = (int)blockIdx.x + q * (int)gridDim.x;
+        const int m0 = (tile % MT) * Cfg::BM, n0 = (tile / MT) * Cfg::BN;
+        for (int kb = 0; kb < KB; ++kb, ++g) {
+          const int s = g % Cfg::STAGES;
+          mbar_wait(&empty[s], ((g / Cfg::STAGES) & 1) ^ 1);
+          uint8_t* st = smem + s * Cfg::STAGE_BYTES;
+          mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
+          tma_load_2d(st, &tm_ahi, kb * Cfg::BK, m0, &full[s]);
+          tma_load_2d(st + Cfg::A_BYTES, &tm_alo, kb * Cfg::BK, m0, &full[s]);
+          tma_load_2d(st + 2 * Cfg::A_BYTES, &tm_bhi, kb * Cfg::BK, n0, &full[s]);
+          tma_load_2d(st + 2 * Cfg::A_BYTES + Cfg::B_BYTES, &tm_blo, kb * Cfg::BK, n0, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer ----
+      constexpr uint32_t idesc = idesc_tf32(Cfg::BM, Cfg::BN);
+      int g = 0;
+      for (int q = 0; q < my_tiles; ++q) {
+        const int a = q & 1;
+        mbar_wait(&acc_empty[a], ((q >> 1) & 1) ^ 1);  // the epilogue has drained this accumulator
+        tc_fence_after();
+        const uint32_t acc = tmem + a * Cfg::BN;
+        for (int kb = 0; kb < KB; ++kb, ++g) {
+          const int s = g % Cfg::STAGES;
+          mbar_wait(&full[s], (g / Cfg::STAGES) & 1);
+          tc_fence_after();
+          const uint32_t st = smem_u32(smem + s * Cfg::STAGE_BYTES);
+          const uint32_t ahi = st, alo = st + Cfg::A_BYTES, bhi = st + 2 * Cfg::A_BYTES, blo = bhi + Cfg::B_BYTES;
+#pragma unroll
+          for (int k = 0; k < Cfg::BK / 8; ++k) {
+            const uint32_t off = k * 32;
+            const uint64_t dah = umma_desc_k_sw128(ahi + off), dal = umma_desc_k_sw128(alo + off);
+            const uint64_t dbh = umma_desc_k_sw128(bhi + off), dbl = umma_desc_k_sw128(blo + off);
+            umma_tf32(acc, dah, dbh, idesc, (kb | k) != 0);
+            umma_tf32(acc, dah, dbl, idesc, 1u);
+            umma_tf32(acc, dal, dbh, idesc, 1u);
+          }
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&acc_full[a]);
+      }
+    }
+  } else {
+    // ---- epilogue warps 2..5: drain accumulator q & 1 while the next tile accumulates ----
+    const int qw = warp & 3;
+    for (int q = 0; q < my_tiles; ++q) {
+      const int a = q & 1;
+      const int tile = (int)blockIdx.x + q * (int)gridDim.x;
+      const int m0 = (tile % MT) * Cfg::BM, n0 = (tile / MT) * Cfg::BN;
+      mbar_wait(&acc_full[a], (q >> 1) & 1);
+      tc_fence_after();
+      const int row = m0 + 32 * qw + lane;
+      float* crow = C + (long long)row * ldc;
+#pragma unroll 1
+      for (int c0 = 0; c0 < Cfg::BN; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem + a * Cfg::BN + ((uint32_t)(32 * qw) << 16) + c0, r);
+        const int col = n0 + c0;
+        if (row < n) {
+          if (col + 32 <= N2 && (ldc & 3) == 0) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4)
+              *reinterpret_cast<float4*>(crow + col + j) =
+                  make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                              __uint_as_float(r[j + 3]));
+          } else if (col + 32 <= N2) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 2)
+              *reinterpret_cast<float2*>(crow + col + j) = make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1]));
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (col + j < N2) crow[col + j] = __uint_as_float(r[j]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[a]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
   }
 }
 
