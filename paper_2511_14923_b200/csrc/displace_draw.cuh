@@ -12,6 +12,7 @@
 
 #pragma once
 #include <cstdint>
+#include <type_traits>
 
 #include "c64_gemm.cuh"
 #include "ptx.cuh"
@@ -248,9 +249,16 @@ __device__ __forceinline__ float2 disp_row_f(const float2* T, int D, int k, cons
   return e;
 }
 
-template <int DT, bool C64>
+// RING: the C row streams through a 2-slot shared-memory ring of 128-j chunks filled by 1-D TMA
+// bulk copies (mbarrier per slot), for both passes; loads in flight cost no registers, so the
+// kernel stops being bound on global-load latency.  Each thread still owns j = tid + 128 c, so
+// the reduction order (and every result bit) is the same with and without the ring.
+template <int DT, bool C64, bool RING>
 __global__ void __launch_bounds__(DRAW_THREADS, C64 ? 8 : 4)
     displace_draw_kernel(DrawArgs A) {
+  using ElemT = typename std::conditional<C64, float2, double2>::type;
+  extern __shared__ __align__(16) uint8_t ring_smem[];
+  __shared__ uint64_t ring_bar[2];
   __shared__ double2 T[DMAX * DMAX];
   __shared__ float2 Tf[C64 ? DMAX * DMAX : 1];
   __shared__ double red[DRAW_THREADS / 32][DMAX];
@@ -264,12 +272,34 @@ __global__ void __launch_bounds__(DRAW_THREADS, C64 ? 8 : 4)
   const int D = DT ? DT : A.D;
   const unsigned long long gi = (unsigned long long)(A.first_index + b);
   const long long crow = (long long)b * A.ld_c + A.m;
-
   const long long cbase = (long long)b * A.ldc;
+  const ElemT* Crow = (C64 ? reinterpret_cast<const ElemT*>(A.C32) : reinterpret_cast<const ElemT*>(A.C)) + cbase;
+  const int nchunks = (A.chi_r + DRAW_THREADS - 1) / DRAW_THREADS;
+  const int chunk_elems = DRAW_THREADS * D;
+
+  // ring: chunk u (of the 2 * nchunks loads, pass 1 then pass 2) goes to slot u & 1
+  auto ring_issue = [&](int u) {
+    const int c = u % nchunks;
+    const int j0 = c * DRAW_THREADS;
+    const int nj = min(DRAW_THREADS, A.chi_r - j0);
+    const uint32_t bytes = (uint32_t)(nj * D * (int)sizeof(ElemT));
+    uint64_t* bar = &ring_bar[u & 1];
+    mbar_arrive_expect_tx(bar, bytes);
+    bulk_load_1d(ring_smem + (size_t)(u & 1) * chunk_elems * sizeof(ElemT), Crow + (long long)j0 * D, bytes, bar);
+  };
+  auto ring_slot = [&](int u) -> const ElemT* {
+    mbar_wait(&ring_bar[u & 1], (u >> 1) & 1);
+    return reinterpret_cast<const ElemT*>(ring_smem) + (size_t)(u & 1) * chunk_elems;
+  };
 
   // ---- displacement matrix for (b, m): inputs only, so it runs before the PDL wait and
   //      overlaps the tail of the site GEMM that produces C ----
   griddep_launch_dependents();
+  if (RING && tid == 0) {
+    mbar_init(&ring_bar[0], 1);
+    mbar_init(&ring_bar[1], 1);
+    fence_barrier_init();
+  }
   const bool ident = !(A.disp || A.alpha || A.alpha_sigma >= 0.0);
   if (A.disp) {
     const double2* src = A.disp + ((long long)b * A.M + A.m) * D * D;
@@ -288,65 +318,58 @@ __global__ void __launch_bounds__(DRAW_THREADS, C64 ? 8 : 4)
     for (int e = tid; e < D * D; e += DRAW_THREADS) Tf[e] = make_float2((float)T[e].x, (float)T[e].y);
   }
   griddep_wait();  // the GEMM (and transitively the previous draw) is complete: C, status valid
+  const bool dead = (A.status[b] & ST_FAILED) != 0;
+  if (RING && tid == 0 && !dead) {  // uses 0 and 1 (with one chunk, use 1 is pass 2's chunk 0)
+    ring_issue(0);
+    ring_issue(1);
+  }
   __syncthreads();
 
-  if (A.status[b] & ST_FAILED) {  // dead sample: zero state, count -1 (deterministic chain)
+  if (dead) {  // dead sample: zero state, count -1 (deterministic chain)
     for (int j = tid; j < A.chi_r; j += DRAW_THREADS) store_state<C64>(A, b, j, make_double2(0.0, 0.0));
     if (tid == 0) A.counts[crow] = -1;
     if (A.marg && tid < D) A.marg[crow * D + tid] = 0.0;
     return;
   }
 
-  // ---- pass 1: partial marginals ----
+  // ---- pass 1: partial marginals (thread tid owns j = tid + 128 c) ----
   constexpr int DR = DT ? DT : DMAX;
-  if constexpr (C64) {
-    float acc[DR];
+  using AccT = typename std::conditional<C64, float, double>::type;
+  AccT acc[DR];
 #pragma unroll
-    for (int k = 0; k < DR; ++k) acc[k] = 0.f;
-    for (int j = tid; j < A.chi_r; j += DRAW_THREADS) {
-      float2 c[DR];
+  for (int k = 0; k < DR; ++k) acc[k] = AccT(0);
+  for (int cidx = 0; cidx < nchunks; ++cidx) {
+    const int j = cidx * DRAW_THREADS + tid;
+    const ElemT* src = RING ? ring_slot(cidx) + tid * D : Crow + (long long)j * D;
+    if (j < A.chi_r) {
+      ElemT c[DR];
 #pragma unroll
       for (int d = 0; d < DR; ++d)
-        if (DT || d < D) c[d] = A.C32[cbase + (long long)j * D + d];
+        if (DT || d < D) c[d] = src[d];
 #pragma unroll
       for (int k = 0; k < DR; ++k) {
         if (!DT && k >= D) break;
-        const float2 e = ident ? c[k] : disp_row_f<DT>(Tf, D, k, c);
-        acc[k] = fmaf(e.x, e.x, fmaf(e.y, e.y, acc[k]));
+        if constexpr (C64) {
+          const float2 e = ident ? c[k] : disp_row_f<DT>(Tf, D, k, c);
+          acc[k] = fmaf(e.x, e.x, fmaf(e.y, e.y, acc[k]));
+        } else {
+          const double2 e = ident ? c[k] : disp_row<DT>(T, D, k, c);
+          acc[k] = fma(e.x, e.x, fma(e.y, e.y, acc[k]));
+        }
       }
     }
-#pragma unroll
-    for (int k = 0; k < DR; ++k) {
-      if (!DT && k >= D) break;
-      float v = acc[k];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0) red[warp][k] = (double)v;
+    if (RING) {
+      __syncthreads();  // every thread is done with this slot
+      if (tid == 0 && cidx + 2 < 2 * nchunks) ring_issue(cidx + 2);  // pass 1's next chunk, or pass 2's first
     }
-  } else {
-    double acc[DR];
+  }
 #pragma unroll
-    for (int k = 0; k < DR; ++k) acc[k] = 0.0;
-    for (int j = tid; j < A.chi_r; j += DRAW_THREADS) {
-      double2 c[DR];
+  for (int k = 0; k < DR; ++k) {
+    if (!DT && k >= D) break;
+    AccT v = acc[k];
 #pragma unroll
-      for (int d = 0; d < DR; ++d)
-        if (DT || d < D) c[d] = load_c<C64>(A, cbase + (long long)j * D + d);
-#pragma unroll
-      for (int k = 0; k < DR; ++k) {
-        if (!DT && k >= D) break;
-        const double2 e = ident ? c[k] : disp_row<DT>(T, D, k, c);
-        acc[k] = fma(e.x, e.x, fma(e.y, e.y, acc[k]));
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < DR; ++k) {
-      if (!DT && k >= D) break;
-      double v = acc[k];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0) red[warp][k] = v;
-    }
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp][k] = (double)v;
   }
   __syncthreads();
   if (tid < D) {  // fixed order over warps
@@ -395,45 +418,49 @@ __global__ void __launch_bounds__(DRAW_THREADS, C64 ? 8 : 4)
   }
 
   // ---- pass 2: gather + renormalise ----
-  if (ks < 0) {
-    for (int j = tid; j < A.chi_r; j += DRAW_THREADS) store_state<C64>(A, b, j, make_double2(0.0, 0.0));
-    return;
-  }
-  if constexpr (C64) {
-    const float fs = (float)scale;
-    for (int j = tid; j < A.chi_r; j += DRAW_THREADS) {
-      float2 e;
-      if (ident) {
-        e = A.C32[cbase + (long long)j * D + ks];
+  for (int cidx = 0; cidx < nchunks; ++cidx) {
+    const int j = cidx * DRAW_THREADS + tid;
+    const ElemT* src = RING ? ring_slot(nchunks + cidx) + tid * D : Crow + (long long)j * D;
+    if (j < A.chi_r) {
+      if (ks < 0) {
+        store_state<C64>(A, b, j, make_double2(0.0, 0.0));
+      } else if constexpr (C64) {
+        const float fs = (float)scale;
+        float2 e;
+        if (ident) {
+          e = src[ks];
+        } else {
+          float2 c[DR];
+#pragma unroll
+          for (int d = 0; d < DR; ++d)
+            if (DT || d < D) c[d] = src[d];
+          e = disp_row_f<DT>(Tf, D, ks, c);
+        }
+        store_state<true>(A, b, j, make_double2(e.x * fs, e.y * fs));
       } else {
-        float2 c[DR];
+        double2 e;
+        if (ident) {
+          e = src[ks];
+        } else {
+          e = make_double2(0.0, 0.0);
 #pragma unroll
-        for (int d = 0; d < DR; ++d)
-          if (DT || d < D) c[d] = A.C32[cbase + (long long)j * D + d];
-        e = disp_row_f<DT>(Tf, D, ks, c);
-      }
-      store_state<true>(A, b, j, make_double2(e.x * fs, e.y * fs));
-    }
-    return;
-  }
-  for (int j = tid; j < A.chi_r; j += DRAW_THREADS) {
-    double2 e;
-    if (ident) {
-      e = load_c<C64>(A, cbase + (long long)j * D + ks);
-    } else {
-      e = make_double2(0.0, 0.0);
-#pragma unroll
-      for (int d = 0; d < DR; ++d) {
-        if (!DT && d >= D) break;
-        const double2 c = load_c<C64>(A, cbase + (long long)j * D + d);
-        const double2 tk = lds_c128(&T[ks * D + d]);
-        e.x = fma(tk.x, c.x, e.x);
-        e.x = fma(-tk.y, c.y, e.x);
-        e.y = fma(tk.x, c.y, e.y);
-        e.y = fma(tk.y, c.x, e.y);
+          for (int d = 0; d < DR; ++d) {
+            if (!DT && d >= D) break;
+            const double2 c = src[d];
+            const double2 tk = lds_c128(&T[ks * D + d]);
+            e.x = fma(tk.x, c.x, e.x);
+            e.x = fma(-tk.y, c.y, e.x);
+            e.y = fma(tk.x, c.y, e.y);
+            e.y = fma(tk.y, c.x, e.y);
+          }
+        }
+        store_state<false>(A, b, j, make_double2(e.x * scale, e.y * scale));
       }
     }
-    store_state<C64>(A, b, j, make_double2(e.x * scale, e.y * scale));
+    if (RING) {
+      __syncthreads();
+      if (tid == 0 && nchunks + cidx + 2 < 2 * nchunks) ring_issue(nchunks + cidx + 2);
+    }
   }
 }
 

@@ -228,6 +228,7 @@ struct mps_ctx {
   bool sum_planes = true;                           // feed the 3M GEMM precomputed sums
   int dtype = -1;                                   // MPS_C128 / MPS_C64, fixed by the first site
   int oz_S = 7;                                     // Ozaki digits per operand (gemm mode 8)
+  bool draw_ring = true;                            // stage C rows through a TMA ring in the draw kernel
   // host->HBM site streaming: 2-slot ring filled on a copy stream ahead of the GEMMs
   cudaStream_t copy_st = nullptr;
   cudaEvent_t slot_ready[2] = {}, slot_free[2][MAX_LANES] = {};
@@ -313,6 +314,20 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+// draw kernel instantiation for (D, dtype, ring)
+static void (*draw_kernel_for(int D, bool c64, bool ring))(DrawArgs) {
+  if (c64) {
+    if (ring) return D == 10 ? displace_draw_kernel<10, true, true> : D == 4 ? displace_draw_kernel<4, true, true>
+                                                                             : displace_draw_kernel<0, true, true>;
+    return D == 10 ? displace_draw_kernel<10, true, false> : D == 4 ? displace_draw_kernel<4, true, false>
+                                                                    : displace_draw_kernel<0, true, false>;
+  }
+  if (ring) return D == 10 ? displace_draw_kernel<10, false, true> : D == 4 ? displace_draw_kernel<4, false, true>
+                                                                            : displace_draw_kernel<0, false, true>;
+  return D == 10 ? displace_draw_kernel<10, false, false> : D == 4 ? displace_draw_kernel<4, false, false>
+                                                                   : displace_draw_kernel<0, false, false>;
 }
 
 // K1 operands of one launch.  Vs / tgs (the sum planes) may be null: the 3M kernel then
@@ -700,6 +715,10 @@ int mps_create(int n_dev, const int* dev_ids, int layout, mps_ctx** out) {
     cudaGetLastError();
     delete c;
     return MPS_ERR_GENERIC;
+  }
+  {
+    const char* e = getenv("MPS_DRAW_RING");
+    if (e && e[0] == '0') c->draw_ring = false;
   }
   *out = c;
   return MPS_OK;
@@ -1146,14 +1165,22 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
         cudaEventRecord(rd.a, lst[l]);
       }
       {
-        void (*dk)(DrawArgs);
-        if (c64)
-          dk = (D == 10) ? displace_draw_kernel<10, true> : (D == 4) ? displace_draw_kernel<4, true>
-                                                                     : displace_draw_kernel<0, true>;
-        else
-          dk = (D == 10) ? displace_draw_kernel<10, false> : (D == 4) ? displace_draw_kernel<4, false>
-                                                                      : displace_draw_kernel<0, false>;
-        CU(c, launch_pdl(dk, dim3(nl), dim3(DRAW_THREADS), 0, lst[l], a), "displace_draw launch");
+        // the C row streams through a shared-memory TMA ring when its bytes are 16-B granular
+        const size_t esz = c64 ? 8 : 16;
+        const bool ring = c->draw_ring && ((size_t)N * esz) % 16 == 0;
+        const size_t ring_bytes = ring ? 2 * (size_t)DRAW_THREADS * D * esz : 0;
+        void (*dk)(DrawArgs) = draw_kernel_for(D, c64, ring);
+        if (ring) {
+          static bool attr_set[2][3] = {};
+          const int di = D == 10 ? 0 : D == 4 ? 1 : 2;
+          if (!attr_set[c64][di]) {
+            CU(c, cudaFuncSetAttribute(dk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       2 * DRAW_THREADS * DMAX * 16),
+               "draw ring smem");
+            attr_set[c64][di] = true;
+          }
+        }
+        CU(c, launch_pdl(dk, dim3(nl), dim3(DRAW_THREADS), ring_bytes, lst[l], a), "displace_draw launch");
       }
       c->launches++;
       if (c->profile & 2) {
