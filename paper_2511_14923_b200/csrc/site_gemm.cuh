@@ -282,11 +282,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
           // 64B swizzle: 16B chunk t of a 64B row XOR (row >> 1) & 3, row & 7 == g
           as[mf] = *reinterpret_cast<const double*>(Ass + mf * 8 * 64 + ((t ^ ((g >> 1) & 3)) << 4) + (step << 3));
         } else {
-#ifdef MPS_EXPERIMENT_NO_DADD  // timing experiment only: wrong results
-          as[mf] = v.x;
-#else
           as[mf] = __dadd_rn(v.x, v.y);
-#endif
         }
       }
 #pragma unroll
@@ -301,11 +297,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
           const int c = ((fi & 1) * 4 + (g >> 1)) ^ i;
           bs[nf] = *reinterpret_cast<const double*>(Bss + (fi >> 1) * 1024 + i * 128 + (c << 4) + ((g & 1) << 3));
         } else {
-#ifdef MPS_EXPERIMENT_NO_DADD
-          bs[nf] = w.y;
-#else
           bs[nf] = __dadd_rn(w.x, w.y);
-#endif
         }
       }
 #pragma unroll

@@ -129,3 +129,118 @@ def gather_columns(local, m_begin: int, M: int, rank: int, world: int, dst: int 
         mb, w = int(m[0].item()), int(m[1].item())
         out[:, mb: mb + w] = b[:, :w]
     return out
+
+
+# ---------------------------------------------------------------------------------------------
+# user-facing multi-GPU sampling (one process per GPU, torch.distributed initialised)
+# ---------------------------------------------------------------------------------------------
+
+
+def _dist_info():
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_rank(), dist.get_world_size()
+    return 0, 1
+
+
+def sample_sharded(config, mps, device: int | None = None, group=None):
+    """Sample-sharded batch_sample: every rank holds the whole MPS and samples the contiguous
+    index block shard_range(N, rank, world); counts are gathered to rank 0 (the only
+    collective, after sampling).  Returns an MpsSampleBatch on rank 0, None elsewhere.
+    Output is identical to single-GPU batch_sample for any world size (counter streams)."""
+    import time
+
+    import torch
+
+    from .sampler import MpsSampleBatch, MpsSampler
+    from . import _native
+
+    rank, world = _dist_info()
+    dev = torch.cuda.current_device() if device is None else device
+    a, b = shard_range(config.N, rank, world)
+    t0 = time.perf_counter()
+    with MpsSampler(mps, device=dev) as eng:
+        res = eng.sample(config, start=a, stop=b)
+    counts = torch.from_numpy(res["counts"]).to(dev)
+    status = torch.from_numpy(res["status"]).to(dev)
+    if world > 1:
+        counts = gather_rows(counts, rank, world, group=group)
+        status = gather_rows(status, rank, world, group=group)
+    if rank != 0:
+        return None
+    counts, status = counts.cpu().numpy(), status.cpu().numpy()
+    failed = (status & _native.MPS_STATUS_FAILED) != 0
+    keep = ~failed
+    wall = time.perf_counter() - t0
+    return MpsSampleBatch(M=mps.M, N=int(keep.sum()), counts=counts[keep], method="mps", seed=config.seed, D=mps.D,
+                          chi=mps.chi, wall_time=wall, per_sample_mean=wall / max(int(keep.sum()), 1),
+                          n_failed=int(failed.sum()),
+                          n_flagged=int(((status & _native.MPS_STATUS_FLAGGED) != 0)[keep].sum()),
+                          indices=np.nonzero(keep)[0])
+
+
+def sample_pipelined(config, mps_block, device: int | None = None, group=None):
+    """Mode-pipelined batch_sample: rank g holds the sites of stage_blocks(...)[g] (the other
+    sites may be SiteShape placeholders), micro-batches of config.batch_size samples flow
+    through the ranks with the n x chi state handed on by send/recv; each rank's count columns
+    are gathered to rank 0.  Returns an MpsSampleBatch on rank 0, None elsewhere."""
+    import time
+
+    import torch
+
+    from .sampler import MpsSampleBatch, MpsSampler
+    from . import _native
+
+    rank, world = _dist_info()
+    dev = torch.cuda.current_device() if device is None else device
+    dims = mps_block.bond_dims
+    mb, me = stage_blocks(dims, mps_block.D, world)[rank]
+    n = config.batch_size or 1024
+    N = config.N
+    T = (N + n - 1) // n
+    cdt = torch.complex64 if mps_block.dtype == "complex64" else torch.complex128
+    counts = torch.zeros((T * n, mps_block.M), dtype=torch.int32, device=dev)
+    status = torch.zeros(T * n, dtype=torch.uint8, device=dev)
+    y = torch.empty((n, dims[me]), dtype=cdt, device=dev) if rank < world - 1 else None
+    t0 = time.perf_counter()
+    with MpsSampler(mps_block, device=dev, sites_range=(mb, me), layout=1) as eng:
+        eng.set_streams(config.seed, config.alpha_sigma)
+
+        def stage(t, x):
+            # the last micro-batch may be short: pad to n rows (the padding samples are dropped)
+            eng.run(t * n, n, counts[t * n:(t + 1) * n], m_begin=mb, m_end=me, state_in=x, state_out=y,
+                    status=status[t * n:(t + 1) * n])
+            return y
+
+        if world > 1:
+            run_pipeline(stage, T, recv_like=lambda: torch.empty((n, dims[mb]), dtype=cdt, device=dev),
+                         send_like=lambda: torch.empty((n, dims[me]), dtype=cdt, device=dev), rank=rank, world=world,
+                         group=group)
+        else:
+            for t in range(T):
+                stage(t, None)
+        torch.cuda.synchronize(dev)
+    local = counts[:, mb:me].contiguous()
+    if world > 1:
+        allc = gather_columns(local, mb, mps_block.M, rank, world, group=group)
+        import torch.distributed as dist
+
+        # status bits OR-ed over the stages (NCCL has no bitwise reduce: MAX per bit)
+        bits = torch.stack([status & 1, (status >> 1) & 1]).to(torch.int32)
+        dist.all_reduce(bits, op=dist.ReduceOp.MAX, group=group)
+        status = (bits[0] | (bits[1] << 1)).to(torch.uint8)
+    else:
+        allc = counts
+    if rank != 0:
+        return None
+    counts_np = allc[:N].cpu().numpy()
+    st = status[:N].cpu().numpy()
+    failed = (st & _native.MPS_STATUS_FAILED) != 0
+    keep = ~failed
+    wall = time.perf_counter() - t0
+    return MpsSampleBatch(M=mps_block.M, N=int(keep.sum()), counts=counts_np[keep], method="mps", seed=config.seed,
+                          D=mps_block.D, chi=max(dims), wall_time=wall,
+                          per_sample_mean=wall / max(int(keep.sum()), 1), n_failed=int(failed.sum()),
+                          n_flagged=int(((st & _native.MPS_STATUS_FLAGGED) != 0)[keep].sum()),
+                          indices=np.nonzero(keep)[0])

@@ -599,3 +599,15 @@ def test_host_streamed_refusals(c2_sites):
         eng.set_gemm_mode(8)
         with pytest.raises(ValidationError):
             eng.sample(MpsSamplerConfig(N=10, seed=1))
+
+
+def test_distributed_entry_points_single_rank(c2_sites):
+    """sample_sharded / sample_pipelined at world size 1 reproduce batch_sample (the
+    multi-rank schedule itself is covered over gloo in tests/test_distributed.py)."""
+    from paper_2511_14923_b200.distributed import sample_pipelined, sample_sharded
+
+    cfg = MpsSamplerConfig(N=250, seed=31, alpha_sigma=0.5, batch_size=100)
+    ref = batch_sample(cfg, MPS(c2_sites))
+    a = sample_sharded(cfg, MPS(c2_sites))
+    b = sample_pipelined(cfg, MPS(c2_sites))
+    assert np.array_equal(a.counts, ref.counts) and np.array_equal(b.counts, ref.counts)
