@@ -351,6 +351,128 @@ def run_pipelined(args, rank, world, local, W, K, config, dims):
     return line
 
 
+def run_stage(args, local, W, K, config, dims):
+    """One stage of a G-stage mode pipeline on this GPU (configs c4/c5 exceed one B200):
+    the flops-balanced site block of stage g (distributed.stage_blocks), fed a random
+    normalised n x chi state per micro-batch as the upstream stage's hand-off would be.
+    Stages are flops-balanced and the hand-off (n x chi complex per micro-batch) is < 0.1%
+    of a stage's time, so the pipeline's steady-state throughput is
+    the slowest stage's samples/s, and with T micro-batches it is that x T / (T + G - 1)."""
+    import torch
+
+    from paper_2511_14923_b200 import MPS, MpsSampler
+    from paper_2511_14923_b200.distributed import stage_blocks
+
+    M, chi, D, n, sigma, N_total, desc = CONFIGS[args.config]
+    n = args.n or n
+    G, g = args.stage_of, args.stage
+    dev = torch.device("cuda", local)
+    blocks = stage_blocks(dims, D, G)
+    mb, me = blocks[g]
+    t_setup = time.perf_counter()
+    mps = MPS.random(M, chi, D, seed=0, device=dev, block=(mb, me))
+    if args.dtype == "c64":
+        mps = mps.astype("complex64")
+    torch.cuda.empty_cache()
+    block_bytes = sum(dims[m] * dims[m + 1] for m in range(mb, me)) * D * (8.0 if args.dtype == "c64" else 16.0)
+    eng = MpsSampler(mps, device=local, sites_range=(mb, me), layout=1)
+    eng.set_lanes(args.lanes)
+    eng.set_gemm_mode({"3m": 3, "4m": 4, "ozaki": 8}[args.gemm])
+    eng.set_streams(0, sigma)
+    cdt = torch.complex64 if args.dtype == "c64" else torch.complex128
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + g)
+    nst = W + K
+    x = torch.randn((nst, n, dims[mb]), dtype=cdt, device=dev, generator=gen)
+    x /= torch.linalg.vector_norm(x, dim=2, keepdim=True)
+    counts = torch.empty((nst, n, M), dtype=torch.int32, device=dev)
+    status = torch.zeros((nst, n), dtype=torch.uint8, device=dev)
+    y = torch.empty((n, dims[me]), dtype=cdt, device=dev) if me < M else None
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t_setup
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+
+    def step(s, copy_out=None):
+        eng.run(s * n, n, counts[s], m_begin=mb, m_end=me, state_in=x[s] if mb > 0 else None, state_out=y,
+                status=status[s], stream=stream.cuda_stream)
+        if copy_out is not None:
+            copy_out.copy_(counts[s, :, mb:me], non_blocking=True)
+
+    for s in range(W):
+        step(s)
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    clocks.start()
+    l0 = eng.kernel_launches
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for s in range(W, W + K):
+        step(s)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    launches = eng.kernel_launches - l0
+    ck = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    c_host = torch.empty((n, me - mb), dtype=torch.int32).pin_memory()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    for s in range(W, W + K):
+        step(s, copy_out=c_host)
+    e3.record(stream)
+    torch.cuda.synchronize()
+    ms_e2e = e2.elapsed_time(e3)
+    eng.set_lanes(1)
+    step(0)
+    torch.cuda.synchronize()
+    eng.profile(1)
+    for s in range(W, W + min(K, 2)):
+        step(s)
+    torch.cuda.synchronize()
+    prof = eng.profile_read()
+    eng.profile(0)
+    peak, peak_src = fp64_peak()
+    gemm_ms_avg = prof["gemm_ms"] / max(prof["gemm_launches"], 1)
+    gemm_flops_avg = prof["gemm_flops"] / max(prof["gemm_launches"], 1)
+    achieved = gemm_flops_avg / (gemm_ms_avg / 1e3) / 1e12 if gemm_ms_avg > 0 else 0.0
+    kernel_name = {"3m": "site_gemm3m_kernel (K1, FP64 DMMA, 3M)", "4m": "site_gemm_kernel (K1, FP64 DMMA, 4M)",
+                   "ozaki": "ozaki_gemm_kernel (K1, fp64 emulated on INT8 tcgen05, 7 digits)"}[args.gemm]
+    if args.dtype == "c64":
+        bf16, src = measured_bf16()
+        achieved, peak = 3.0 * achieved, bf16 / 2.0
+        peak_src = f"dense TF32 = 1/2 of {src} bf16 {bf16:.0f} TFLOP/s"
+        kernel_name = "c64_gemm_kernel (K1, tcgen05 kind::tf32, 3xTF32; achieved = executed tensor flops)"
+    stage_flops = sum(site_flops(dims, D, n)[mb:me])
+    value = K * n / (ms / 1e3)
+    T = (N_total + n - 1) // n
+    ok = not bool((status[W:] & 1).any().item())
+    cfg = dict(config, layout=f"one stage of a {G}-stage mode pipeline, measured alone on one B200",
+               l2="inputs larger than L2 (stage sites %.1f GB streamed per step)" % (block_bytes / 1e9),
+               stage=g, stage_blocks=blocks, stage_sites=[mb, me], stage_site_bytes=block_bytes,
+               state_in="random normalised n x chi_l state per micro-batch (the upstream hand-off)")
+    line = {
+        "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": 1, "steps": K, "warmup": W,
+        "ms_per_step": ms / K, "higher_is_better": True, "scaling": "stage", "vs_baseline": None,
+        "dtype": args.dtype, "data": "synthetic (random row-orthonormal sites of this stage's block, generated "
+                                     "on the device from per-site seeds; device counter-stream uniforms and alpha)",
+        "config": cfg,
+        "e2e": {"value": K * n / (ms_e2e / 1e3), "unit": "samples/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": n * (me - mb) * 4},
+        "gpu_launches": int(launches),
+        "pipeline_estimate": {
+            "samples_per_s": value * T / (T + G - 1), "micro_batches": T, "stages": G,
+            "note": f"{G}-GPU pipeline steady state = this stage's rate (stages flops-balanced, hand-off < 0.1%), "
+                    f"x T/(T+G-1) fill/drain for N={N_total}"},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak if peak else None, "traffic": None, "kernel": kernel_name,
+                     "peak_source": peak_src, "per_launch": {"ms": gemm_ms_avg, "algorithmic_flops": gemm_flops_avg},
+                     "stage_chain_tflops": K * stage_flops / (ms / 1e3) / 1e12},
+        "clocks": ck, "valid_outputs": ok, "setup_s": setup_s,
+    }
+    eng.close()
+    return line
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -368,6 +490,12 @@ def main():
                     help="c64: complex64 chain, K1 on tcgen05 (3xTF32), parity 1e-4")
     ap.add_argument("--layout", default="auto", choices=["auto", "sharded", "pipelined"],
                     help="auto: sample-sharded when the MPS fits one GPU, else mode-pipelined")
+    ap.add_argument("--stage-of", type=int, default=0,
+                    help="measure one stage (--stage g) of a G-stage mode pipeline alone on one GPU (c4/c5)")
+    ap.add_argument("--stage", type=int, default=0)
+    ap.add_argument("--n", type=int, default=0,
+                    help="pipeline micro-batch size for --stage-of runs (default: the config's batch n); "
+                         "per-sample results do not depend on it")
     args = ap.parse_args()
     W = max(args.warmup, 3)
     K = args.steps
@@ -378,7 +506,7 @@ def main():
     from paper_2511_14923_b200.mps import bond_dims
 
     dims = bond_dims(M, chi, D)
-    config = {"workload": f"{args.config}: {desc}", "M": M, "chi": chi, "D": D, "n": n, "gemm": args.gemm,
+    config = {"workload": f"{args.config}: {desc}", "M": M, "chi": chi, "D": D, "n": args.n or n, "gemm": args.gemm,
               "sites_in": "host, streamed per step" if args.stream_sites else "HBM",
               "alpha": "CN(0,%.3g)" % (sigma * sigma), "sites": "random row-orthonormal, seed 0",
               "layout": "sample-sharded" if world > 1 else "single GPU",
@@ -415,6 +543,11 @@ def main():
     if layout == "auto":
         layout = "sharded" if site_bytes * 1.5 < HBM_USABLE else "pipelined"
     torch.cuda.set_device(local)
+    if args.stage_of > 0:
+        if world > 1 or not 0 <= args.stage < args.stage_of:
+            raise SystemExit("--stage-of runs one stage on one GPU: need world 1 and 0 <= --stage < --stage-of")
+        print(json.dumps(run_stage(args, local, W, K, config, dims)), flush=True)
+        return
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     if layout == "pipelined":

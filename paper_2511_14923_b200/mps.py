@@ -59,10 +59,14 @@ def device_site(seed: int, m: int, chi_l: int, chi_r: int, D: int, device="cuda"
     g.manual_seed((int(seed) * 1_000_003 + int(m)) & (2**63 - 1))
     Z = torch.randn(chi_r * D, chi_l, dtype=torch.complex128, device=device, generator=g)
     Q, R = torch.linalg.qr(Z)
+    del Z
     d = torch.diagonal(R)
-    Q = Q * (d / d.abs())
+    Q.mul_(d / d.abs())
+    del R, d
     out = Q.conj().T.reshape(chi_l, chi_r, D).contiguous()
-    del Z, Q, R
+    del Q
+    if out.numel() * 16 > 2**31:  # multi-GB sites (config 5): return the QR transients to the device
+        torch.cuda.empty_cache()
     return out
 
 
