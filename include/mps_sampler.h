@@ -170,7 +170,8 @@ int mps_set_gemm_mode(mps_ctx* ctx, int mode);
 /* complex128 K1 emulated on the INT8 tensor cores (Ozaki scheme with S = 5..7 digits):
  * C (n x N) = V (n x K) . G (K x N), all complex128.  Test/benchmark entry (slices per call). */
 int mps_site_gemm_ozaki(const void* V, const void* G, void* C, int n, int K, int N, int S, uint64_t stream);
-/* Its pieces: int8 digit planes (S stacked planes of rows_pad x ld bytes, ld % 16 == 0) and
+/* Its pieces: int8 digit planes (S planes of rows_pad x ld bytes in the tiled stage layout of
+ * ozaki_gemm.cuh; ld = 2K rounded up to a multiple of 32, rows_pad a multiple of 256) and
  * exponents of a state (n x K) and of a site's B_r^T (2N rows), and the GEMM on them. */
 int mps_ozaki_state_planes(const void* V, int n, int K, int S, int8_t* planes, int* e, int ld, int n_pad,
                            uint64_t stream);

@@ -97,35 +97,10 @@ bool make_tmap(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
   return true;
 }
 
-// int8 digit planes: rows x cols bytes, 32-byte boxes with the 32B swizzle (Ozaki K1)
-bool make_tmap_u8(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t pitch, uint32_t box_rows) {
-  EncodeTiledFn enc = get_encode_fn();
-  if (!enc) return false;
-  cuuint64_t dims[2] = {cols, rows};
-  cuuint64_t strides[1] = {pitch};
-  cuuint32_t box[2] = {32, box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
-// S stacked digit planes (plane p at rows [p * rows_pad, (p+1) * rows_pad)) as one 3-D tensor,
-// so a single TMA op brings a {32 B x box_rows x S} box: all digits of a tile for one K step
-bool make_tmap_u8_planes(CUtensorMap* map, const void* base, uint64_t rows_pad, uint64_t cols, uint64_t pitch, int S,
-                         uint32_t box_rows) {
-  EncodeTiledFn enc = get_encode_fn();
-  if (!enc) return false;
-  cuuint64_t dims[3] = {cols, rows_pad, (cuuint64_t)S};
-  cuuint64_t strides[2] = {pitch, pitch * rows_pad};
-  cuuint32_t box[3] = {32, box_rows, (cuuint32_t)S};
-  cuuint32_t estr[3] = {1, 1, 1};
-  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
+// K bytes of a real-doubled Ozaki operand row (2 chi_l int8), padded to whole 32-byte k steps
+inline int oz_ld(int K) { return round_up(2 * K, 32); }
 
 // fp32 plane row pitch (floats): TMA needs 16-byte row strides
 inline int plane_ld(int cols_fp32) { return (cols_fp32 + 3) & ~3; }
@@ -515,10 +490,10 @@ static int launch_site_gemm(mps_ctx* ctx, const GemmOps& o, cudaStream_t st, int
 }
 
 // ---- complex128 K1 emulated on the INT8 tensor cores (Ozaki scheme, gemm mode 8) -----------------
-template <int S>
-static cudaError_t launch_ozaki_s(const int8_t* a_planes, int n_pad, const int* ea, const int8_t* b_planes, int b_pad,
-                                  const int* eb, int ld, double2* C, int n, int K, int N, cudaStream_t st) {
-  using Cfg = OzCfg<S>;
+template <int S, int CM, int CN>
+static cudaError_t launch_ozaki_cl(const int8_t* a_planes, int n_pad, const int* ea, const int8_t* b_planes, int b_pad,
+                                   const int* eb, int ld, double2* C, int n, int K, int N, cudaStream_t st) {
+  using Cfg = OzCfg<S, CM, CN>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(ozaki_gemm_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -526,14 +501,84 @@ static cudaError_t launch_ozaki_s(const int8_t* a_planes, int n_pad, const int* 
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  CUtensorMap ta, tb;
-  if (!make_tmap_u8_planes(&ta, a_planes, n_pad, 2 * (uint64_t)K, ld, S, Cfg::BM) ||
-      !make_tmap_u8_planes(&tb, b_planes, b_pad, 2 * (uint64_t)K, ld, S, Cfg::BN))
-    return cudaErrorInvalidValue;
-  dim3 grid((n + Cfg::BM - 1) / Cfg::BM, (2 * N + Cfg::BN - 1) / Cfg::BN);
-  const int KB = (2 * K + Cfg::BK - 1) / Cfg::BK;
-  return launch_pdl(ozaki_gemm_kernel<Cfg>, grid, dim3(Cfg::THREADS), Cfg::SMEM_BYTES, st, ta, tb, ea, eb,
-                    (double*)C, n, 2 * N, n_pad, b_pad, KB, 2LL * N);
+  // grid padded to whole clusters: padding CTAs read padding rows (n_pad, b_pad are multiples of 256) and
+  // store nothing
+  dim3 grid(round_up((n + Cfg::BM - 1) / Cfg::BM, CM), round_up((2 * N + Cfg::BN - 1) / Cfg::BN, CN));
+  const int KB = ld / Cfg::BK;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(Cfg::THREADS);
+  cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (CM * CN > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = CM;
+    attr[na].val.clusterDim.y = CN;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  return cudaLaunchKernelEx(&cfg, ozaki_gemm_kernel<Cfg>, a_planes, b_planes, ea, eb, (double*)C, n, 2 * N, KB,
+                            2LL * N);
+}
+
+// diagonal-split kernel: clusters of MP CTA pairs, 128 x 128 tiles (ozaki_gemm.cuh)
+template <int S, int MP>
+static cudaError_t launch_ozaki2(const int8_t* a_planes, int n_pad, const int* ea, const int8_t* b_planes, int b_pad,
+                                 const int* eb, int ld, double2* C, int n, int K, int N, cudaStream_t st) {
+  using Cfg = Oz2Cfg<S, MP>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(ozaki2_gemm_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Cfg::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const int mtiles = round_up((n + Cfg::BM - 1) / Cfg::BM, MP);
+  dim3 grid(2 * mtiles, (2 * N + Cfg::BN - 1) / Cfg::BN);
+  const int KB = ld / Cfg::BK;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(Cfg::THREADS);
+  cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = Cfg::CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, ozaki2_gemm_kernel<Cfg>, a_planes, b_planes, ea, eb, (double*)C, n, 2 * N, KB,
+                            2LL * N);
+}
+
+static bool ozaki_v1() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MPS_OZ_KERNEL");
+    v = (e && strcmp(e, "v1") == 0) ? 1 : 0;
+  }
+  return v == 1;
+}
+
+// K1 emulated on INT8: the diagonal-split pair kernel (default) or, with MPS_OZ_KERNEL=v1, the
+// single-CTA 128 x 64 kernel that keeps all S diagonals (2/3 of the MMA rate, kept for comparison)
+template <int S>
+static cudaError_t launch_ozaki_s(const int8_t* a_planes, int n_pad, const int* ea, const int8_t* b_planes, int b_pad,
+                                  const int* eb, int ld, double2* C, int n, int K, int N, cudaStream_t st) {
+  if (ozaki_v1()) return launch_ozaki_cl<S, 1, 1>(a_planes, n_pad, ea, b_planes, b_pad, eb, ld, C, n, K, N, st);
+  return launch_ozaki2<S, 1>(a_planes, n_pad, ea, b_planes, b_pad, eb, ld, C, n, K, N, st);
 }
 
 static cudaError_t launch_ozaki(int S, const int8_t* a_planes, int n_pad, const int* ea, const int8_t* b_planes,
@@ -548,7 +593,7 @@ static cudaError_t launch_ozaki(int S, const int8_t* a_planes, int n_pad, const 
 // digit planes of a state (n x K complex128): S planes of n_pad x ld bytes + n exponents
 static cudaError_t ozaki_slice_state(const double2* V, int n, int K, int S, int8_t* planes, int n_pad, int ld, int* e,
                                      cudaStream_t st) {
-  ozaki_slice_rows_kernel<<<n, 128, 0, st>>>(V, K, S, planes, (long long)n_pad * ld, ld, e);
+  ozaki_slice_rows_kernel<<<n, 128, 0, st>>>(V, K, S, planes, ld, e);
   return cudaGetLastError();
 }
 
@@ -560,12 +605,12 @@ static cudaError_t ozaki_prepare_site(Site& s, int D, int S) {
   s.oz = nullptr;
   s.oz_e = nullptr;
   const int N = s.chi_r * D;
-  s.oz_ld = round_up(2 * s.chi_l, 16);
-  s.oz_pad = round_up(2 * N, 64);
+  s.oz_ld = oz_ld(s.chi_l);
+  s.oz_pad = round_up(2 * N, 256);
   cudaError_t e = cudaMalloc(&s.oz, (size_t)S * s.oz_pad * s.oz_ld);
   if (e == cudaSuccess) e = cudaMalloc(&s.oz_e, (size_t)2 * N * sizeof(int));
   if (e != cudaSuccess) return e;
-  ozaki_slice_site_kernel<<<2 * N, 128>>>(s.data, s.chi_l, N, S, s.oz, (long long)s.oz_pad * s.oz_ld, s.oz_ld, s.oz_e);
+  ozaki_slice_site_kernel<<<2 * N, 128>>>(s.data, s.chi_l, N, S, s.oz, s.oz_ld, s.oz_e);
   e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   s.oz_S = S;
@@ -905,7 +950,7 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
     CU(c, c->lv1[l].ensure(nl * chi_max), "alloc state");
     CU(c, c->lcbuf[l].ensure(nl * cmax), "alloc C buffer");
     if (c->gemm_mode == 8) {
-      CU(c, c->loz[l].ensure((size_t)c->oz_S * round_up((int)nl, 128) * round_up(2 * chi_max, 16)), "alloc digits");
+      CU(c, c->loz[l].ensure((size_t)c->oz_S * round_up((int)nl, 256) * oz_ld(chi_max)), "alloc digits");
       CU(c, c->loz_e[l].ensure(nl), "alloc digit exponents");
     }
     if (c->sum_planes && c->gemm_mode == 3) {
@@ -916,8 +961,12 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
   const bool use_sums = !c64 && c->sum_planes && c->gemm_mode == 3;
   const bool ozaki = !c64 && c->gemm_mode == 8;
   if (ozaki) {
-    for (int m = m_begin; m < m_end; ++m)
+    for (int m = m_begin; m < m_end; ++m) {
       if (c->sites[m].host) return fail(c, MPS_ERR_VALIDATION, "host-streamed sites do not support gemm mode 8");
+      if (c->sites[m].chi_l > OZ_MAX_K)
+        return fail(c, MPS_ERR_VALIDATION, "gemm mode 8 supports chi_l <= %d (int32 diagonal sums); site %d has %d",
+                    OZ_MAX_K, m, c->sites[m].chi_l);
+    }
     for (int m = m_begin; m < m_end; ++m) CU(c, ozaki_prepare_site(c->sites[m], D, c->oz_S), "Ozaki site digits");
   }
 
@@ -1101,7 +1150,7 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
         c->launches++;
         if (e != cudaSuccess) return cuda_fail(c, e, "c64 site_gemm launch");
       } else if (ozaki) {
-        const int n_pad = round_up(nl, 128);
+        const int n_pad = round_up(nl, 256);
         CU(c, ozaki_slice_state(v_in[l], nl, s.chi_l, c->oz_S, c->loz[l].p, n_pad, s.oz_ld, c->loz_e[l].p, lst[l]),
            "Ozaki state digits");
         cudaError_t e = launch_ozaki(c->oz_S, c->loz[l].p, n_pad, c->loz_e[l].p, s.oz, s.oz_pad, s.oz_e, s.oz_ld,
@@ -1339,9 +1388,9 @@ int mps_site_gemm(const void* V, const void* G, void* C, int n, int K, int N, in
 }
 
 int mps_site_gemm_ozaki(const void* V, const void* G, void* C, int n, int K, int N, int S, uint64_t stream) {
-  if (!V || !G || !C || n < 1 || K < 1 || N < 1 || S < 5 || S > 7) return MPS_ERR_VALIDATION;
+  if (!V || !G || !C || n < 1 || K < 1 || K > OZ_MAX_K || N < 1 || S < 5 || S > 7) return MPS_ERR_VALIDATION;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const int ld = round_up(2 * K, 16), n_pad = round_up(n, 128), b_pad = round_up(2 * N, 64);
+  const int ld = oz_ld(K), n_pad = round_up(n, 256), b_pad = round_up(2 * N, 256);
   int8_t *ap = nullptr, *bp = nullptr;
   int *ea = nullptr, *eb = nullptr;
   if (cudaMallocAsync(&ap, (size_t)S * n_pad * ld, st) != cudaSuccess ||
@@ -1351,8 +1400,8 @@ int mps_site_gemm_ozaki(const void* V, const void* G, void* C, int n, int K, int
     cudaGetLastError();
     return MPS_ERR_RESOURCE;
   }
-  ozaki_slice_rows_kernel<<<n, 128, 0, st>>>((const double2*)V, K, S, ap, (long long)n_pad * ld, ld, ea);
-  ozaki_slice_site_kernel<<<2 * N, 128, 0, st>>>((const double2*)G, K, N, S, bp, (long long)b_pad * ld, ld, eb);
+  ozaki_slice_rows_kernel<<<n, 128, 0, st>>>((const double2*)V, K, S, ap, ld, ea);
+  ozaki_slice_site_kernel<<<2 * N, 128, 0, st>>>((const double2*)G, K, N, S, bp, ld, eb);
   cudaError_t e = launch_ozaki(S, ap, n_pad, ea, bp, b_pad, eb, ld, (double2*)C, n, K, N, st);
   cudaFreeAsync(ap, st);
   cudaFreeAsync(bp, st);
@@ -1367,7 +1416,7 @@ int mps_site_gemm_ozaki(const void* V, const void* G, void* C, int n, int K, int
 
 int mps_ozaki_state_planes(const void* V, int n, int K, int S, int8_t* planes, int* e, int ld, int n_pad,
                            uint64_t stream) {
-  if (!V || !planes || !e || n < 1 || K < 1 || S < 5 || S > 7 || ld < 2 * K || ld % 16 || n_pad < n)
+  if (!V || !planes || !e || n < 1 || K < 1 || S < 5 || S > 7 || ld < 2 * K || ld % 32 || n_pad < n || n_pad % 256)
     return MPS_ERR_VALIDATION;
   return ozaki_slice_state((const double2*)V, n, K, S, planes, n_pad, ld, e, reinterpret_cast<cudaStream_t>(stream)) ==
                  cudaSuccess
@@ -1377,16 +1426,19 @@ int mps_ozaki_state_planes(const void* V, int n, int K, int S, int8_t* planes, i
 
 int mps_ozaki_site_planes(const void* G, int K, int N, int S, int8_t* planes, int* e, int ld, int b_pad,
                           uint64_t stream) {
-  if (!G || !planes || !e || K < 1 || N < 1 || S < 5 || S > 7 || ld < 2 * K || ld % 16 || b_pad < 2 * N)
+  if (!G || !planes || !e || K < 1 || N < 1 || S < 5 || S > 7 || ld < 2 * K || ld % 32 || b_pad < 2 * N ||
+      b_pad % 256)
     return MPS_ERR_VALIDATION;
-  ozaki_slice_site_kernel<<<2 * N, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      (const double2*)G, K, N, S, planes, (long long)b_pad * ld, ld, e);
+  ozaki_slice_site_kernel<<<2 * N, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>((const double2*)G, K, N, S, planes,
+                                                                                     ld, e);
   return cudaGetLastError() == cudaSuccess ? MPS_OK : MPS_ERR_GENERIC;
 }
 
 int mps_ozaki_gemm_planes(const int8_t* a_planes, int n_pad, const int* ea, const int8_t* b_planes, int b_pad,
                           const int* eb, int ld, void* C, int n, int K, int N, int S, uint64_t stream) {
-  if (!a_planes || !b_planes || !ea || !eb || !C || n < 1 || K < 1 || N < 1 || S < 5 || S > 7) return MPS_ERR_VALIDATION;
+  if (!a_planes || !b_planes || !ea || !eb || !C || n < 1 || K < 1 || K > OZ_MAX_K || N < 1 || S < 5 || S > 7 || ld < 2 * K ||
+      ld % 32 || n_pad < n || n_pad % 256 || b_pad < 2 * N || b_pad % 256)
+    return MPS_ERR_VALIDATION;
   return launch_ozaki(S, a_planes, n_pad, ea, b_planes, b_pad, eb, ld, (double2*)C, n, K, N,
                       reinterpret_cast<cudaStream_t>(stream)) == cudaSuccess
              ? MPS_OK

@@ -549,6 +549,15 @@ def test_site_gemm_ozaki_vs_torch(n, K, N, S):
     assert err <= (2e-13 if S == 7 else 3e-11) * scale, (err, scale)
 
 
+def test_ozaki_refuses_int32_overflow_shapes():
+    """7 x (2 chi_l) x 127^2 must stay below 2^31 in a diagonal accumulator: chi_l > 9400 is refused."""
+    L = _native.lib()
+    V = torch.zeros(1, 9401, dtype=torch.complex128, device="cuda")
+    G = torch.zeros(9401, 1, dtype=torch.complex128, device="cuda")
+    C = torch.zeros(1, 1, dtype=torch.complex128, device="cuda")
+    assert L.mps_site_gemm_ozaki(V.data_ptr(), G.data_ptr(), C.data_ptr(), 1, 9401, 1, 7, 0) == 2
+
+
 def test_chain_parity_ozaki(c2_sites):
     N, M = 400, 16
     cfg = MpsSamplerConfig(N=N, seed=13, alpha_sigma=0.5, batch_size=200)

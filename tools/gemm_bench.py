@@ -52,7 +52,7 @@ for name in sys.argv[1:] or list(SHAPES):
     # complex128 emulated on INT8 tcgen05 (Ozaki): site digits prepared once (as in the chain),
     # state digits + GEMM timed
     for S in (7, 6):
-        ld, n_pad, b_pad = (2 * K + 15) // 16 * 16, (n + 127) // 128 * 128, (2 * N + 63) // 64 * 64
+        ld, n_pad, b_pad = (2 * K + 31) // 32 * 32, (n + 255) // 256 * 256, (2 * N + 255) // 256 * 256
         ap = torch.empty(S * n_pad * ld, dtype=torch.int8, device="cuda")
         bp = torch.empty(S * b_pad * ld, dtype=torch.int8, device="cuda")
         ea = torch.empty(n, dtype=torch.int32, device="cuda")
