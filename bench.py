@@ -674,6 +674,48 @@ def main():
     e2e = world * K * n / (ms_e2e / 1e3)
 
     ok = bool((counts[W:] >= 0).all().item()) and not bool((status[W:] & 1).any().item())
+
+    # Same run, same inputs, K1 emulated on the INT8 tensor cores (gemm mode 8, Ozaki, ~1e-13):
+    # reported next to the FP64-DMMA headline (the path the north star names) as "alt_gemm".
+    alt = None
+    if args.dtype == "c128" and args.gemm != "ozaki" and not args.stream_sites and max(dims) <= 9400:
+        eng.set_gemm_mode(8)
+        for s in range(W):
+            step(s)
+        barrier()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for s in range(W, W + K):
+            step(s)
+        a1.record(stream)
+        barrier()
+        ms_alt = a0.elapsed_time(a1)
+        if world > 1:
+            t = torch.tensor([ms_alt], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_alt = float(t.item())
+        ok_alt = not bool((status[W:] & 1).any().item())
+        eng.set_lanes(1)
+        step(0)
+        barrier()
+        eng.profile(1)
+        for s in range(W, W + min(K, 3)):
+            step(s)
+        barrier()
+        pa = eng.profile_read()
+        eng.profile(0)
+        eng.set_lanes(args.lanes)
+        eng.set_gemm_mode({"3m": 3, "4m": 4}[args.gemm])
+        k1_ms = pa["gemm_ms"] / max(pa["gemm_launches"], 1)
+        k1_tf = (pa["gemm_flops"] / max(pa["gemm_launches"], 1)) / (k1_ms / 1e3) / 1e12 if k1_ms > 0 else 0.0
+        i8_peak = 4510.5  # TOP/s: profiles/r01_umma_probe.jsonl, kind::i8 M=128 N=128 issue-rate probe
+        alt = {"gemm": "ozaki_gemm (complex128 K1 emulated on INT8 tcgen05: 7 digits of 7 bits, "
+                       "~1e-13 of the row scales; mps_set_gemm_mode 8)",
+               "value": world * K * n / (ms_alt / 1e3), "unit": "samples/s", "ms_per_step": ms_alt / K,
+               "valid_outputs": ok_alt,
+               "k1": {"ms_per_launch": k1_ms, "algorithmic_tflops": k1_tf, "vs_fp64_dmma_peak": k1_tf / fp64_peak()[0],
+                      "executed_int8_tops": 28.0 * k1_tf, "int8_frac": 28.0 * k1_tf / i8_peak,
+                      "int8_peak_source": "profiles/r01_umma_probe.jsonl (kind::i8 N=128, 4510 TOP/s)"}}
     peak, peak_src = fp64_peak()
     traffic, traffic_note = ncu_traffic(args.config, n)
     if args.dtype == "c64":
@@ -722,6 +764,8 @@ def main():
         "valid_outputs": ok,
         "setup_s": setup_s,
     }
+    if alt is not None:
+        line["alt_gemm"] = alt
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, cores, sample = CpuBaseline(args.config).run()
         line["cpu_baseline"] = {"value": v, "unit": "samples/s", "cores": cores, "kind": "port", "sample": sample}

@@ -342,19 +342,47 @@ __global__ void __launch_bounds__(DRAW_THREADS, C64 ? 8 : 4)
     const int j = cidx * DRAW_THREADS + tid;
     const ElemT* src = RING ? ring_slot(cidx) + tid * D : Crow + (long long)j * D;
     if (j < A.chi_r) {
-      ElemT c[DR];
+      bool done = false;
+      if constexpr (!C64 && DT > 0) {
+        if (!ident) {
+          // d-outer / k-inner: the D complex FMA chains E[k] = sum_d T[k][d] c[d] advance together
+          // (same per-k operation order as disp_row, so the same bits), hiding the DFMA latency
+          // that the k-outer form exposes as one 2D-long dependent chain at a time
+          double2 e[DR];
 #pragma unroll
-      for (int d = 0; d < DR; ++d)
-        if (DT || d < D) c[d] = src[d];
+          for (int k = 0; k < DR; ++k) e[k] = make_double2(0.0, 0.0);
 #pragma unroll
-      for (int k = 0; k < DR; ++k) {
-        if (!DT && k >= D) break;
-        if constexpr (C64) {
-          const float2 e = ident ? c[k] : disp_row_f<DT>(Tf, D, k, c);
-          acc[k] = fmaf(e.x, e.x, fmaf(e.y, e.y, acc[k]));
-        } else {
-          const double2 e = ident ? c[k] : disp_row<DT>(T, D, k, c);
-          acc[k] = fma(e.x, e.x, fma(e.y, e.y, acc[k]));
+          for (int d = 0; d < DR; ++d) {
+            const double2 cd = src[d];
+#pragma unroll
+            for (int k = 0; k < DR; ++k) {
+              const double2 tk = lds_c128(&T[k * D + d]);
+              e[k].x = fma(tk.x, cd.x, e[k].x);
+              e[k].x = fma(-tk.y, cd.y, e[k].x);
+              e[k].y = fma(tk.x, cd.y, e[k].y);
+              e[k].y = fma(tk.y, cd.x, e[k].y);
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < DR; ++k) acc[k] = fma(e[k].x, e[k].x, fma(e[k].y, e[k].y, acc[k]));
+          done = true;
+        }
+      }
+      if (!done) {
+        ElemT c[DR];
+#pragma unroll
+        for (int d = 0; d < DR; ++d)
+          if (DT || d < D) c[d] = src[d];
+#pragma unroll
+        for (int k = 0; k < DR; ++k) {
+          if (!DT && k >= D) break;
+          if constexpr (C64) {
+            const float2 e = ident ? c[k] : disp_row_f<DT>(Tf, D, k, c);
+            acc[k] = fmaf(e.x, e.x, fmaf(e.y, e.y, acc[k]));
+          } else {
+            const double2 e = ident ? c[k] : disp_row<DT>(T, D, k, c);
+            acc[k] = fma(e.x, e.x, fma(e.y, e.y, acc[k]));
+          }
         }
       }
     }
