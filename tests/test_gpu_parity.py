@@ -549,6 +549,34 @@ def test_site_gemm_ozaki_vs_torch(n, K, N, S):
     assert err <= (2e-13 if S == 7 else 3e-11) * scale, (err, scale)
 
 
+def test_ozaki_stage_split_and_ragged_lanes(c2_sites):
+    """INT8 K1 (mode 8) through a stage hand-off (state_in digit slicing) with an odd batch split
+    into ragged lanes (padding rows of the 256-row digit tiles) reproduces the single-context
+    mode-8 chain bit-for-bit, and stays within the parity bar of the oracle."""
+    N, M, cut = 301, 16, 6
+    mps = MPS(c2_sites)
+    cfg = MpsSamplerConfig(N=N, seed=21, alpha_sigma=0.5, batch_size=N)
+    with MpsSampler(mps) as eng:
+        eng.set_gemm_mode(8)
+        eng.set_lanes(1)
+        full = eng.sample(cfg, return_marginals=True)
+    _check_parity(c2_sites, full, stream_uniforms(21, 0, N, M), alpha=alpha_stream(21, 0, N, M, 0.5))
+    counts = torch.empty((N, M), dtype=torch.int32, device="cuda")
+    marg = torch.empty((N, M, 10), dtype=torch.float64, device="cuda")
+    status = torch.zeros(N, dtype=torch.uint8, device="cuda")
+    state = torch.empty((N, mps.bond_dims[cut]), dtype=torch.complex128, device="cuda")
+    with MpsSampler(mps, sites_range=(0, cut)) as s0, MpsSampler(mps, sites_range=(cut, M)) as s1:
+        for e, lanes in ((s0, 3), (s1, 2)):
+            e.set_gemm_mode(8)
+            e.set_lanes(lanes)
+            e.set_streams(21, 0.5)
+        s0.run(0, N, counts, state_out=state, marginals=marg, status=status)
+        s1.run(0, N, counts, state_in=state, marginals=marg, status=status)
+    torch.cuda.synchronize()
+    assert np.array_equal(counts.cpu().numpy(), full["counts"])
+    assert np.array_equal(marg.cpu().numpy(), full["marginals"])
+
+
 def test_ozaki_refuses_int32_overflow_shapes():
     """7 x (2 chi_l) x 127^2 must stay below 2^31 in a diagonal accumulator: chi_l > 9400 is refused."""
     L = _native.lib()
