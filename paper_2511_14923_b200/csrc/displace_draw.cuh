@@ -319,9 +319,10 @@ __global__ void __launch_bounds__(DRAW_THREADS, C64 ? 8 : 4)
   }
   griddep_wait();  // the GEMM (and transitively the previous draw) is complete: C, status valid
   const bool dead = (A.status[b] & ST_FAILED) != 0;
-  if (RING && tid == 0 && !dead) {  // uses 0 and 1 (with one chunk, use 1 is pass 2's chunk 0)
+  // with one chunk the row stays in slot 0 for pass 2 (no re-load); else loads 0 and 1 go out now
+  if (RING && tid == 0 && !dead) {
     ring_issue(0);
-    ring_issue(1);
+    if (nchunks > 1) ring_issue(1);
   }
   __syncthreads();
 
@@ -386,7 +387,7 @@ __global__ void __launch_bounds__(DRAW_THREADS, C64 ? 8 : 4)
         }
       }
     }
-    if (RING) {
+    if (RING && nchunks > 1) {
       __syncthreads();  // every thread is done with this slot
       if (tid == 0 && cidx + 2 < 2 * nchunks) ring_issue(cidx + 2);  // pass 1's next chunk, or pass 2's first
     }
@@ -448,7 +449,9 @@ __global__ void __launch_bounds__(DRAW_THREADS, C64 ? 8 : 4)
   // ---- pass 2: gather + renormalise ----
   for (int cidx = 0; cidx < nchunks; ++cidx) {
     const int j = cidx * DRAW_THREADS + tid;
-    const ElemT* src = RING ? ring_slot(nchunks + cidx) + tid * D : Crow + (long long)j * D;
+    const ElemT* src = !RING           ? Crow + (long long)j * D
+                       : (nchunks > 1) ? ring_slot(nchunks + cidx) + tid * D
+                                       : reinterpret_cast<const ElemT*>(ring_smem) + tid * D;  // slot 0, still resident
     if (j < A.chi_r) {
       if (ks < 0) {
         store_state<C64>(A, b, j, make_double2(0.0, 0.0));
@@ -485,7 +488,7 @@ __global__ void __launch_bounds__(DRAW_THREADS, C64 ? 8 : 4)
         store_state<false>(A, b, j, make_double2(e.x * scale, e.y * scale));
       }
     }
-    if (RING) {
+    if (RING && nchunks > 1) {
       __syncthreads();
       if (tid == 0 && nchunks + cidx + 2 < 2 * nchunks) ring_issue(nchunks + cidx + 2);
     }

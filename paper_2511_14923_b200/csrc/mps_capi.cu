@@ -275,6 +275,10 @@ static bool pdl_enabled() {
   return v == 1;
 }
 
+// set while the autotuner times back-to-back launches: each must wait for its predecessor, as a
+// GEMM does in the chain, so latency-bound shapes are ranked by latency, not by PDL overlap
+static thread_local bool t_no_pdl = false;
+
 template <typename... KArgs, typename... Args>
 static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                               Args&&... args) {
@@ -287,7 +291,7 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = (pdl_enabled() && !t_no_pdl) ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
@@ -385,6 +389,11 @@ using G32x128 = GemmCfgT<32, 128, 1, 4, 4, 2>;
 using G64x80 = GemmCfgT<64, 80, 4, 1, 4, 3>;    // 40 complex columns: whole D=10 groups, 4000 tiles at C3
 using G64x64w8 = GemmCfgT<64, 64, 4, 2, 4, 2>;  // 3M: 8 warps of 16 x 16 complex, 16 warps/SM
 using G32x64w4 = GemmCfgT<32, 64, 2, 2, 4, 4>;  // 3M: 4 warps of 16 x 16 complex
+// deep rings for short K (chi_l ~ 100: 13 k-stages): most of K in flight at once, so a small-chi
+// GEMM costs ~one TMA round trip instead of one per ring refill (latency, not throughput, bound)
+using G16x32d8 = GemmCfgT<16, 32, 1, 1, 8, 4>;
+using G16x32d16 = GemmCfgT<16, 32, 1, 1, 16, 2>;
+using G32x64d8 = GemmCfgT<32, 64, 2, 2, 8, 2>;
 static const GemmCfgInfo kGemm4[] = {
     cfg_info<G128x128, 4>("4m_128x128_w4x2"), cfg_info<G64x128, 4>("4m_64x128_w2x4"),
     cfg_info<G64x128p, 4>("4m_64x128_w2x2_occ2"), cfg_info<G32x64, 4>("4m_32x64_w1x2_occ4"),
@@ -394,7 +403,8 @@ static const GemmCfgInfo kGemm3[] = {
     cfg_info<G64x64, 3>("3m_64x64_w2x2_occ3"), cfg_info<G32x64, 3>("3m_32x64_w1x2_occ4"),
     cfg_info<G16x32, 3>("3m_16x32_w1x1_occ8"), cfg_info<G32x128, 3>("3m_32x128_w1x4_occ2"),
     cfg_info<G64x80, 3>("3m_64x80_w4x1_occ3"), cfg_info<G64x64w8, 3>("3m_64x64_w4x2_occ2"),
-    cfg_info<G32x64w4, 3>("3m_32x64_w2x2_occ4")};
+    cfg_info<G32x64w4, 3>("3m_32x64_w2x2_occ4"), cfg_info<G16x32d8, 3>("3m_16x32_w1x1_s8_occ4"),
+    cfg_info<G16x32d16, 3>("3m_16x32_w1x1_s16_occ2"), cfg_info<G32x64d8, 3>("3m_32x64_w2x2_s8_occ2")};
 constexpr int N_GEMM4 = sizeof(kGemm4) / sizeof(kGemm4[0]);
 constexpr int N_GEMM3 = sizeof(kGemm3) / sizeof(kGemm3[0]);
 constexpr int N_GEMM_CFGS = N_GEMM3 > N_GEMM4 ? N_GEMM3 : N_GEMM4;  // index bound for the API
@@ -436,9 +446,11 @@ static int tune_gemm(int mode, const GemmOps& o, cudaStream_t st) {
   }
   int best = 0;
   {
-    // one timed run per candidate when a GEMM is long (> ~20 ms), else the best of two
+    // one timed run per candidate when a GEMM is long (> ~20 ms), the best of two when it is
+    // ms-scale, the best of eight when it is us-scale (latency-bound shapes time noisily)
     const double est_ms = 8.0 * o.n * (double)o.K * o.N / 37e9;
-    const int reps = est_ms > 20.0 ? 1 : 2;
+    const int reps = est_ms > 20.0 ? 1 : est_ms > 0.5 ? 2 : 4;
+    const int inner = est_ms > 0.5 ? 1 : 16;  // us-scale: time 16 back-to-back launches per event pair
     float best_ms = 1e30f;
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
@@ -447,12 +459,16 @@ static int tune_gemm(int mode, const GemmOps& o, cudaStream_t st) {
       float ms_min = 1e30f;
       for (int r = 0; r < reps; ++r) {
         cudaEventRecord(e0, st);
-        if (cfg_of(mode, cfg).fn(o, st) != cudaSuccess) break;
+        bool ok = true;
+        t_no_pdl = true;
+        for (int i = 0; i < inner && ok; ++i) ok = cfg_of(mode, cfg).fn(o, st) == cudaSuccess;
+        t_no_pdl = false;
+        if (!ok) break;
         cudaEventRecord(e1, st);
         cudaEventSynchronize(e1);
         float ms = 0.f;
         cudaEventElapsedTime(&ms, e0, e1);
-        ms_min = std::min(ms_min, ms);
+        ms_min = std::min(ms_min, ms / inner);
       }
       if (ms_min < best_ms * 0.995f) {
         best_ms = ms_min;

@@ -308,7 +308,7 @@ def test_staged_and_global_draw_agree():
     _check_parity(sites, res, stream_uniforms(2, 0, N, M), alpha=alpha_stream(2, 0, N, M, 0.5))
 
 
-@pytest.mark.parametrize("mode,cfg_id", [(m, c) for m in (3, 4) for c in range(-2, 9 if m == 3 else 6)])
+@pytest.mark.parametrize("mode,cfg_id", [(m, c) for m in (3, 4) for c in range(-2, 12 if m == 3 else 6)])
 def test_gemm_configs_bit_identical(cfg_id, mode):
     """Within a product mode every tile config (and the autotuner's pick) gives the same bits."""
     L = _native.lib()
