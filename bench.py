@@ -47,7 +47,7 @@ CONFIGS = {
            "BASELINE configs[4]: M=64 chi=10000 D=10 n=4096 alpha~CN(0,0.5), mode-pipelined"),
 }
 HBM_USABLE = 170e9  # bytes per B200 we plan to fill with sites + workspaces
-LANES = 2  # concurrent row-block chains per micro-batch (mps_set_lanes)
+LANES = {"3m": 2, "4m": 2, "ozaki": 1}  # concurrent row-block chains per micro-batch (mps_set_lanes), per K1
 METRIC = "MPS samples/sec (chi,D,M stated) at 1/2/4/8 B200; % of FP64 tensor-core peak"
 
 
@@ -481,7 +481,8 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--lanes", type=int, default=LANES, help="concurrent row-block chains per micro-batch")
+    ap.add_argument("--lanes", type=int, default=0,
+                    help="concurrent row-block chains per micro-batch (default: 2 for the DMMA K1, 1 for INT8)")
     ap.add_argument("--stream-sites", action="store_true",
                     help="keep the sites in pinned host memory and stream them into HBM every step")
     ap.add_argument("--gemm", default="3m", choices=["3m", "4m", "ozaki"],
@@ -497,6 +498,7 @@ def main():
                     help="pipeline micro-batch size for --stage-of runs (default: the config's batch n); "
                          "per-sample results do not depend on it")
     args = ap.parse_args()
+    args.lanes = args.lanes or LANES[args.gemm]
     W = max(args.warmup, 3)
     K = args.steps
     rank = int(os.environ.get("RANK", "0"))
@@ -680,6 +682,7 @@ def main():
     alt = None
     if args.dtype == "c128" and args.gemm != "ozaki" and not args.stream_sites and max(dims) <= 9400:
         eng.set_gemm_mode(8)
+        eng.set_lanes(LANES["ozaki"])
         for s in range(W):
             step(s)
         barrier()
@@ -712,6 +715,7 @@ def main():
         alt = {"gemm": "ozaki_gemm (complex128 K1 emulated on INT8 tcgen05: 7 digits of 7 bits, "
                        "~1e-13 of the row scales; mps_set_gemm_mode 8)",
                "value": world * K * n / (ms_alt / 1e3), "unit": "samples/s", "ms_per_step": ms_alt / K,
+               "lanes": LANES["ozaki"],
                "valid_outputs": ok_alt,
                "k1": {"ms_per_launch": k1_ms, "algorithmic_tflops": k1_tf, "vs_fp64_dmma_peak": k1_tf / fp64_peak()[0],
                       "executed_int8_tops": 28.0 * k1_tf, "int8_frac": 28.0 * k1_tf / i8_peak,
