@@ -388,7 +388,9 @@ using G64x64 = GemmCfgT<64, 64, 2, 2, 4, 3>;
 using G32x128 = GemmCfgT<32, 128, 1, 4, 4, 2>;
 using G64x80 = GemmCfgT<64, 80, 4, 1, 4, 3>;    // 40 complex columns: whole D=10 groups, 4000 tiles at C3
 using G64x64w8 = GemmCfgT<64, 64, 4, 2, 4, 2>;  // 3M: 8 warps of 16 x 16 complex, 16 warps/SM
-using G32x64w4 = GemmCfgT<32, 64, 2, 2, 4, 4>;  // 3M: 4 warps of 16 x 16 complex
+// (a 32x64 tile with 2 x 2 warps of 16 x 16 complex, 4 CTAs/SM, was dropped: with the state sum planes
+//  and two concurrent lanes it intermittently produced wrong values in the upper 16 rows of a tile,
+//  ~5% of fresh-shape calls, tools/tune_race_probe.py; every other config ran 720 calls clean)
 // deep rings for short K (chi_l ~ 100: 13 k-stages): most of K in flight at once, so a small-chi
 // GEMM costs ~one TMA round trip instead of one per ring refill (latency, not throughput, bound)
 using G16x32d8 = GemmCfgT<16, 32, 1, 1, 8, 4>;
@@ -403,7 +405,7 @@ static const GemmCfgInfo kGemm3[] = {
     cfg_info<G64x64, 3>("3m_64x64_w2x2_occ3"), cfg_info<G32x64, 3>("3m_32x64_w1x2_occ4"),
     cfg_info<G16x32, 3>("3m_16x32_w1x1_occ8"), cfg_info<G32x128, 3>("3m_32x128_w1x4_occ2"),
     cfg_info<G64x80, 3>("3m_64x80_w4x1_occ3"), cfg_info<G64x64w8, 3>("3m_64x64_w4x2_occ2"),
-    cfg_info<G32x64w4, 3>("3m_32x64_w2x2_occ4"), cfg_info<G16x32d8, 3>("3m_16x32_w1x1_s8_occ4"),
+    cfg_info<G16x32d8, 3>("3m_16x32_w1x1_s8_occ4"),
     cfg_info<G16x32d16, 3>("3m_16x32_w1x1_s16_occ2"), cfg_info<G32x64d8, 3>("3m_32x64_w2x2_s8_occ2")};
 constexpr int N_GEMM4 = sizeof(kGemm4) / sizeof(kGemm4[0]);
 constexpr int N_GEMM3 = sizeof(kGemm3) / sizeof(kGemm3[0]);
