@@ -49,6 +49,33 @@ CONFIGS = {
 HBM_USABLE = 170e9  # bytes per B200 we plan to fill with sites + workspaces
 LANES = {"3m": 2, "4m": 2, "ozaki": 1}  # concurrent row-block chains per micro-batch (mps_set_lanes), per K1
 METRIC = "MPS samples/sec (chi,D,M stated) at 1/2/4/8 B200; % of FP64 tensor-core peak"
+# Multi-rank plumbing: NCCL, one GPU per rank.  MPS_BENCH_BACKEND=gloo + MPS_BENCH_ONE_GPU=1 run the
+# same N>1 code path with every rank on cuda:0 (a plumbing check on a one-GPU box: ranks never wait
+# on each other inside kernels in the sample-sharded layout; its timings mean nothing).
+BACKEND = os.environ.get("MPS_BENCH_BACKEND", "nccl")
+ONE_GPU = os.environ.get("MPS_BENCH_ONE_GPU") == "1"
+
+
+def dist_barrier(local):
+    import torch.distributed as dist
+
+    if dist.is_initialized() and dist.get_world_size() > 1:
+        if BACKEND == "nccl":
+            dist.barrier(device_ids=[local])
+        else:
+            dist.barrier()
+
+
+def dist_max(x, dev):
+    """Max over ranks of a host float (device tensor for NCCL, host tensor for gloo)."""
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_initialized() and dist.get_world_size() > 1):
+        return x
+    t = torch.tensor([x], device=dev if BACKEND == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
 
 
 def fp64_peak():
@@ -268,16 +295,11 @@ def run_pipelined(args, rank, world, local, W, K, config, dims):
                      rank=rank, world=world)
 
     def barrier():
-        if world > 1:
-            dist.barrier(device_ids=[local])
+        dist_barrier(local)
         torch.cuda.synchronize()
 
     def max_ms(ms):
-        if world > 1:
-            t = torch.tensor([ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
-        return ms
+        return dist_max(ms, dev)
 
     pipe(0, W)
     barrier()
@@ -503,7 +525,7 @@ def main():
     K = args.steps
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if ONE_GPU else int(os.environ.get("LOCAL_RANK", "0"))
     M, chi, D, n, sigma, N_total, desc = CONFIGS[args.config]
     from paper_2511_14923_b200.mps import bond_dims
 
@@ -551,7 +573,10 @@ def main():
         print(json.dumps(run_stage(args, local, W, K, config, dims)), flush=True)
         return
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if BACKEND == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(BACKEND)
     if layout == "pipelined":
         if site_bytes / world > HBM_USABLE:
             if rank == 0:
@@ -596,8 +621,7 @@ def main():
                 stream=stream.cuda_stream)
 
     def barrier():
-        if world > 1:
-            dist.barrier(device_ids=[local])
+        dist_barrier(local)
         torch.cuda.synchronize()
 
     for s in range(W):
@@ -640,11 +664,7 @@ def main():
     prof.update({k: v for k, v in prof_draw.items() if k.startswith("draw")})
     eng.profile(0)
     eng.set_lanes(args.lanes)
-    ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = dist_max(e0.elapsed_time(e1), dev)
     value = world * K * n / (ms / 1e3)
 
     # e2e: host (pinned) uniforms + alpha in, counts out, through the same C ABI call
@@ -668,11 +688,7 @@ def main():
         step_e2e(s)
     e3.record(stream)
     barrier()
-    ms_e2e = e2.elapsed_time(e3)
-    if world > 1:
-        t = torch.tensor([ms_e2e], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_e2e = float(t.item())
+    ms_e2e = dist_max(e2.elapsed_time(e3), dev)
     e2e = world * K * n / (ms_e2e / 1e3)
 
     ok = bool((counts[W:] >= 0).all().item()) and not bool((status[W:] & 1).any().item())
@@ -692,11 +708,7 @@ def main():
             step(s)
         a1.record(stream)
         barrier()
-        ms_alt = a0.elapsed_time(a1)
-        if world > 1:
-            t = torch.tensor([ms_alt], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms_alt = float(t.item())
+        ms_alt = dist_max(a0.elapsed_time(a1), dev)
         ok_alt = not bool((status[W:] & 1).any().item())
         eng.set_lanes(1)
         step(0)

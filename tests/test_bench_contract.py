@@ -1,10 +1,12 @@
-"""bench.py's driver contract on the CPU: the reference arm prints one JSON line with the
-required keys (the GPU arm is exercised on the B200 by the driver and tools/)."""
+"""bench.py's driver contract: the reference arm's JSON line on the CPU, the GPU arm's line and
+its N>1 sample-sharded code path on a B200 (pytest -m gpu)."""
 
 import json
 import subprocess
 import sys
 from pathlib import Path
+
+import pytest
 
 ROOT = Path(__file__).resolve().parents[1]
 
@@ -33,3 +35,31 @@ def test_gpu_arm_fails_loudly_without_gpu():
     out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--config", "c1", "--steps", "1"],
                          capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert out.returncode != 0  # no CPU fallback for the product path
+
+
+@pytest.mark.gpu
+def test_gpu_arm_json_line_and_two_rank_path():
+    """One GPU arm line at N=1 (c2), then the N>1 sample-sharded code path under torchrun with
+    two ranks sharing cuda:0 over gloo (MPS_BENCH_ONE_GPU plumbing mode: keys, max-over-ranks,
+    whole-job value; the timing of that run means nothing)."""
+    import os
+
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--config", "c2", "--steps", "2", "--warmup", "3",
+                          "--no-cpu-baseline"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "e2e", "gpu_launches", "roofline", "clocks", "alt_gemm"):
+        assert k in d, k
+    assert d["n_gpus"] == 1 and d["value"] > 0 and d["gpu_launches"] > 0 and d["valid_outputs"]
+    assert d["roofline"]["bound"] == "tensor" and d["roofline"]["frac"] > 0
+    env = dict(os.environ, MPS_BENCH_BACKEND="gloo", MPS_BENCH_ONE_GPU="1")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", "29547", str(ROOT / "bench.py"), "--gpus", "2",
+                          "--config", "c2", "--steps", "2", "--warmup", "3", "--no-cpu-baseline"],
+                         capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1  # rank 0 only
+    d2 = json.loads(lines[0])
+    assert d2["n_gpus"] == 2 and d2["scaling"] == "weak" and d2["value"] > 0 and d2["valid_outputs"]
