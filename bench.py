@@ -253,7 +253,7 @@ def run_pipelined(args, rank, world, local, W, K, config, dims):
     import torch.distributed as dist
 
     from paper_2511_14923_b200 import MPS, MpsSampler
-    from paper_2511_14923_b200.distributed import run_pipeline, stage_blocks
+    from paper_2511_14923_b200.distributed import P2PHandoff, run_pipeline, run_pipeline_p2p, stage_blocks
 
     M, chi, D, n, sigma, _, desc = CONFIGS[args.config]
     dev = torch.device("cuda", local)
@@ -288,7 +288,22 @@ def run_pipelined(args, rank, world, local, W, K, config, dims):
             return y
         return stage
 
+    hp = None
+    if args.handoff == "p2p" and world > 1:  # fused hand-off: the draw kernel writes into the next GPU
+        host_group = dist.new_group(backend="gloo") if BACKEND == "nccl" else None
+        hp = P2PHandoff(rank, world, n * dims[mb] * (8 if args.dtype == "c64" else 16), host_group=host_group)
+
     def pipe(offset, count, copy_out=False):
+        if hp is not None:
+            def stage_p2p(t, x, out):
+                s_ = offset + t
+                eng.run(s_ * n, n, counts[s_], m_begin=mb, m_end=me, state_in=x, state_out=out, status=status[s_],
+                        stream=stream.cuda_stream)
+                if copy_out:
+                    c_host.copy_(counts[s_, :, mb:me], non_blocking=True)
+
+            run_pipeline_p2p(stage_p2p, count, hp, stream.cuda_stream, rank, world, group=hp.group)
+            return
         run_pipeline(stage_for(offset, copy_out), count,
                      recv_like=lambda: torch.empty((n, dims[mb]), dtype=cdt, device=dev),
                      send_like=lambda: torch.empty((n, dims[me]), dtype=cdt, device=dev),
@@ -351,6 +366,9 @@ def run_pipelined(args, rank, world, local, W, K, config, dims):
     whole_tf = K * step_flops / (ms / 1e3) / 1e12
     ok = not bool((status[W:] & 1).any().item())
     cfg = dict(config, layout="mode-pipelined", stage_blocks=blocks,
+               handoff=("fused peer-memory hand-off: the stage's last draw kernel writes the n x chi state into "
+                        "the next GPU's CUDA-IPC buffer, interprocess events order the stages")
+               if hp is not None else "NCCL send/recv of the n x chi state",
                pipeline=f"{K} micro-batches over {world} stages = {K + world - 1} ticks (fill+drain timed)")
     line = {
         "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": K, "warmup": W,
@@ -369,6 +387,9 @@ def run_pipelined(args, rank, world, local, W, K, config, dims):
                      "whole_chain_tflops": whole_tf, "whole_chain_frac": whole_tf / (world * peak)},
         "clocks": ck, "valid_outputs": ok, "setup_s": setup_s,
     }
+    if hp is not None:
+        dist_barrier(local)
+        hp.close()
     eng.close()
     return line
 
@@ -513,6 +534,8 @@ def main():
                     help="c64: complex64 chain, K1 on tcgen05 (3xTF32), parity 1e-4")
     ap.add_argument("--layout", default="auto", choices=["auto", "sharded", "pipelined"],
                     help="auto: sample-sharded when the MPS fits one GPU, else mode-pipelined")
+    ap.add_argument("--handoff", default="p2p", choices=["p2p", "nccl"],
+                    help="mode-pipelined stage hand-off: fused peer-memory writes (p2p) or NCCL send/recv")
     ap.add_argument("--stage-of", type=int, default=0,
                     help="measure one stage (--stage g) of a G-stage mode pipeline alone on one GPU (c4/c5)")
     ap.add_argument("--stage", type=int, default=0)

@@ -190,6 +190,22 @@ int mps_c64_state_planes(const void* V, int rows, int cols, float* hi, float* lo
 int mps_c64_site_planes(const void* G, int K, int N, float* hi, float* lo, int ld, uint64_t stream);
 int mps_c64_gemm_planes(const float* ahi, const float* alo, const float* bhi, const float* blo, int ld, void* C,
                         int n, int K, int N, uint64_t stream);
+/* Fused stage hand-off over peer memory (mode-pipelined layout; replaces the NCCL send/recv of
+ * the n x chi state).  The receiving stage allocates its input buffers with mps_ipc_alloc and
+ * passes the 64-byte handles to the previous stage's process, which maps them with mps_ipc_open
+ * (NVLink peer memory) and hands the mapped pointer to mps_sample_range as state_out, so its last
+ * draw kernel writes the state into the next GPU directly.  Interprocess events (64-byte
+ * handles) order the two sides on the GPU: mps_event_record after the producer's stage,
+ * mps_stream_wait_event before the consumer's (and the reverse for buffer reuse). */
+int mps_ipc_alloc(uint64_t bytes, void** dptr, void* mem_handle64);
+int mps_ipc_free(void* dptr);
+int mps_ipc_open(const void* mem_handle64, void** dptr);
+int mps_ipc_close(void* dptr);
+int mps_ipc_event_create(void** ev, void* ev_handle64);
+int mps_ipc_event_open(const void* ev_handle64, void** ev);
+int mps_event_record(void* ev, uint64_t stream);
+int mps_stream_wait_event(uint64_t stream, void* ev);
+int mps_event_destroy(void* ev);
 /* D x D truncated displacement matrices for `count` alphas: out[count][D][D] */
 int mps_displacement(const void* alpha, int count, int D, void* out, uint64_t stream);
 /* Uniforms of samples first..first+count-1 (count x M float64), bit-equal to

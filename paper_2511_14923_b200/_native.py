@@ -22,6 +22,8 @@ EXPORTS = (
     "mps_set_sum_planes", "mps_displacement", "mps_stream_uniforms", "mps_site_gemm_c64",
     "mps_c64_state_planes", "mps_c64_site_planes", "mps_c64_gemm_planes", "mps_site_gemm_ozaki",
     "mps_ozaki_state_planes", "mps_ozaki_site_planes", "mps_ozaki_gemm_planes",
+    "mps_ipc_alloc", "mps_ipc_free", "mps_ipc_open", "mps_ipc_close", "mps_ipc_event_create", "mps_ipc_event_open",
+    "mps_event_record", "mps_stream_wait_event", "mps_event_destroy",
 )
 
 MPS_SITE_HOST, MPS_SITE_DEVICE_COPY, MPS_SITE_DEVICE_BORROW, MPS_SITE_HOST_STREAM = 0, 1, 2, 3
@@ -69,6 +71,15 @@ def _declare(L):
     L.mps_set_gemm_config.argtypes = [c_void_p, c_int]
     L.mps_displacement.argtypes = [c_void_p, c_int, c_int, c_void_p, c_uint64]
     L.mps_stream_uniforms.argtypes = [c_uint64, c_int64, c_int, c_int, c_void_p, c_uint64]
+    L.mps_ipc_alloc.argtypes = [c_uint64, ctypes.POINTER(c_void_p), c_void_p]
+    L.mps_ipc_free.argtypes = [c_void_p]
+    L.mps_ipc_open.argtypes = [c_void_p, ctypes.POINTER(c_void_p)]
+    L.mps_ipc_close.argtypes = [c_void_p]
+    L.mps_ipc_event_create.argtypes = [ctypes.POINTER(c_void_p), c_void_p]
+    L.mps_ipc_event_open.argtypes = [c_void_p, ctypes.POINTER(c_void_p)]
+    L.mps_event_record.argtypes = [c_void_p, c_uint64]
+    L.mps_stream_wait_event.argtypes = [c_uint64, c_void_p]
+    L.mps_event_destroy.argtypes = [c_void_p]
     for name in EXPORTS:  # everything else returns an int status (include/mps_sampler.h)
         if name not in ("mps_kernel_launches", "mps_last_error", "mps_destroy"):
             getattr(L, name).restype = c_int

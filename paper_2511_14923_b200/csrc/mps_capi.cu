@@ -1559,6 +1559,80 @@ int mps_displacement(const void* alpha, int count, int D, void* out, uint64_t st
   return cudaGetLastError() == cudaSuccess ? MPS_OK : MPS_ERR_GENERIC;
 }
 
+// ---- fused stage hand-off over peer memory (mode-pipelined layout) ------------------------------
+// The next stage's receive buffers are exported with CUDA IPC and mapped by the previous stage's
+// process (NVLink peer memory); its last draw kernel then writes the n x chi state straight into
+// them (state_out = the mapped pointer), and interprocess events order producer and consumer on
+// the GPU.  No collective runs on the data path.
+int mps_ipc_alloc(uint64_t bytes, void** dptr, void* mem_handle64) {
+  if (!dptr || !mem_handle64 || bytes == 0) return MPS_ERR_VALIDATION;
+  *dptr = nullptr;
+  if (cudaMalloc(dptr, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return MPS_ERR_RESOURCE;
+  }
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, *dptr) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(*dptr);
+    *dptr = nullptr;
+    return MPS_ERR_GENERIC;
+  }
+  memcpy(mem_handle64, &h, sizeof(h));
+  return MPS_OK;
+}
+int mps_ipc_free(void* dptr) { return cudaFree(dptr) == cudaSuccess ? MPS_OK : MPS_ERR_GENERIC; }
+int mps_ipc_open(const void* mem_handle64, void** dptr) {
+  if (!mem_handle64 || !dptr) return MPS_ERR_VALIDATION;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, mem_handle64, sizeof(h));
+  if (cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+    cudaGetLastError();
+    return MPS_ERR_GENERIC;
+  }
+  return MPS_OK;
+}
+int mps_ipc_close(void* dptr) { return cudaIpcCloseMemHandle(dptr) == cudaSuccess ? MPS_OK : MPS_ERR_GENERIC; }
+int mps_ipc_event_create(void** ev, void* ev_handle64) {
+  if (!ev || !ev_handle64) return MPS_ERR_VALIDATION;
+  cudaEvent_t e;
+  if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming | cudaEventInterprocess) != cudaSuccess) {
+    cudaGetLastError();
+    return MPS_ERR_GENERIC;
+  }
+  cudaIpcEventHandle_t h;
+  if (cudaIpcGetEventHandle(&h, e) != cudaSuccess) {
+    cudaGetLastError();
+    cudaEventDestroy(e);
+    return MPS_ERR_GENERIC;
+  }
+  memcpy(ev_handle64, &h, sizeof(h));
+  *ev = e;
+  return MPS_OK;
+}
+int mps_ipc_event_open(const void* ev_handle64, void** ev) {
+  if (!ev_handle64 || !ev) return MPS_ERR_VALIDATION;
+  cudaIpcEventHandle_t h;
+  memcpy(&h, ev_handle64, sizeof(h));
+  cudaEvent_t e;
+  if (cudaIpcOpenEventHandle(&e, h) != cudaSuccess) {
+    cudaGetLastError();
+    return MPS_ERR_GENERIC;
+  }
+  *ev = e;
+  return MPS_OK;
+}
+int mps_event_record(void* ev, uint64_t stream) {
+  return cudaEventRecord((cudaEvent_t)ev, reinterpret_cast<cudaStream_t>(stream)) == cudaSuccess ? MPS_OK
+                                                                                                  : MPS_ERR_GENERIC;
+}
+int mps_stream_wait_event(uint64_t stream, void* ev) {
+  return cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(stream), (cudaEvent_t)ev, 0) == cudaSuccess
+             ? MPS_OK
+             : MPS_ERR_GENERIC;
+}
+int mps_event_destroy(void* ev) { return cudaEventDestroy((cudaEvent_t)ev) == cudaSuccess ? MPS_OK : MPS_ERR_GENERIC; }
+
 int mps_stream_uniforms(uint64_t seed, int64_t first, int count, int M, double* out, uint64_t stream) {
   if (!out || count < 0 || M < 1 || first < 0) return MPS_ERR_VALIDATION;
   if (count == 0) return MPS_OK;

@@ -85,16 +85,155 @@ def run_pipeline(stage_fn, n_micro: int, recv_like, send_like, rank: int, world:
             r.wait()
 
 
+class P2PHandoff:
+    """Fused stage hand-off over peer memory (the B200-native alternative to the NCCL send/recv of
+    run_pipeline).  Rank g > 0 owns two receive buffers for its input state and two "consumed"
+    interprocess events; rank g < G-1 maps rank g+1's receive buffers (CUDA IPC, NVLink peer
+    memory) and owns two "filled" events.  A stage's last draw kernel writes the next stage's input
+    directly into the mapped buffer (state_out = the peer pointer): no collective and no staging
+    copy on the data path.  GPU-side ordering uses the events; the only host traffic is one tiny
+    message per micro-batch and direction on a gloo group (which event record to wait on)."""
+
+    def __init__(self, rank: int, world: int, recv_bytes: int, host_group=None):
+        import ctypes
+
+        import torch.distributed as dist
+
+        from . import _native
+
+        self.L = _native.lib()
+        self.rank, self.world, self.group = rank, world, host_group
+        self.recv, self.consumed, self.filled = [None, None], [None, None], [None, None]
+        self.peer_recv, self.peer_consumed, self.peer_filled = [None, None], [None, None], [None, None]
+        mine = {}
+        H = ctypes.c_char * 64
+
+        def new_event():
+            ev, h = ctypes.c_void_p(), H()
+            _native.check(self.L.mps_ipc_event_create(ctypes.byref(ev), h))
+            return ev.value, bytes(h)
+
+        if rank > 0:
+            mine["recv"], mine["consumed"] = [], []
+            for b in range(2):
+                p, h = ctypes.c_void_p(), H()
+                _native.check(self.L.mps_ipc_alloc(recv_bytes, ctypes.byref(p), h))
+                self.recv[b] = p.value
+                mine["recv"].append(bytes(h))
+                self.consumed[b], hb = new_event()
+                mine["consumed"].append(hb)
+        if rank < world - 1:
+            mine["filled"] = []
+            for b in range(2):
+                self.filled[b], hb = new_event()
+                mine["filled"].append(hb)
+        everyone = [None] * world
+        dist.all_gather_object(everyone, mine, group=host_group)
+
+        def open_mem(hb):
+            p = ctypes.c_void_p()
+            _native.check(self.L.mps_ipc_open(H.from_buffer_copy(hb), ctypes.byref(p)))
+            return p.value
+
+        def open_event(hb):
+            ev = ctypes.c_void_p()
+            _native.check(self.L.mps_ipc_event_open(H.from_buffer_copy(hb), ctypes.byref(ev)))
+            return ev.value
+
+        if rank < world - 1:
+            nxt = everyone[rank + 1]
+            self.peer_recv = [open_mem(h) for h in nxt["recv"]]
+            self.peer_consumed = [open_event(h) for h in nxt["consumed"]]
+        if rank > 0:
+            self.peer_filled = [open_event(h) for h in everyone[rank - 1]["filled"]]
+
+    def close(self):
+        for p in self.peer_recv:
+            if p:
+                self.L.mps_ipc_close(p)
+        for ev in self.peer_consumed + self.peer_filled + self.consumed + self.filled:
+            if ev:
+                self.L.mps_event_destroy(ev)
+        for p in self.recv:
+            if p:
+                self.L.mps_ipc_free(p)
+        self.recv = self.peer_recv = [None, None]
+        self.consumed = self.filled = self.peer_consumed = self.peer_filled = [None, None]
+
+
+def run_pipeline_p2p(stage_fn, n_micro: int, handoff: P2PHandoff, stream: int, rank: int, world: int,
+                     group=None):
+    """Drive one pipeline stage with the fused peer-memory hand-off.
+
+    stage_fn(t, state_in_ptr, state_out_ptr) enqueues this stage's sites for micro-batch t on
+    `stream` (raw cudaStream_t); state_in_ptr is None on stage 0 and state_out_ptr None on the last
+    stage.  Buffer b = t % 2 on both sides; the producer waits for the consumer's "consumed"
+    record of micro-batch t - 2 before overwriting buffer b, the consumer for the producer's
+    "filled" record of t.  Host messages (gloo, asynchronous sends) say which record to wait on;
+    nothing blocks the GPU or spins in a kernel."""
+    import torch
+    import torch.distributed as dist
+
+    L = handoff.L
+    pending = []
+
+    def send(dst, t):
+        msg = torch.tensor([t], dtype=torch.int64)
+        pending.append((dist.isend(msg, dst=dst, group=group), msg))
+
+    def recv(src, expect):
+        msg = torch.zeros(1, dtype=torch.int64)
+        dist.recv(msg, src=src, group=group)
+        if int(msg.item()) != expect:
+            raise ValidationError(f"pipeline hand-off out of order: got {int(msg.item())}, expected {expect}")
+
+    consumed_seen = 0
+    for t in range(n_micro):
+        b = t % 2
+        x = out = None
+        if rank > 0:
+            recv(rank - 1, t)  # stage rank-1 has enqueued micro-batch t into my buffer b
+            L.mps_stream_wait_event(stream, handoff.peer_filled[b])
+            x = handoff.recv[b]
+        if rank < world - 1:
+            if t >= 2:
+                recv(rank + 1, t - 2)  # the next stage has enqueued its read of buffer b (t - 2)
+                consumed_seen += 1
+                L.mps_stream_wait_event(stream, handoff.peer_consumed[b])
+            out = handoff.peer_recv[b]
+        stage_fn(t, x, out)
+        if rank > 0:
+            L.mps_event_record(handoff.consumed[b], stream)
+            send(rank - 1, t)
+        if rank < world - 1:
+            L.mps_event_record(handoff.filled[b], stream)
+            send(rank + 1, t)
+    if rank < world - 1:  # drain the consumer's last acknowledgements
+        for t in range(consumed_seen, n_micro):
+            recv(rank + 1, t)
+    for req, _ in pending:
+        req.wait()
+
+
 def _as_real(t):
     import torch
 
     return torch.view_as_real(t) if t.is_complex() else t
 
 
+def _for_backend(t, group):
+    """gloo collectives take host tensors, NCCL device tensors."""
+    import torch.distributed as dist
+
+    return t.cpu() if dist.get_backend(group) == "gloo" else t
+
+
 def gather_rows(local, rank: int, world: int, dst: int = 0, group=None):
     """Gather variable-length row blocks (first axis) to `dst`, in rank order."""
     import torch
     import torch.distributed as dist
+
+    local = _for_backend(local, group)
 
     rows = torch.tensor([local.shape[0]], dtype=torch.int64, device=local.device)
     all_rows = [torch.zeros_like(rows) for _ in range(world)]
@@ -113,6 +252,8 @@ def gather_columns(local, m_begin: int, M: int, rank: int, world: int, dst: int 
     """Assemble per-stage column blocks (counts of the stage's modes) into N x M on `dst`."""
     import torch
     import torch.distributed as dist
+
+    local = _for_backend(local, group)
 
     meta = torch.tensor([m_begin, local.shape[1]], dtype=torch.int64, device=local.device)
     metas = [torch.zeros_like(meta) for _ in range(world)]
@@ -180,11 +321,15 @@ def sample_sharded(config, mps, device: int | None = None, group=None):
                           indices=np.nonzero(keep)[0])
 
 
-def sample_pipelined(config, mps_block, device: int | None = None, group=None):
+def sample_pipelined(config, mps_block, device: int | None = None, group=None, handoff: str = "nccl",
+                     host_group=None):
     """Mode-pipelined batch_sample: rank g holds the sites of stage_blocks(...)[g] (the other
     sites may be SiteShape placeholders), micro-batches of config.batch_size samples flow
-    through the ranks with the n x chi state handed on by send/recv; each rank's count columns
-    are gathered to rank 0.  Returns an MpsSampleBatch on rank 0, None elsewhere."""
+    through the ranks with the n x chi state handed on by NCCL send/recv (handoff="nccl") or
+    written by the stage's last draw kernel straight into the next rank's buffer over peer memory
+    (handoff="p2p", P2PHandoff; host_group: a gloo group for its per-micro-batch messages, default
+    `group`); each rank's count columns are gathered to rank 0.  Returns an MpsSampleBatch on
+    rank 0, None elsewhere; the counts do not depend on the hand-off."""
     import time
 
     import torch
@@ -213,7 +358,25 @@ def sample_pipelined(config, mps_block, device: int | None = None, group=None):
                     status=status[t * n:(t + 1) * n])
             return y
 
-        if world > 1:
+        if world > 1 and handoff == "p2p":
+            hp = P2PHandoff(rank, world, n * dims[mb] * (8 if cdt == torch.complex64 else 16),
+                            host_group=host_group if host_group is not None else group)
+            stream = torch.cuda.current_stream(dev).cuda_stream
+
+            def stage_p2p(t, x, out):
+                eng.run(t * n, n, counts[t * n:(t + 1) * n], m_begin=mb, m_end=me, state_in=x, state_out=out,
+                        status=status[t * n:(t + 1) * n], stream=stream)
+
+            try:
+                run_pipeline_p2p(stage_p2p, T, hp, stream, rank, world,
+                                 group=host_group if host_group is not None else group)
+                torch.cuda.synchronize(dev)
+            finally:
+                import torch.distributed as dist
+
+                dist.barrier(group=host_group if host_group is not None else group)  # peers are done with my buffers
+                hp.close()
+        elif world > 1:
             run_pipeline(stage, T, recv_like=lambda: torch.empty((n, dims[mb]), dtype=cdt, device=dev),
                          send_like=lambda: torch.empty((n, dims[me]), dtype=cdt, device=dev), rank=rank, world=world,
                          group=group)
@@ -227,7 +390,7 @@ def sample_pipelined(config, mps_block, device: int | None = None, group=None):
         import torch.distributed as dist
 
         # status bits OR-ed over the stages (NCCL has no bitwise reduce: MAX per bit)
-        bits = torch.stack([status & 1, (status >> 1) & 1]).to(torch.int32)
+        bits = _for_backend(torch.stack([status & 1, (status >> 1) & 1]).to(torch.int32), group)
         dist.all_reduce(bits, op=dist.ReduceOp.MAX, group=group)
         status = (bits[0] | (bits[1] << 1)).to(torch.uint8)
     else:

@@ -94,6 +94,8 @@ class MpsSampleBatch:
 def _ptr(x) -> int | None:
     if x is None:
         return None
+    if isinstance(x, int):  # a raw device pointer (e.g. a peer buffer mapped by distributed.P2PHandoff)
+        return x
     if isinstance(x, np.ndarray):
         return x.ctypes.data
     return x.data_ptr()  # torch tensor
