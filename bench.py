@@ -351,7 +351,7 @@ def run_pipelined(args, rank, world, local, W, K, config, dims):
     gemm_flops_avg = prof["gemm_flops"] / max(prof["gemm_launches"], 1)
     achieved = gemm_flops_avg / (gemm_ms_avg / 1e3) / 1e12 if gemm_ms_avg > 0 else 0.0
     kernel_name = {"3m": "site_gemm3m_kernel (K1, FP64 DMMA, 3M)", "4m": "site_gemm_kernel (K1, FP64 DMMA, 4M)",
-                   "ozaki": "ozaki_gemm_kernel (K1, fp64 emulated on INT8 tcgen05, 7 digits)"}[args.gemm]
+                   "ozaki": "ozaki2_gemm_kernel (K1, fp64 emulated on INT8 tcgen05, 7 digits)"}[args.gemm]
     bound_note = None
     if args.dtype == "c64":
         # tcgen05 kind::tf32 executes 3 passes (hi.hi, hi.lo, lo.hi) of the real-doubled
@@ -362,6 +362,13 @@ def run_pipelined(args, rank, world, local, W, K, config, dims):
         peak_src = f"dense TF32 = 1/2 of {src} bf16 {bf16:.0f} TFLOP/s"
         kernel_name = "c64_gemm_kernel (K1, tcgen05 kind::tf32, 3xTF32)"
         bound_note = "achieved counts executed tensor flops (3 passes x 8 per complex MAC)"
+    elif args.gemm == "ozaki":
+        # 28 int8 digit products (diagonals i + j < 7) of the real-doubled product per complex MAC;
+        # the roofline is the measured kind::i8 issue rate
+        achieved, peak = 28.0 * achieved, 4510.5
+        peak_src = "profiles/r01_umma_probe.jsonl (kind::i8 M=128 N=128 issue-rate probe), TOP/s"
+        kernel_name = "ozaki2_gemm_kernel (K1, complex128 emulated on INT8 tcgen05, 7 digits, CTA pairs)"
+        bound_note = "achieved counts executed int8 tensor ops (28 digit products x 8 per complex MAC)"
     step_flops = sum(site_flops(dims, D, n))
     whole_tf = K * step_flops / (ms / 1e3) / 1e12
     ok = not bool((status[W:] & 1).any().item())
@@ -479,12 +486,16 @@ def run_stage(args, local, W, K, config, dims):
     gemm_flops_avg = prof["gemm_flops"] / max(prof["gemm_launches"], 1)
     achieved = gemm_flops_avg / (gemm_ms_avg / 1e3) / 1e12 if gemm_ms_avg > 0 else 0.0
     kernel_name = {"3m": "site_gemm3m_kernel (K1, FP64 DMMA, 3M)", "4m": "site_gemm_kernel (K1, FP64 DMMA, 4M)",
-                   "ozaki": "ozaki_gemm_kernel (K1, fp64 emulated on INT8 tcgen05, 7 digits)"}[args.gemm]
+                   "ozaki": "ozaki2_gemm_kernel (K1, fp64 emulated on INT8 tcgen05, 7 digits)"}[args.gemm]
     if args.dtype == "c64":
         bf16, src = measured_bf16()
         achieved, peak = 3.0 * achieved, bf16 / 2.0
         peak_src = f"dense TF32 = 1/2 of {src} bf16 {bf16:.0f} TFLOP/s"
         kernel_name = "c64_gemm_kernel (K1, tcgen05 kind::tf32, 3xTF32; achieved = executed tensor flops)"
+    elif args.gemm == "ozaki":
+        achieved, peak = 28.0 * achieved, 4510.5
+        peak_src = "profiles/r01_umma_probe.jsonl (kind::i8 M=128 N=128 issue-rate probe), TOP/s"
+        kernel_name = "ozaki2_gemm_kernel (K1, INT8 tcgen05; achieved = executed int8 ops, 28 per algorithmic flop)"
     stage_flops = sum(site_flops(dims, D, n)[mb:me])
     value = K * n / (ms / 1e3)
     T = (N_total + n - 1) // n
@@ -763,7 +774,7 @@ def main():
     gemm_flops_avg = prof["gemm_flops"] / max(prof["gemm_launches"], 1)
     achieved = gemm_flops_avg / (gemm_ms_avg / 1e3) / 1e12 if gemm_ms_avg > 0 else 0.0
     kernel_name = {"3m": "site_gemm3m_kernel (K1, FP64 DMMA, 3M)", "4m": "site_gemm_kernel (K1, FP64 DMMA, 4M)",
-                   "ozaki": "ozaki_gemm_kernel (K1, fp64 emulated on INT8 tcgen05, 7 digits)"}[args.gemm]
+                   "ozaki": "ozaki2_gemm_kernel (K1, fp64 emulated on INT8 tcgen05, 7 digits)"}[args.gemm]
     bound_note = None
     if args.dtype == "c64":
         # tcgen05 kind::tf32 executes 3 passes (hi.hi, hi.lo, lo.hi) of the real-doubled
@@ -774,6 +785,13 @@ def main():
         peak_src = f"dense TF32 = 1/2 of {src} bf16 {bf16:.0f} TFLOP/s"
         kernel_name = "c64_gemm_kernel (K1, tcgen05 kind::tf32, 3xTF32)"
         bound_note = "achieved counts executed tensor flops (3 passes x 8 per complex MAC)"
+    elif args.gemm == "ozaki":
+        # 28 int8 digit products (diagonals i + j < 7) of the real-doubled product per complex MAC;
+        # the roofline is the measured kind::i8 issue rate
+        achieved, peak = 28.0 * achieved, 4510.5
+        peak_src = "profiles/r01_umma_probe.jsonl (kind::i8 M=128 N=128 issue-rate probe), TOP/s"
+        kernel_name = "ozaki2_gemm_kernel (K1, complex128 emulated on INT8 tcgen05, 7 digits, CTA pairs)"
+        bound_note = "achieved counts executed int8 tensor ops (28 digit products x 8 per complex MAC)"
     step_flops = sum(site_flops(dims, D, n))
     whole_tf = world * K * step_flops / (ms / 1e3) / 1e12
 
