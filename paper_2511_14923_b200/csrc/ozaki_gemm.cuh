@@ -539,10 +539,31 @@ __global__ void ozaki_slice_rows_kernel(const double2* __restrict__ V, int K, in
   int e = 0;
   if (red[0] > 0.0) frexp(red[0], &e);  // max < 2^e
   if (threadIdx.x == 0) e_out[b] = e;
+  // each thread slices 16 consecutive reals (a 16-byte run of every digit plane: one contiguous,
+  // 16-byte aligned piece of the tiled layout) and stores it with one vector store per plane
   const int KS = ld / 32;
-  for (int kk = threadIdx.x; kk < ld; kk += blockDim.x) {
-    const double x = (kk < 2 * K) ? ((kk & 1) ? v[kk >> 1].y : v[kk >> 1].x) : 0.0;
-    ozaki_digits(x, e, S, planes + oz_tiled(b, kk, OZ_TR_A, KS, S));
+  const double sc = ldexp(1.0, -e);
+  for (int c0 = 16 * threadIdx.x; c0 < ld; c0 += 16 * blockDim.x) {
+    double t[16];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int kc = (c0 >> 1) + q;
+      const double2 z = (2 * kc < 2 * K) ? v[kc] : make_double2(0.0, 0.0);
+      t[2 * q] = z.x * sc;  // exact: a power-of-two scaling
+      t[2 * q + 1] = z.y * sc;
+    }
+    int8_t* dst = planes + oz_tiled(b, c0, OZ_TR_A, KS, S);
+    for (int i = 0; i < S; ++i) {
+      uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        t[q] *= 128.0;
+        const double d = trunc(t[q]);
+        t[q] -= d;
+        w[q >> 2] |= ((uint32_t)(uint8_t)(int8_t)(int)d) << (8 * (q & 3));
+      }
+      *reinterpret_cast<uint4*>(dst + i * 256) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
   }
 }
 
