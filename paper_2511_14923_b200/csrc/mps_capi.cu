@@ -562,7 +562,7 @@ static cudaError_t launch_ozaki2(const int8_t* a_planes, int n_pad, const int* e
   }
   const int mtiles = round_up((n + Cfg::BM - 1) / Cfg::BM, MP);
   dim3 grid(2 * mtiles, (2 * N + Cfg::BN - 1) / Cfg::BN);
-  const int KB = ld / Cfg::BK;
+  const int KS = ld / Cfg::BK;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(Cfg::THREADS);
@@ -577,8 +577,14 @@ static cudaError_t launch_ozaki2(const int8_t* a_planes, int n_pad, const int* e
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  return cudaLaunchKernelEx(&cfg, ozaki2_gemm_kernel<Cfg>, a_planes, b_planes, ea, eb, (double*)C, n, 2 * N, KB,
-                            2LL * N);
+  // K segments of <= OZ_SEG_KB steps keep every int32 diagonal sum exact; later ones add into C
+  for (int kb0 = 0; kb0 < KS; kb0 += OZ_SEG_KB) {
+    const int KB = std::min(OZ_SEG_KB, KS - kb0);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, ozaki2_gemm_kernel<Cfg>, a_planes, b_planes, ea, eb, (double*)C, n, 2 * N,
+                                       KB, 2LL * N, KS, kb0, kb0 > 0 ? 1 : 0);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 static bool ozaki_v1() {
@@ -595,7 +601,7 @@ static bool ozaki_v1() {
 template <int S>
 static cudaError_t launch_ozaki_s(const int8_t* a_planes, int n_pad, const int* ea, const int8_t* b_planes, int b_pad,
                                   const int* eb, int ld, double2* C, int n, int K, int N, cudaStream_t st) {
-  if (ozaki_v1()) return launch_ozaki_cl<S, 1, 1>(a_planes, n_pad, ea, b_planes, b_pad, eb, ld, C, n, K, N, st);
+  if (ozaki_v1() && K <= OZ_MAX_K) return launch_ozaki_cl<S, 1, 1>(a_planes, n_pad, ea, b_planes, b_pad, eb, ld, C, n, K, N, st);
   return launch_ozaki2<S, 1>(a_planes, n_pad, ea, b_planes, b_pad, eb, ld, C, n, K, N, st);
 }
 
@@ -981,9 +987,6 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
   if (ozaki) {
     for (int m = m_begin; m < m_end; ++m) {
       if (c->sites[m].host) return fail(c, MPS_ERR_VALIDATION, "host-streamed sites do not support gemm mode 8");
-      if (c->sites[m].chi_l > OZ_MAX_K)
-        return fail(c, MPS_ERR_VALIDATION, "gemm mode 8 supports chi_l <= %d (int32 diagonal sums); site %d has %d",
-                    OZ_MAX_K, m, c->sites[m].chi_l);
     }
     for (int m = m_begin; m < m_end; ++m) CU(c, ozaki_prepare_site(c->sites[m], D, c->oz_S), "Ozaki site digits");
   }
@@ -1406,7 +1409,7 @@ int mps_site_gemm(const void* V, const void* G, void* C, int n, int K, int N, in
 }
 
 int mps_site_gemm_ozaki(const void* V, const void* G, void* C, int n, int K, int N, int S, uint64_t stream) {
-  if (!V || !G || !C || n < 1 || K < 1 || K > OZ_MAX_K || N < 1 || S < 5 || S > 7) return MPS_ERR_VALIDATION;
+  if (!V || !G || !C || n < 1 || K < 1 || N < 1 || S < 5 || S > 7) return MPS_ERR_VALIDATION;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int ld = oz_ld(K), n_pad = round_up(n, 256), b_pad = round_up(2 * N, 256);
   int8_t *ap = nullptr, *bp = nullptr;
@@ -1454,7 +1457,7 @@ int mps_ozaki_site_planes(const void* G, int K, int N, int S, int8_t* planes, in
 
 int mps_ozaki_gemm_planes(const int8_t* a_planes, int n_pad, const int* ea, const int8_t* b_planes, int b_pad,
                           const int* eb, int ld, void* C, int n, int K, int N, int S, uint64_t stream) {
-  if (!a_planes || !b_planes || !ea || !eb || !C || n < 1 || K < 1 || K > OZ_MAX_K || N < 1 || S < 5 || S > 7 || ld < 2 * K ||
+  if (!a_planes || !b_planes || !ea || !eb || !C || n < 1 || K < 1 || N < 1 || S < 5 || S > 7 || ld < 2 * K ||
       ld % 32 || n_pad < n || n_pad % 256 || b_pad < 2 * N || b_pad % 256)
     return MPS_ERR_VALIDATION;
   return launch_ozaki(S, a_planes, n_pad, ea, b_planes, b_pad, eb, ld, (double2*)C, n, K, N,

@@ -7,8 +7,8 @@
 // exact up to 2^{-7S} of the row scale).  A product of two rows is then
 //   a.b = 2^{e_a + e_b} sum_d 2^{-7(d+2)} sum_{i+j=d} a_i . b_j
 // where every a_i . b_j is an exact int32 dot product, and a diagonal's int32 accumulator holds
-// at most S products: |sum| <= S K 127^2 < 2^31 needs K (real) <= 18862 for S = 7, so the
-// library refuses mode 8 for chi_l > 9400.  Diagonals d = i + j >= S are dropped (their weight is
+// at most S products: |sum| <= S K 127^2 < 2^31 needs K (real) <= 18862 for S = 7, so a longer K
+// runs as several launches of <= 588 K steps, each adding its fp64 partial into C.  Diagonals d = i + j >= S are dropped (their weight is
 // <= 2^{-7(S+2)}: S = 7 leaves ~1e-13 of the row scales, far inside the 1e-10 parity bar;
 // tests/test_gpu_parity.py checks it).
 //
@@ -28,7 +28,8 @@
 namespace mps {
 
 constexpr int OZ_MAX_S = 7;
-constexpr int OZ_MAX_K = 9400;  // complex K: 7 x (2 K) x 127^2 < 2^31
+constexpr int OZ_MAX_K = 9400;  // complex K per launch of the single-CTA kernel: 7 x (2 K) x 127^2 < 2^31
+constexpr int OZ_SEG_KB = 588;  // 32-byte K steps per launch of the pair kernel (18816 reals, same bound)
 
 // K-major, 32-byte swizzle (rows of 32 B = one K step); sbo = byte stride between 8-row atoms
 __device__ __forceinline__ uint64_t umma_desc_k_sw32(uint32_t saddr, uint32_t sbo) {
@@ -334,7 +335,9 @@ template <class Cfg>
 __global__ void __launch_bounds__(Cfg::THREADS, 1)
     ozaki2_gemm_kernel(const int8_t* __restrict__ a_planes, const int8_t* __restrict__ b_planes,
                        const int* __restrict__ ea, const int* __restrict__ eb, double* __restrict__ C, int n, int N2,
-                       int KB, long long ldc) {
+                       int KB, long long ldc, int KS, int kb0, int accumulate) {
+  // K steps [kb0, kb0 + KB) of the KS of the tiled planes; accumulate: C += this segment's product
+  // (K longer than the int32-exact OZ_SEG_KB steps runs as several launches, see launch_ozaki2)
   constexpr int S = Cfg::S, CL = Cfg::CL;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -383,13 +386,14 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         uint8_t* st = smem + s * Cfg::STAGE_BYTES;
         mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
         if constexpr (Cfg::MC) {
-          bulk_load_mc(st + a_off, a_planes + oz_slice(ar, kb, OZ_TR_A, KB, S), a_bytes, &full[s], mask_a);
-          bulk_load_mc(st + Cfg::A_BYTES + b_off, b_planes + oz_slice(br, kb, OZ_TR_B, KB, S), b_bytes, &full[s],
+          bulk_load_mc(st + a_off, a_planes + oz_slice(ar, kb0 + kb, OZ_TR_A, KS, S), a_bytes, &full[s], mask_a);
+          bulk_load_mc(st + Cfg::A_BYTES + b_off, b_planes + oz_slice(br, kb0 + kb, OZ_TR_B, KS, S), b_bytes, &full[s],
                        mask_all);
         } else {
-          bulk_load_1d(st, a_planes + oz_slice(m0, kb, OZ_TR_A, KB, S), Cfg::A_BYTES, &full[s]);
-          bulk_load_1d(st + Cfg::A_BYTES, b_planes + oz_slice(n0, kb, OZ_TR_B, KB, S), Cfg::B_BYTES / 2, &full[s]);
-          bulk_load_1d(st + Cfg::A_BYTES + Cfg::B_BYTES / 2, b_planes + oz_slice(n0 + 64, kb, OZ_TR_B, KB, S),
+          bulk_load_1d(st, a_planes + oz_slice(m0, kb0 + kb, OZ_TR_A, KS, S), Cfg::A_BYTES, &full[s]);
+          bulk_load_1d(st + Cfg::A_BYTES, b_planes + oz_slice(n0, kb0 + kb, OZ_TR_B, KS, S), Cfg::B_BYTES / 2,
+                       &full[s]);
+          bulk_load_1d(st + Cfg::A_BYTES + Cfg::B_BYTES / 2, b_planes + oz_slice(n0 + 64, kb0 + kb, OZ_TR_B, KS, S),
                        Cfg::B_BYTES / 2, &full[s]);
         }
       }
@@ -494,9 +498,14 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     }
     const double fr = oz_scale(1.0, era);  // 2^ea of my row: v 2^ea 2^eb is exact (powers of two)
     asm volatile("bar.sync 1, 128;" ::: "memory");  // epilogue warps only
+    const double* cold = C + (long long)row * ldc + n0 + oc0;  // the previous segments' sum
+    const bool add_old = accumulate && row < n;
     fold_half(oc0, [&](int c0, double (&acc)[16]) {
 #pragma unroll
-      for (int c = 0; c < 16; ++c) otile[rl * 66 + c0 + c] = (acc[c] + part[(c0 + c) * Cfg::BM + rl]) * fr * fcs[c0 + c];
+      for (int c = 0; c < 16; ++c) {
+        const double v = (acc[c] + part[(c0 + c) * Cfg::BM + rl]) * fr * fcs[c0 + c];
+        otile[rl * 66 + c0 + c] = (add_old && n0 + oc0 + c0 + c < N2) ? v + cold[c0 + c] : v;
+      }
     });
     fence_proxy_async();  // generic-proxy smem writes -> visible to the bulk copy engine
     const int ncols = min(Cfg::BN / 2, N2 - (n0 + oc0));

@@ -590,13 +590,21 @@ def test_ozaki_stage_split_and_ragged_lanes(c2_sites):
     assert np.array_equal(marg.cpu().numpy(), full["marginals"])
 
 
-def test_ozaki_refuses_int32_overflow_shapes():
-    """7 x (2 chi_l) x 127^2 must stay below 2^31 in a diagonal accumulator: chi_l > 9400 is refused."""
+@pytest.mark.parametrize("n,K,N", [(37, 9401, 45), (130, 20000, 70)])
+def test_ozaki_long_k_segments(n, K, N):
+    """K beyond the int32-exact 588 steps (chi_l > 9400) runs as several launches that add their
+    fp64 partials into C; the result keeps the 7-digit accuracy."""
     L = _native.lib()
-    V = torch.zeros(1, 9401, dtype=torch.complex128, device="cuda")
-    G = torch.zeros(9401, 1, dtype=torch.complex128, device="cuda")
-    C = torch.zeros(1, 1, dtype=torch.complex128, device="cuda")
-    assert L.mps_site_gemm_ozaki(V.data_ptr(), G.data_ptr(), C.data_ptr(), 1, 9401, 1, 7, 0) == 2
+    g = torch.Generator(device="cuda").manual_seed(K)
+    V = torch.randn(n, K, dtype=torch.complex128, device="cuda", generator=g)
+    G = torch.randn(K, N, dtype=torch.complex128, device="cuda", generator=g)
+    C = torch.full((n, N), complex(np.nan, np.nan), dtype=torch.complex128, device="cuda")
+    assert L.mps_site_gemm_ozaki(V.data_ptr(), G.data_ptr(), C.data_ptr(), n, K, N, 7, 0) == 0
+    torch.cuda.synchronize()
+    ref = V @ G
+    err = (C - ref).abs().max().item()
+    scale = (V.abs().max() * G.abs().max()).item() * np.sqrt(K)
+    assert err <= 2e-13 * scale, (err, scale)
 
 
 def test_chain_parity_ozaki(c2_sites):
