@@ -730,7 +730,7 @@ def main():
     # Same run, same inputs, K1 emulated on the INT8 tensor cores (gemm mode 8, Ozaki, ~1e-13):
     # reported next to the FP64-DMMA headline (the path the north star names) as "alt_gemm".
     alt = None
-    if args.dtype == "c128" and args.gemm != "ozaki" and not args.stream_sites and max(dims) <= 9400:
+    if args.dtype == "c128" and args.gemm != "ozaki" and not args.stream_sites:
         eng.set_gemm_mode(8)
         eng.set_lanes(LANES["ozaki"])
         for s in range(W):
