@@ -444,6 +444,24 @@ def test_sum_planes_chi1000_parity():
     _check_parity(sites, res, stream_uniforms(7, 0, N, M), alpha=alpha_stream(7, 0, N, M, 0.7))
 
 
+@pytest.fixture(scope="module")
+def chi4000_sites():
+    return orc.random_mps(8, 4000, 10, seed=11)
+
+
+@pytest.mark.parametrize("mode", [3, 8])
+def test_chi4000_chain_parity(mode, chi4000_sites):
+    """The C4 bond dimension (chi = 4000: a 40000-column site, the global-memory draw path) in both
+    complex128 K1 products, against the oracle."""
+    M, D, N = 8, 10, 48
+    sites = chi4000_sites
+    cfg = MpsSamplerConfig(N=N, seed=11, alpha_sigma=0.7, batch_size=N)
+    with MpsSampler(MPS(sites)) as eng:
+        eng.set_gemm_mode(mode)
+        res = eng.sample(cfg, return_marginals=True)
+    _check_parity(sites, res, stream_uniforms(11, 0, N, M), alpha=alpha_stream(11, 0, N, M, 0.7))
+
+
 # ------------------------------------------------------------------ complex64 (tcgen05)
 
 
