@@ -551,8 +551,8 @@ def main():
                     help="measure one stage (--stage g) of a G-stage mode pipeline alone on one GPU (c4/c5)")
     ap.add_argument("--stage", type=int, default=0)
     ap.add_argument("--n", type=int, default=0,
-                    help="pipeline micro-batch size for --stage-of runs (default: the config's batch n); "
-                         "per-sample results do not depend on it")
+                    help="micro-batch size (default: the config's batch n); with --lanes L it runs as L "
+                         "concurrent chains of n / L rows; per-sample results do not depend on either")
     args = ap.parse_args()
     args.lanes = args.lanes or LANES[args.gemm]
     W = max(args.warmup, 3)
@@ -561,10 +561,13 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = 0 if ONE_GPU else int(os.environ.get("LOCAL_RANK", "0"))
     M, chi, D, n, sigma, N_total, desc = CONFIGS[args.config]
+    if args.n and args.stage_of == 0:  # micro-batch override for the sample-sharded / pipelined runs
+        n = args.n
     from paper_2511_14923_b200.mps import bond_dims
 
     dims = bond_dims(M, chi, D)
-    config = {"workload": f"{args.config}: {desc}", "M": M, "chi": chi, "D": D, "n": args.n or n, "gemm": args.gemm,
+    config = {"workload": f"{args.config}: {desc}", "M": M, "chi": chi, "D": D, "n": n, "lanes": args.lanes,
+              "gemm": args.gemm,
               "sites_in": "host, streamed per step" if args.stream_sites else "HBM",
               "alpha": "CN(0,%.3g)" % (sigma * sigma), "sites": "random row-orthonormal, seed 0",
               "layout": "sample-sharded" if world > 1 else "single GPU",

@@ -152,7 +152,7 @@ int mps_site_gemm_cfg(const void* V, const void* G, void* C, int n, int K, int N
                       int64_t ldc, uint64_t stream, int cfg, int mode);
 /* Pin the K1 tile config of a context (-1 = autotune, the default; -2 = model). */
 int mps_set_gemm_config(mps_ctx* ctx, int cfg);
-/* Concurrent chains per call (1..4, default 2): the micro-batch is split into contiguous
+/* Concurrent chains per call (1..8, default 2): the micro-batch is split into contiguous
  * row blocks of >= 64 samples, each run on its own stream (forked from and joined back
  * to the caller's stream) so one block's draw kernels and GEMM tails overlap another's
  * GEMMs.  Per-sample results are identical for any lane count. */

@@ -194,7 +194,7 @@ struct mps_ctx {
   // lanes: the micro-batch is split into up to MAX_LANES contiguous row blocks, each run
   // as its own chain on its own stream, so one lane's draw kernel and GEMM tail overlap
   // the other lane's GEMM (per-sample results do not depend on the split)
-  static constexpr int MAX_LANES = 4;
+  static constexpr int MAX_LANES = 8;
   int lanes = 2;
   cudaStream_t lane_st[MAX_LANES] = {};
   cudaEvent_t fork_ev = nullptr, join_ev[MAX_LANES] = {};
