@@ -544,14 +544,19 @@ def test_c64_stage_split(c2_sites):
     assert np.array_equal(counts.cpu().numpy(), full["counts"])
 
 
-@pytest.mark.parametrize("dtype", ["complex128", "complex64"])
+@pytest.mark.parametrize("dtype", ["complex128", "complex64", "complex128-4m", "complex128-int8"])
 @pytest.mark.parametrize("M,chi,D,N", [(7, 7, 3, 37), (5, 9, 5, 130), (3, 1, 16, 64), (1, 1, 7, 33), (9, 40, 2, 257)])
 def test_odd_shapes(M, chi, D, N, dtype):
     """Ragged / odd shapes (odd N = chi_r D, odd K, D up to 16, chi = 1 product states, M = 1):
-    alignment paths of every kernel, both dtypes, against the fp64 oracle."""
+    alignment paths of every kernel, both dtypes and every complex128 K1 product, against the
+    fp64 oracle."""
+    mode = {"complex128-4m": 4, "complex128-int8": 8}.get(dtype, 3)
+    dtype = dtype.split("-")[0]
     sites = [s.astype(dtype) for s in orc.random_mps(M, chi, D, seed=M + D)]
     cfg = MpsSamplerConfig(N=N, seed=M, alpha_sigma=0.4, batch_size=N)
     with MpsSampler(MPS(sites)) as eng:
+        if dtype == "complex128":
+            eng.set_gemm_mode(mode)
         eng.set_lanes(2)
         res = eng.sample(cfg, return_marginals=True)
     u, al = stream_uniforms(M, 0, N, M), alpha_stream(M, 0, N, M, 0.4)
