@@ -157,6 +157,13 @@ int mps_set_gemm_config(mps_ctx* ctx, int cfg);
  * to the caller's stream) so one block's draw kernels and GEMM tails overlap another's
  * GEMMs.  Per-sample results are identical for any lane count. */
 int mps_set_lanes(mps_ctx* ctx, int lanes);
+/* Teacher forcing (the oracle's forced=, the pattern of gbsemu's forced path, sampler.py:394-416):
+ * when enabled, mps_sample / mps_sample_range read sample b's outcome at mode m from counts
+ * (an INPUT, left unchanged) instead of drawing it, and still return the normalised marginals
+ * along that path -- the per-mode conditional probabilities, whose logs sum to the sample's log
+ * probability under the chain.  An outcome outside [0, D) marks the sample failed; uniforms
+ * are ignored. */
+int mps_set_forced(mps_ctx* ctx, int enable);
 /* Sum planes for the 3M GEMM (default on): mps_set_site stores Gr+Gi next to each site
  * (+50% of the site's HBM, skipped per site when memory is short) and the draw kernel
  * writes Vr+Vi next to the state, so K1 loads the operand sums instead of forming them

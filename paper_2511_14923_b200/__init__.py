@@ -12,6 +12,8 @@ from .sampler import (
     MpsSampler,
     MpsSamplerConfig,
     batch_sample,
+    chain_joint_probability,
+    chain_log_probability,
     sample_one,
 )
 from .streams import alpha_stream, stream_uniforms

@@ -23,7 +23,7 @@ EXPORTS = (
     "mps_c64_state_planes", "mps_c64_site_planes", "mps_c64_gemm_planes", "mps_site_gemm_ozaki",
     "mps_ozaki_state_planes", "mps_ozaki_site_planes", "mps_ozaki_gemm_planes",
     "mps_ipc_alloc", "mps_ipc_free", "mps_ipc_open", "mps_ipc_close", "mps_ipc_event_create", "mps_ipc_event_open",
-    "mps_event_record", "mps_stream_wait_event", "mps_event_destroy",
+    "mps_event_record", "mps_stream_wait_event", "mps_event_destroy", "mps_set_forced",
 )
 
 MPS_SITE_HOST, MPS_SITE_DEVICE_COPY, MPS_SITE_DEVICE_BORROW, MPS_SITE_HOST_STREAM = 0, 1, 2, 3
@@ -58,6 +58,7 @@ def _declare(L):
     L.mps_set_gemm_mode.argtypes = [c_void_p, c_int]
     L.mps_set_lanes.argtypes = [c_void_p, c_int]
     L.mps_set_sum_planes.argtypes = [c_void_p, c_int]
+    L.mps_set_forced.argtypes = [c_void_p, c_int]
     L.mps_site_gemm_c64.argtypes = [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_uint64]
     L.mps_site_gemm_ozaki.argtypes = [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_uint64]
     L.mps_ozaki_state_planes.argtypes = [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_int, c_int, c_uint64]

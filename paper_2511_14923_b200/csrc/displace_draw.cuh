@@ -160,6 +160,7 @@ struct DrawArgs {
   float* a_lo;
   int ld_a;
   double tie_eps;           // |cdf - u| band that flags a draw (1e-10 c128, 1e-4 c64)
+  int forced;               // 1: take the outcome from counts (input) instead of drawing
   int32_t* counts;          // n x ld_c
   long long ld_c;
   double* marg;             // n x ld_c x D or null
@@ -328,7 +329,7 @@ __global__ void __launch_bounds__(DRAW_THREADS, C64 ? 8 : 4)
 
   if (dead) {  // dead sample: zero state, count -1 (deterministic chain)
     for (int j = tid; j < A.chi_r; j += DRAW_THREADS) store_state<C64>(A, b, j, make_double2(0.0, 0.0));
-    if (tid == 0) A.counts[crow] = -1;
+    if (tid == 0 && !A.forced) A.counts[crow] = -1;
     if (A.marg && tid < D) A.marg[crow * D + tid] = 0.0;
     return;
   }
@@ -417,6 +418,15 @@ __global__ void __launch_bounds__(DRAW_THREADS, C64 ? 8 : 4)
     int ksel = -1;
     if (!(P > 0.0) || !isfinite(P)) {
       st |= ST_FAILED;
+    } else if (A.forced) {
+      // teacher forcing (the oracle's forced=, sampler.py:394-416): follow the given outcome; an
+      // out-of-range outcome fails the sample, a zero-probability one zeroes the state (the next
+      // mode then fails), exactly as the oracle's chain does
+      ksel = A.counts[crow];
+      if (ksel < 0 || ksel >= D) {
+        st |= ST_FAILED;
+        ksel = -1;
+      }
     } else {
       const double u = A.u ? A.u[(long long)b * A.ld_u + A.m]
                            : philox_double(numpy_key0(A.seed), gi / 64, (gi % 64) * (uint64_t)A.M + A.m);
@@ -433,9 +443,9 @@ __global__ void __launch_bounds__(DRAW_THREADS, C64 ? 8 : 4)
       if (mind <= A.tie_eps) st |= ST_FLAGGED;
     }
     A.status[b] = st;
-    A.counts[crow] = ksel;
+    if (!A.forced) A.counts[crow] = ksel;
     k_s = ksel;
-    scale_s = (ksel >= 0) ? 1.0 / sqrt(p_s[ksel]) : 0.0;
+    scale_s = (ksel >= 0 && p_s[ksel] > 0.0) ? 1.0 / sqrt(p_s[ksel]) : 0.0;
     red[0][0] = P;  // red[] is free again: its reads finished before the last barrier
   }
   __syncthreads();

@@ -204,6 +204,7 @@ struct mps_ctx {
   int dtype = -1;                                   // MPS_C128 / MPS_C64, fixed by the first site
   int oz_S = 7;                                     // Ozaki digits per operand (gemm mode 8)
   bool draw_ring = true;                            // stage C rows through a TMA ring in the draw kernel
+  bool forced = false;                              // teacher forcing: outcomes read from counts
   // host->HBM site streaming: 2-slot ring filled on a copy stream ahead of the GEMMs
   cudaStream_t copy_st = nullptr;
   cudaEvent_t slot_ready[2] = {}, slot_free[2][MAX_LANES] = {};
@@ -1034,8 +1035,8 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
     else
       CU(c, cudaMemsetAsync(status_dev, 0, n, st), "memset status");
   }
-  if (counts_host && m_end - m_begin < M) {
-    // partial range into host arrays: keep the untouched columns
+  if (counts_host && (m_end - m_begin < M || c->forced)) {
+    // partial range into host arrays: keep the untouched columns (forced: the outcomes are inputs)
     CU(c, cudaMemcpyAsync(counts_dev, counts, (size_t)n * ld_c * sizeof(int32_t), cudaMemcpyHostToDevice, st),
        "H2D counts");
   }
@@ -1208,6 +1209,7 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
       a.a_lo = (c64 && !last_out) ? c->la_lo[cur[l]][l].p : nullptr;
       a.ld_a = plane_ld(2 * s.chi_r);
       a.tie_eps = c64 ? 1e-4 : TIE_EPS;
+      a.forced = c->forced ? 1 : 0;
       a.ldc = N;
       a.chi_r = s.chi_r;
       a.D = D;
@@ -1516,6 +1518,12 @@ int mps_site_gemm_c64(const void* V, const void* G, void* C, int n, int K, int N
     return MPS_ERR_GENERIC;
   }
   return cudaGetLastError() == cudaSuccess ? MPS_OK : MPS_ERR_GENERIC;
+}
+
+int mps_set_forced(mps_ctx* c, int enable) {
+  if (!c) return MPS_ERR_VALIDATION;
+  c->forced = enable != 0;
+  return MPS_OK;
 }
 
 int mps_set_sum_planes(mps_ctx* c, int enable) {

@@ -171,6 +171,46 @@ class MpsSampler:
                                      _ptr(status), 0 if stream is None else int(stream))
         _native.check(rc, self.ctx)
 
+    def set_forced(self, enable: bool):
+        """Teacher forcing (mps_set_forced): follow the outcomes in `counts` instead of drawing."""
+        _native.check(self.L.mps_set_forced(self.ctx, int(bool(enable))), self.ctx)
+
+    def evaluate(self, config: MpsSamplerConfig, counts, start: int = 0, disp=None, alpha=None) -> dict:
+        """Teacher-forced chain along given outcomes (the reference's forced path, sampler.py:394-416):
+        counts (n, M) int for samples start..start+n-1 (their displacement streams).  Returns
+        dict(marginals (n, M, D) normalised conditionals along the path, logp (n,) log joint
+        probability, status (n,) uint8); a sample whose path leaves the support has logp = -inf."""
+        torch = self._torch
+        counts = np.ascontiguousarray(counts, dtype=np.int32)
+        if counts.ndim != 2 or counts.shape[1] != self.M:
+            raise ValidationError(f"counts must have shape (n, {self.M}), got {counts.shape}")
+        n_all = counts.shape[0]
+        dev = torch.device("cuda", self.device)
+        c_dev = torch.from_numpy(counts).to(dev)
+        status = torch.zeros(n_all, dtype=torch.uint8, device=dev)
+        marg = torch.empty((n_all, self.M, self.D), dtype=torch.float64, device=dev)
+        self.set_streams(config.seed, config.alpha_sigma)
+        B = config.batch_size or DEFAULT_BATCH
+        self.set_forced(True)
+        try:
+            for s0 in range(0, n_all, B):
+                b = min(B, n_all - s0)
+                sl = slice(s0, s0 + b)
+                dsp = None if disp is None else np.ascontiguousarray(disp[sl], dtype=np.complex128)
+                alp = None if alpha is None else np.ascontiguousarray(alpha[sl], dtype=np.complex128)
+                self.run(start + s0, b, c_dev[sl], m_begin=0, m_end=self.M, disp=dsp, alpha=alp, marginals=marg[sl],
+                         status=status[sl])
+        finally:
+            self.set_forced(False)
+        torch.cuda.synchronize(dev)
+        inside = (c_dev >= 0) & (c_dev < self.D)
+        pk = torch.gather(marg, 2, c_dev.clamp(0, self.D - 1).long().unsqueeze(2)).squeeze(2)
+        logp = torch.where(inside & (pk > 0), torch.log(pk.clamp_min(1e-300)), torch.full_like(pk, -np.inf)).sum(1)
+        st = status.cpu().numpy()
+        logp = logp.cpu().numpy()
+        logp[(st & _native.MPS_STATUS_FAILED) != 0] = -np.inf
+        return dict(marginals=marg.cpu().numpy(), logp=logp, status=st)
+
     def set_lanes(self, lanes: int):
         """Concurrent row-block chains per call (mps_set_lanes); results do not depend on it."""
         _native.check(self.L.mps_set_lanes(self.ctx, int(lanes)), self.ctx)
@@ -294,3 +334,27 @@ def sample_one(mps: MPS, config: MpsSamplerConfig, index: int = 0, sampler: MpsS
     if res["status"][0] & _native.MPS_STATUS_FAILED:
         raise ValidationError("sample failed: non-finite or zero step norm")
     return res["counts"][0]
+
+
+def chain_log_probability(mps: MPS, counts, config: MpsSamplerConfig, start: int = 0, disp=None, alpha=None,
+                          sampler: MpsSampler | None = None) -> np.ndarray:
+    """log P(counts[b]) under the chain for samples start..start+n-1 (their displacement streams),
+    evaluated on the GPU by teacher forcing (batched analogue of gbsemu's chain_joint_probability,
+    sampler.py:590-601).  -inf where a path leaves the support."""
+    own = sampler is None
+    eng = sampler or MpsSampler(mps, device=config.device)
+    try:
+        return eng.evaluate(config, counts, start=start, disp=disp, alpha=alpha)["logp"]
+    finally:
+        if own:
+            eng.close()
+
+
+def chain_joint_probability(mps: MPS, counts, config: MpsSamplerConfig, index: int = 0,
+                            sampler: MpsSampler | None = None) -> float:
+    """Model joint probability of one fixed count string (length M) for sample `index` of the
+    configured streams (gbsemu chain_joint_probability, sampler.py:590-601)."""
+    counts = np.asarray(counts)
+    if counts.shape != (mps.M,):
+        raise ValidationError(f"counts must have length {mps.M}")
+    return float(np.exp(chain_log_probability(mps, counts[None, :], config, start=index, sampler=sampler)[0]))

@@ -21,6 +21,8 @@ if not torch.cuda.is_available():  # pragma: no cover
 
 from oracle import mps_oracle as orc  # noqa: E402
 from paper_2511_14923_b200 import (  # noqa: E402
+    chain_joint_probability,
+    chain_log_probability,
     MPS,
     MpsSampler,
     MpsSamplerConfig,
@@ -712,3 +714,31 @@ def test_pipelined_p2p_handoff_on_one_gpu(tmp_path, c2_sites):
                        capture_output=True, text=True, timeout=600, cwd=root)
     assert r.returncode == 0, r.stderr[-3000:]
     assert np.array_equal(np.load(out), ref.counts)
+
+
+@pytest.mark.parametrize("mode", [3, 8])
+def test_forced_evaluation_vs_oracle(c2_sites, mode):
+    """Teacher forcing (mps_set_forced): along the GPU's own samples and along random count strings
+    the GPU marginals and log joint probabilities match the oracle's forced chain (1e-10 / 1e-9
+    relative), and evaluating a sampled path reproduces the sampling run's marginals."""
+    N, M, D = 300, 16, 10
+    cfg = MpsSamplerConfig(N=N, seed=5, alpha_sigma=0.5, batch_size=128)
+    u, al = stream_uniforms(5, 0, N, M), alpha_stream(5, 0, N, M, 0.5)
+    with MpsSampler(MPS(c2_sites)) as eng:
+        eng.set_gemm_mode(mode)
+        smp = eng.sample(cfg, return_marginals=True)
+        ev = eng.evaluate(cfg, smp["counts"])
+        assert np.array_equal(ev["marginals"], smp["marginals"])
+        rng = np.random.default_rng(0)
+        rand = rng.integers(0, 3, size=(N, M)).astype(np.int32)  # low photon numbers: mostly in support
+        ev2 = eng.evaluate(cfg, rand)
+        lp = chain_log_probability(MPS(c2_sites), rand[:10], cfg, sampler=eng)
+    for counts, out in ((smp["counts"], ev), (rand, ev2)):
+        ref = orc.sample_chain(c2_sites, u, alpha=al, forced=counts, return_marginals=True)
+        assert np.abs(out["marginals"] - ref["marginals"]).max() <= MARG_TOL
+        fin = np.isfinite(ref["logp"])
+        assert np.array_equal(np.isfinite(out["logp"]), fin)
+        assert np.allclose(out["logp"][fin], ref["logp"][fin], rtol=1e-9, atol=1e-9)
+    assert np.allclose(lp, ev2["logp"][:10])
+    p1 = chain_joint_probability(MPS(c2_sites), rand[3], cfg, index=3)
+    assert np.isclose(np.log(p1), ev2["logp"][3], rtol=1e-12) if p1 > 0 else ev2["logp"][3] == -np.inf
