@@ -1,4 +1,4 @@
-"""Command line: ``python -m paper_2511_14923_b200 <gen-mps|sample> ...``.
+"""Command line: ``python -m paper_2511_14923_b200 <gen-mps|sample|evaluate> ...``.
 
 Mirrors the reference CLI's ``sample`` subcommand (cli.py:116-160) and its JSON run
 manifest (cli.py:45-74: config echo, SHA-256 of inputs, versions, wall time, peak RSS,
@@ -18,9 +18,9 @@ import time
 import numpy as np
 
 from .errors import GbsError, ValidationError
-from .formats import load_mps, save_clicks_text, save_counts, save_mps
+from .formats import load_counts, load_mps, save_clicks_text, save_counts, save_mps
 from .mps import MPS
-from .sampler import MpsSamplerConfig, batch_sample
+from .sampler import MpsSamplerConfig, batch_sample, chain_log_probability
 
 __version__ = "0.1.0"
 
@@ -87,6 +87,30 @@ def cmd_sample(args) -> int:
     return 0
 
 
+def cmd_evaluate(args) -> int:
+    """Log joint probability of each count row under the MPS (teacher-forced chain on the GPU;
+    row i is sample index start + i of the displacement stream)."""
+    t0 = time.perf_counter()
+    mps = load_mps(args.mps, device="cuda" if args.device_sites else None)
+    counts, D, seed = load_counts(args.counts)
+    if D != mps.D or counts.shape[1] != mps.M:
+        raise ValidationError(f"counts file (M={counts.shape[1]}, D={D}) does not match the MPS (M={mps.M}, D={mps.D})")
+    config = MpsSamplerConfig(N=counts.shape[0], seed=seed if args.seed is None else args.seed,
+                              alpha_sigma=args.alpha_sigma, batch_size=args.batch_size, device=args.device)
+    t1 = time.perf_counter()
+    logp = chain_log_probability(mps, counts, config, start=args.start)
+    dt = time.perf_counter() - t1
+    np.save(args.out, logp)
+    fin = np.isfinite(logp)
+    cfg = {k: v for k, v in vars(args).items() if k != "func"}
+    _emit(_manifest("evaluate", cfg, [args.mps, args.counts], [args.out], t0, extra={
+        "M": mps.M, "D": mps.D, "chi": mps.chi, "n": int(counts.shape[0]), "seed_used": config.seed,
+        "n_in_support": int(fin.sum()), "mean_logp": float(logp[fin].mean()) if fin.any() else None,
+        "throughput_per_s": counts.shape[0] / dt if dt > 0 else 0.0,
+    }))
+    return 0
+
+
 def build_parser() -> argparse.ArgumentParser:
     p = argparse.ArgumentParser(prog="paper_2511_14923_b200", description="B200 displaced-MPS sampler")
     sub = p.add_subparsers(dest="command", required=True)
@@ -108,6 +132,17 @@ def build_parser() -> argparse.ArgumentParser:
     s.add_argument("--out", required=True, help="counts file (.gmpc)")
     s.add_argument("--clicks-out", default=None, help="also write counts > 0 in the reference's text format")
     s.set_defaults(func=cmd_sample)
+    e = sub.add_parser("evaluate", help="log joint probability of count rows under the MPS (teacher forcing, GPU)")
+    e.add_argument("--mps", required=True)
+    e.add_argument("--counts", required=True, help="counts file (.gmpc) from `sample`")
+    e.add_argument("--seed", type=int, default=None, help="stream seed (default: the counts file's)")
+    e.add_argument("--start", type=int, default=0, help="sample index of the first row")
+    e.add_argument("--alpha-sigma", type=float, default=None)
+    e.add_argument("--batch-size", type=int, default=None)
+    e.add_argument("--device", type=int, default=0)
+    e.add_argument("--device-sites", action="store_true")
+    e.add_argument("--out", required=True, help="log probabilities (.npy)")
+    e.set_defaults(func=cmd_evaluate)
     return p
 
 

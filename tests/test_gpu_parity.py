@@ -421,6 +421,12 @@ def test_cli_sample_end_to_end(tmp_path, capsys):
     lines = clicks.read_text().splitlines()
     assert lines[0].startswith("# gbs-samples v1 M=8 N=300 method=mps")
     assert lines[1] == "".join("1" if c > 0 else "0" for c in counts[0])
+    lp = tmp_path / "logp.npy"
+    assert main(["evaluate", "--mps", str(m), "--counts", str(out), "--alpha-sigma", "0.5", "--out", str(lp)]) == 0
+    man = json.loads(capsys.readouterr().out)
+    assert man["n_in_support"] == 300 and man["seed_used"] == 5
+    ref = orc.sample_chain(sites, stream_uniforms(5, 0, 300, 8), alpha=alpha_stream(5, 0, 300, 8, 0.5), forced=counts)
+    assert np.allclose(np.load(lp), ref["logp"], rtol=1e-9, atol=1e-9)
 
 
 @pytest.mark.parametrize("lanes", [1, 3])
