@@ -26,6 +26,7 @@
 #include "displace_draw.cuh"
 #include "ozaki_gemm.cuh"
 #include "site_gemm.cuh"
+#include "chain_small.cuh"
 
 using namespace mps;
 
@@ -133,6 +134,8 @@ struct Site {
   int8_t* oz = nullptr;
   int* oz_e = nullptr;
   int oz_S = 0, oz_ld = 0, oz_pad = 0;
+  // small-chain kernel copy of the site (chain_site_kernel layout), for chi_l <= 128, chi_r D <= 1024
+  double2* chain = nullptr;
   // complex64 sites: only the tcgen05 operand planes are kept (B_r^T hi / lo, 2N x ld fp32)
   float* bhi = nullptr;
   float* blo = nullptr;
@@ -144,6 +147,8 @@ struct Site {
     if (blo) cudaFree(blo);
     if (oz) cudaFree(oz);
     if (oz_e) cudaFree(oz_e);
+    if (chain) cudaFree(chain);
+    chain = nullptr;
     if (registered && host) cudaHostUnregister(const_cast<double2*>(host));
     host = nullptr;
     registered = false;
@@ -205,6 +210,11 @@ struct mps_ctx {
   int oz_S = 7;                                     // Ozaki digits per operand (gemm mode 8)
   bool draw_ring = true;                            // stage C rows through a TMA ring in the draw kernel
   bool forced = false;                              // teacher forcing: outcomes read from counts
+  // small chains (chi <= 128, chi D <= 1024, 3M): the whole mode loop in one persistent cluster
+  // kernel (chain_small.cuh); its per-site tensor maps + bond dims live in chain_meta
+  bool small_chain = true;
+  bool chain_dirty = true;
+  DevBuf<uint8_t> chain_meta;
   // host->HBM site streaming: 2-slot ring filled on a copy stream ahead of the GEMMs
   cudaStream_t copy_st = nullptr;
   cudaEvent_t slot_ready[2] = {}, slot_free[2][MAX_LANES] = {};
@@ -747,6 +757,90 @@ static cudaError_t launch_c64_gemm(const float* ahi, const float* alo, const flo
   return cudaLaunchKernelEx(&cfg, c64_gemm_kernel<Cfg, true>, tah, tal, tbh, tbl, C, n, 2 * N, KB, ldc_f);
 }
 
+// ---- small chains: the whole mode loop in one persistent cluster launch (chain_small.cuh) ----
+static bool small_chain_ok(const mps_ctx* c, int m_begin, int m_end) {
+  if (!c->small_chain || c->dtype != MPS_C128 || c->gemm_mode != 3) return false;
+  for (int m = m_begin; m < m_end; ++m) {
+    const Site& s = c->sites[m];
+    if (s.host || !s.chain || s.chi_l > SC_KMAX || s.chi_r * c->D > SC_NMAX) return false;
+  }
+  return true;
+}
+
+// per-site chain-layout pointers and chi_0..chi_M in device memory
+static cudaError_t chain_meta_upload(mps_ctx* c) {
+  if (!c->chain_dirty) return cudaSuccess;
+  const int M = c->M;
+  const size_t ptr_bytes = (size_t)M * sizeof(double2*);
+  std::vector<uint8_t> h(ptr_bytes + (M + 1) * sizeof(int), 0);
+  double2** ptrs = reinterpret_cast<double2**>(h.data());
+  int* chi = reinterpret_cast<int*>(h.data() + ptr_bytes);
+  for (int m = 0; m < M; ++m) {
+    const Site& s = c->sites[m];
+    if (!s.loaded) continue;
+    ptrs[m] = s.chain;
+    chi[m] = s.chi_l;
+    chi[m + 1] = s.chi_r;
+  }
+  cudaError_t e = c->chain_meta.ensure(h.size());
+  if (e == cudaSuccess) e = cudaMemcpy(c->chain_meta.p, h.data(), h.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) c->chain_dirty = false;
+  return e;
+}
+
+static void (*small_chain_kernel_for(int D))(ChainArgs) {
+  return D == 10 ? small_chain_kernel<10> : D == 4 ? small_chain_kernel<4> : small_chain_kernel<0>;
+}
+
+static cudaError_t launch_small_chain(mps_ctx* c, const ChainArgs& P, cudaStream_t st) {
+  void (*kern)(ChainArgs) = small_chain_kernel_for(c->D);
+  static std::map<void*, int> max_clusters;  // co-resident 8-CTA clusters per instantiation
+  static std::mutex mu;
+  int mc;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = max_clusters.find((void*)kern);
+    if (it == max_clusters.end()) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SC_SMEM);
+      if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+      cudaLaunchConfig_t q = {};
+      q.gridDim = dim3(SC_CL * 32);
+      q.blockDim = dim3(SC_THREADS);
+      q.dynamicSmemBytes = SC_SMEM;
+      cudaLaunchAttribute a[1];
+      a[0].id = cudaLaunchAttributeClusterDimension;
+      a[0].val.clusterDim.x = SC_CL;
+      a[0].val.clusterDim.y = 1;
+      a[0].val.clusterDim.z = 1;
+      q.attrs = a;
+      q.numAttrs = 1;
+      int num = 0;
+      if (cudaOccupancyMaxActiveClusters(&num, kern, &q) != cudaSuccess) {
+        cudaGetLastError();
+        num = 0;
+      }
+      it = max_clusters.emplace((void*)kern, num).first;
+    }
+    mc = it->second;
+  }
+  if (mc < 1) return cudaErrorNotSupported;  // no 16-CTA cluster fits: the caller takes the per-mode path
+  const int groups = (P.n + SC_CL - 1) / SC_CL;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(SC_CL * std::min(groups, mc));
+  cfg.blockDim = dim3(SC_THREADS);
+  cfg.dynamicSmemBytes = SC_SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = SC_CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, P);
+}
+
 extern "C" {
 
 int mps_create(int n_dev, const int* dev_ids, int layout, mps_ctx** out) {
@@ -789,6 +883,8 @@ int mps_create(int n_dev, const int* dev_ids, int layout, mps_ctx** out) {
   {
     const char* e = getenv("MPS_DRAW_RING");
     if (e && e[0] == '0') c->draw_ring = false;
+    e = getenv("MPS_SMALL_CHAIN");
+    if (e && e[0] == '0') c->small_chain = false;
   }
   *out = c;
   return MPS_OK;
@@ -801,6 +897,7 @@ int mps_configure(mps_ctx* c, int M, int D) {
   cudaSetDevice(c->device);
   for (auto& s : c->sites) s.release();
   c->sites.assign(M, Site());
+  c->chain_dirty = true;
   c->dtype = -1;
   c->M = M;
   c->D = D;
@@ -828,6 +925,7 @@ int mps_set_site(mps_ctx* c, int m, int chi_l, int chi_r, int D, const void* gam
   Site& s = c->sites[m];
   s.release();
   s = Site();
+  c->chain_dirty = true;
   const size_t elems = (size_t)chi_l * chi_r * D;
   const bool dev = is_device_ptr(gamma);
   if (dtype == MPS_C64 && flags == MPS_SITE_HOST_STREAM)
@@ -898,6 +996,20 @@ int mps_set_site(mps_ctx* c, int m, int chi_l, int chi_r, int D, const void* gam
   const uint64_t N = (uint64_t)chi_r * D;
   if (!make_tmap(&s.tmap, s.data, chi_l, 2 * N, 16 * N, 8))
     return fail(c, MPS_ERR_GENERIC, "site %d: cuTensorMapEncodeTiled failed", m);
+  // small-chain copy of the site in the ring's fragment layout (small sites only; no copy -> per-mode path)
+  if (chi_l <= SC_KMAX && (int)N <= SC_NMAX) {
+    const long long total = (long long)((chi_l + 7) / 8) * (((int)N + 7) / 8) * 64;
+    if (cudaMalloc(&s.chain, total * sizeof(double2)) == cudaSuccess) {
+      chain_site_kernel<<<(unsigned)((total + 255) / 256), 256>>>(s.data, chi_l, (int)N, s.chain);
+      if (cudaGetLastError() != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+        cudaFree(s.chain);
+        s.chain = nullptr;
+      }
+    } else {
+      s.chain = nullptr;
+    }
+    cudaGetLastError();
+  }
   // sum plane Gr + Gi for the 3M GEMM (+50% of the site's bytes); skipped when memory is short
   if (c->sum_planes) {
     const int ld = sum_ld((int)N);
@@ -1043,6 +1155,77 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
   if (marg_host && m_end - m_begin < M) {
     CU(c, cudaMemcpyAsync(marg_dev, marginals, (size_t)n * ld_c * D * sizeof(double), cudaMemcpyHostToDevice, st),
        "H2D marginals");
+  }
+
+  // ---- outputs back to the host ----
+  auto finish = [&]() -> int {
+    bool sync = false;
+    if (counts_host) {
+      CU(c, cudaMemcpyAsync(counts, counts_dev, (size_t)n * ld_c * sizeof(int32_t), cudaMemcpyDeviceToHost, st), "D2H counts");
+      sync = true;
+    }
+    if (marg_host) {
+      CU(c, cudaMemcpyAsync(marginals, marg_dev, (size_t)n * ld_c * D * sizeof(double), cudaMemcpyDeviceToHost, st),
+         "D2H marginals");
+      sync = true;
+    }
+    if (status_host) {
+      CU(c, cudaMemcpyAsync(status, status_dev, n, cudaMemcpyDeviceToHost, st), "D2H status");
+      sync = true;
+    }
+    if (sync || uniforms != u_dev || alpha != (const void*)alpha_dev || disp != (const void*)disp_dev)
+      CU(c, cudaStreamSynchronize(st), "stream sync");
+    return MPS_OK;
+  };
+
+  if (small_chain_ok(c, m_begin, m_end)) {
+    CU(c, chain_meta_upload(c), "chain metadata");
+    ChainArgs P;
+    P.sites = reinterpret_cast<const double2* const*>(c->chain_meta.p);
+    P.chi = reinterpret_cast<const int*>(c->chain_meta.p + (size_t)M * sizeof(double2*));
+    P.m_begin = m_begin;
+    P.m_end = m_end;
+    P.n = n;
+    P.state_in = (const double2*)state_in;
+    P.state_out = (double2*)state_out;
+    DrawArgs& a = P.d;
+    a = DrawArgs{};
+    a.tie_eps = TIE_EPS;
+    a.forced = c->forced ? 1 : 0;
+    a.D = D;
+    a.M = M;
+    a.first_index = first_index;
+    a.u = u_dev;
+    a.ld_u = ldu;
+    a.seed = c->seed;
+    a.disp = disp_dev;
+    a.alpha = alpha_dev;
+    a.alpha_sigma = (disp_dev || alpha_dev) ? -1.0 : c->alpha_sigma;
+    a.counts = counts_dev;
+    a.ld_c = ld_c;
+    a.marg = marg_dev;
+    a.status = status_dev;
+    double flops = 0.0;  // K1 algorithmic flops of the chain (8 per complex MAC)
+    for (int m = m_begin; m < m_end; ++m) flops += 8.0 * n * c->sites[m].chi_l * (double)c->sites[m].chi_r * D;
+    mps_ctx::Rec rg{0, nullptr, nullptr, flops};
+    if (c->profile & 1) {
+      rg.a = c->get_event();
+      rg.b = c->get_event();
+      cudaEventRecord(rg.a, st);
+    }
+    const cudaError_t le = launch_small_chain(c, P, st);
+    if (le == cudaErrorNotSupported) {
+      c->small_chain = false;  // this GPU cannot host the clusters: per-mode kernels from now on
+      if (c->profile & 1) c->event_pool.insert(c->event_pool.end(), {rg.a, rg.b});
+    } else {
+      CU(c, le, "small_chain launch");
+      c->launches++;
+      if (c->profile & 1) {
+        cudaEventRecord(rg.b, st);
+        c->recs.push_back(rg);
+      }
+      return finish();
+    }
   }
 
   // ---- the mode loop: L lanes (row blocks), each a chain on its own stream ----
@@ -1277,24 +1460,7 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
     CU(c, cudaStreamWaitEvent(st, c->join_ev[0], 0), "copy join wait");
   }
 
-  // ---- outputs back to the host ----
-  bool sync = false;
-  if (counts_host) {
-    CU(c, cudaMemcpyAsync(counts, counts_dev, (size_t)n * ld_c * sizeof(int32_t), cudaMemcpyDeviceToHost, st), "D2H counts");
-    sync = true;
-  }
-  if (marg_host) {
-    CU(c, cudaMemcpyAsync(marginals, marg_dev, (size_t)n * ld_c * D * sizeof(double), cudaMemcpyDeviceToHost, st),
-       "D2H marginals");
-    sync = true;
-  }
-  if (status_host) {
-    CU(c, cudaMemcpyAsync(status, status_dev, n, cudaMemcpyDeviceToHost, st), "D2H status");
-    sync = true;
-  }
-  if (sync || uniforms != u_dev || alpha != (const void*)alpha_dev || disp != (const void*)disp_dev)
-    CU(c, cudaStreamSynchronize(st), "stream sync");
-  return MPS_OK;
+  return finish();
 }
 
 int mps_sample(mps_ctx* c, int64_t first_index, int n, const double* uniforms, const void* disp, const void* alpha,
@@ -1386,6 +1552,7 @@ void mps_destroy(mps_ctx* c) {
   c->marg_d.release();
   c->counts_d.release();
   c->status_d.release();
+  c->chain_meta.release();
   for (auto& r : c->recs) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
@@ -1529,6 +1696,7 @@ int mps_set_forced(mps_ctx* c, int enable) {
 int mps_set_sum_planes(mps_ctx* c, int enable) {
   if (!c) return MPS_ERR_VALIDATION;
   c->sum_planes = enable != 0;
+  c->chain_dirty = true;
   if (!c->sum_planes)
     for (auto& s : c->sites)
       if (s.gsum) {
@@ -1536,6 +1704,25 @@ int mps_set_sum_planes(mps_ctx* c, int enable) {
         s.gsum = nullptr;
       }
   return MPS_OK;
+}
+
+int mps_set_small_chain(mps_ctx* c, int enable) {
+  if (!c) return MPS_ERR_VALIDATION;
+  c->small_chain = enable != 0;
+  return MPS_OK;
+}
+
+#ifdef SC_TRACE
+int mps_debug_chain_trace(long long* out) {
+  return cudaMemcpyFromSymbol(out, sc_trace, sizeof(sc_trace)) == cudaSuccess ? MPS_OK : MPS_ERR_GENERIC;
+}
+#endif
+
+int mps_small_chain_eligible(const mps_ctx* c, int m_begin, int m_end) {
+  if (!c || m_begin < 0 || m_end > c->M || m_begin >= m_end) return 0;
+  for (int m = m_begin; m < m_end; ++m)
+    if (!c->sites[m].loaded) return 0;
+  return small_chain_ok(c, m_begin, m_end) ? 1 : 0;
 }
 
 int mps_set_lanes(mps_ctx* c, int lanes) {

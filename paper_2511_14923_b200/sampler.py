@@ -215,6 +215,16 @@ class MpsSampler:
         """Concurrent row-block chains per call (mps_set_lanes); results do not depend on it."""
         _native.check(self.L.mps_set_lanes(self.ctx, int(lanes)), self.ctx)
 
+    def set_small_chain(self, enable: bool):
+        """Whole-chain persistent cluster kernel for small chains (mps_set_small_chain); results
+        are bit-identical with it on or off."""
+        _native.check(self.L.mps_set_small_chain(self.ctx, int(bool(enable))), self.ctx)
+
+    @property
+    def small_chain_active(self) -> bool:
+        """Whether a call over this context's sites runs the small-chain kernel."""
+        return bool(self.L.mps_small_chain_eligible(self.ctx, *self.sites_range))
+
     def set_gemm_mode(self, mode: int):
         """K1 complex product: 3 (3M, default) or 4 (4M)."""
         _native.check(self.L.mps_set_gemm_mode(self.ctx, int(mode)), self.ctx)

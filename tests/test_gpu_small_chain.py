@@ -1,0 +1,132 @@
+"""The small-chain persistent cluster kernel (chain_small.cuh) against the per-mode kernels.
+
+Both paths run the same 3M DMMA k order, the same draw reduction tree and the same draw rule,
+so every output bit must agree: counts, marginals, status and the handed-off state.  The
+per-mode path is itself checked against the CPU oracle in test_gpu_parity.py; here the chain
+kernel is also checked against the oracle directly.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from oracle import mps_oracle as orc  # noqa: E402
+from paper_2511_14923_b200 import MPS, MpsSampler, MpsSamplerConfig, alpha_stream, stream_uniforms  # noqa: E402
+from paper_2511_14923_b200 import _native  # noqa: E402
+
+
+def _both(mps, fn):
+    outs = []
+    for on in (False, True):
+        with MpsSampler(mps) as eng:
+            eng.set_small_chain(on)
+            outs.append((fn(eng), eng.kernel_launches))
+    return outs
+
+
+def _same(a, b):
+    for k in ("counts", "marginals", "status"):
+        if k in a:
+            assert np.array_equal(a[k], b[k]), k
+
+
+@pytest.mark.parametrize("M,chi,D,n", [(8, 16, 4, 100), (16, 100, 10, 100), (16, 100, 10, 1000), (7, 7, 3, 37),
+                                       (9, 40, 2, 257), (5, 128, 8, 61), (3, 1, 16, 9), (1, 1, 7, 5),
+                                       (6, 64, 16, 130)])
+def test_small_chain_bit_identical_device_streams(M, chi, D, n):
+    mps = MPS(orc.random_mps(M, chi, D, seed=M + chi))
+    cfg = MpsSamplerConfig(N=n, seed=11, alpha_sigma=0.5, batch_size=n)
+    (off, l0), (on, l1) = _both(mps, lambda e: e.sample(cfg, return_marginals=True))
+    _same(off, on)
+    assert l1 < l0  # one persistent launch instead of two per mode
+
+
+@pytest.mark.parametrize("kind", ["alpha", "disp", "none", "uniforms"])
+def test_small_chain_bit_identical_host_inputs(c2_sites, kind):
+    M, D, n = 16, 10, 203
+    u = stream_uniforms(4, 17, n, M)
+    alpha = alpha_stream(4, 17, n, M, 0.5)
+    disp = None
+    if kind == "disp":
+        rng = np.random.default_rng(2)
+        z = rng.standard_normal((n, M, D, D)) + 1j * rng.standard_normal((n, M, D, D))
+        disp = np.linalg.qr(z)[0]
+    mps = MPS(c2_sites)
+
+    def run(eng):
+        if kind == "uniforms":  # host uniforms, device alpha stream
+            eng.set_streams(4, 0.5)
+        counts = np.zeros((n, M), np.int32)
+        marg = np.zeros((n, M, D))
+        status = np.zeros(n, np.uint8)
+        eng.run(17, n, counts, uniforms=u, alpha=alpha if kind == "alpha" else None,
+                disp=disp, marginals=marg, status=status)
+        return dict(counts=counts, marginals=marg, status=status)
+
+    (off, _), (on, _) = _both(mps, run)
+    _same(off, on)
+    if kind == "alpha":
+        ref = orc.sample_chain(c2_sites, u, alpha=alpha, forced=on["counts"], return_marginals=True)
+        assert np.abs(ref["marginals"] - on["marginals"]).max() <= 1e-10
+
+
+def test_small_chain_oracle_parity_c2(c2_sites):
+    n, M = 300, 16
+    cfg = MpsSamplerConfig(N=n, seed=5, alpha_sigma=0.5, batch_size=n)
+    with MpsSampler(MPS(c2_sites)) as eng:
+        res = eng.sample(cfg, return_marginals=True)
+        assert eng.kernel_launches <= 3
+    u = stream_uniforms(5, 0, n, M)
+    alpha = alpha_stream(5, 0, n, M, 0.5)
+    ref = orc.sample_chain(c2_sites, u, alpha=alpha, forced=res["counts"], return_marginals=True)
+    assert np.abs(res["marginals"] - ref["marginals"]).max() <= 1e-10
+    free = orc.sample_chain(c2_sites, u, alpha=alpha)
+    flagged = (res["status"] & _native.MPS_STATUS_FLAGGED) != 0
+    assert not (((res["counts"] != free["counts"]).any(1)) & ~flagged & ~free["flagged"]).any()
+
+
+def test_small_chain_stage_split_and_state(c2_sites):
+    """state_in / state_out through the chain kernel == the per-mode kernels, bit for bit."""
+    N, M, cut = 150, 16, 6
+    mps = MPS(c2_sites)
+    chi_cut = mps.bond_dims[cut]
+    res = []
+    for on in (False, True):
+        counts = torch.zeros((N, M), dtype=torch.int32, device="cuda")
+        marg = torch.zeros((N, M, 10), dtype=torch.float64, device="cuda")
+        status = torch.zeros(N, dtype=torch.uint8, device="cuda")
+        state = torch.zeros((N, chi_cut), dtype=torch.complex128, device="cuda")
+        out = torch.zeros((N, 1), dtype=torch.complex128, device="cuda")
+        with MpsSampler(mps, sites_range=(0, cut), layout=1) as s0, \
+                MpsSampler(mps, sites_range=(cut, M), layout=1) as s1:
+            for e in (s0, s1):
+                e.set_streams(9, 0.5)
+                e.set_small_chain(on)
+            s0.run(0, N, counts, state_out=state, marginals=marg, status=status)
+            s1.run(0, N, counts, state_in=state, state_out=out, marginals=marg, status=status)
+        torch.cuda.synchronize()
+        res.append([x.cpu().numpy() for x in (counts, marg, status, state, out)])
+    for a, b in zip(*res):
+        assert np.array_equal(a, b)
+
+
+def test_small_chain_forced(c2_sites):
+    n, M = 120, 16
+    mps = MPS(c2_sites)
+    rng = np.random.default_rng(0)
+    counts = rng.integers(0, 3, size=(n, M)).astype(np.int32)
+    counts[5, 3] = 10  # out of range: the sample fails
+    outs = []
+    for on in (False, True):
+        with MpsSampler(mps) as eng:
+            eng.set_small_chain(on)
+            outs.append(eng.evaluate(MpsSamplerConfig(N=n, seed=2, alpha_sigma=0.5, batch_size=n), counts))
+    assert np.array_equal(outs[0]["marginals"], outs[1]["marginals"])
+    assert np.array_equal(outs[0]["status"], outs[1]["status"])
+    assert np.array_equal(outs[0]["logp"], outs[1]["logp"])
+    assert outs[1]["status"][5] & _native.MPS_STATUS_FAILED
