@@ -320,8 +320,8 @@ __global__ void __launch_bounds__(SC_THREADS, 1) small_chain_kernel(const __grid
       const int jpad = (chi_r + 7) & ~7;
       // v' of j goes to row `rank` of every CTA's V tile, or to state_out after the last mode
       auto emit = [&](int j, double2 v) {
-        if (last) {
-          if (P.state_out && j < chi_r) P.state_out[(long long)b * chi_r + j] = v;
+        if (last) {  // rows past n (padding of the last group) have no state_out row
+          if (P.state_out && valid && j < chi_r) P.state_out[(long long)b * chi_r + j] = v;
           return;
         }
         const uint32_t vo = vt_addr + (uint32_t)(rank * SC_VP + j * 16);

@@ -130,3 +130,22 @@ def test_small_chain_forced(c2_sites):
     assert np.array_equal(outs[0]["status"], outs[1]["status"])
     assert np.array_equal(outs[0]["logp"], outs[1]["logp"])
     assert outs[1]["status"][5] & _native.MPS_STATUS_FAILED
+
+
+@pytest.mark.parametrize("n", [1, 37, 100])
+def test_small_chain_state_out_stays_in_bounds(c2_sites, n):
+    """Padding rows of the last 16-row group must not write past state_out's n rows (a view of a
+    larger buffer whose tail holds a sentinel)."""
+    M, cut = 16, 8
+    mps = MPS(c2_sites)
+    chi = mps.bond_dims[cut]
+    big = torch.full((n + 32, chi), 7.0 + 3.0j, dtype=torch.complex128, device="cuda")
+    counts = torch.zeros((n, M), dtype=torch.int32, device="cuda")
+    status = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    with MpsSampler(mps, sites_range=(0, cut), layout=1) as s0:
+        assert s0.small_chain_active
+        s0.set_streams(1, 0.5)
+        s0.run(0, n, counts, state_out=big[:n], status=status)
+    torch.cuda.synchronize()
+    assert bool((big[n:] == 7.0 + 3.0j).all())
+    assert bool((big[:n] != 7.0 + 3.0j).all())
