@@ -356,11 +356,6 @@ def run_pipelined(args, rank, world, local, W, K, config, dims):
     if args.gemm == "3m":
         bound_note = ("achieved counts algorithmic flops (8 per complex MAC, SURVEY.md §8d); the 3M product executes "
                       "6 on the DMMA pipe, so the executed rate is 0.75 x achieved and frac can exceed 1")
-    if small_chain:
-        kernel_name = ("small_chain_kernel (whole mode chain in one persistent launch: K1 3M FP64 DMMA + K2/K3 "
-                       "draw, 8-CTA clusters, DSMEM exchange)")
-        bound_note = ("achieved = K1 algorithmic flops over the fused kernel's whole duration (the draw and the "
-                      "cluster exchanges included); " + bound_note)
     if args.dtype == "c64":
         # tcgen05 kind::tf32 executes 3 passes (hi.hi, hi.lo, lo.hi) of the real-doubled
         # product = 24 tensor flops per complex MAC; the roofline is the dense TF32 rate,
@@ -538,7 +533,9 @@ def run_stage(args, local, W, K, config, dims):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default: 10; c1/c2, whose steps take 0.03-0.13 ms, 20000/10000 so the "
+                         "timed region spans the clock sampler's interval)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -564,7 +561,7 @@ def main():
     args = ap.parse_args()
     args.lanes = args.lanes or LANES[args.gemm]
     W = max(args.warmup, 3)
-    K = args.steps
+    K = args.steps if args.steps is not None else {"c1": 20000, "c2": 10000}.get(args.config, 10)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = 0 if ONE_GPU else int(os.environ.get("LOCAL_RANK", "0"))
@@ -589,6 +586,8 @@ def main():
             return
         steps = []
         cpu = CpuBaseline(args.config)
+        if args.steps is None:  # the c1/c2 GPU defaults (10^4 steps) would take hours on the host
+            K = min(K, 10)
         for i in range(W + K):
             v, cores, sample = cpu.run(target_s=max(1.0, 60.0 / (W + K)))
             if i >= W:
@@ -792,6 +791,11 @@ def main():
     if args.gemm == "3m":
         bound_note = ("achieved counts algorithmic flops (8 per complex MAC, SURVEY.md §8d); the 3M product executes "
                       "6 on the DMMA pipe, so the executed rate is 0.75 x achieved and frac can exceed 1")
+    if small_chain:
+        kernel_name = ("small_chain_kernel (whole mode chain in one persistent launch: K1 3M FP64 DMMA + K2/K3 "
+                       "draw, 16-CTA clusters, st.async exchange)")
+        bound_note = ("achieved = K1 algorithmic flops over the fused kernel's whole duration (the draw and the "
+                      "cluster exchanges included); " + bound_note)
     if args.dtype == "c64":
         # tcgen05 kind::tf32 executes 3 passes (hi.hi, hi.lo, lo.hi) of the real-doubled
         # product = 24 tensor flops per complex MAC; the roofline is the dense TF32 rate,
