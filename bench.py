@@ -645,7 +645,7 @@ def main():
     eng = MpsSampler(mps, device=local, stream_sites=args.stream_sites)
     eng.set_lanes(args.lanes)
     eng.set_gemm_mode({"3m": 3, "4m": 4, "ozaki": 8}[args.gemm])
-    small_chain = eng.small_chain_active  # whole chain in one persistent launch (chi <= 128)
+    small_chain = eng.small_chain_active(n)  # whole chain in one persistent launch (chi <= 128, small n)
     config["path"] = "small_chain_kernel (one launch per step)" if small_chain else "per-mode K1 + K2/K3 kernels"
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t_setup

@@ -158,14 +158,15 @@ int mps_set_gemm_config(mps_ctx* ctx, int cfg);
  * GEMMs.  Per-sample results are identical for any lane count. */
 int mps_set_lanes(mps_ctx* ctx, int lanes);
 /* Small chains (complex128, 3M product mode, every site chi_l <= 128 and chi_r * D <= 1024):
- * run the whole mode range of a call as ONE persistent kernel -- clusters of 8 CTAs each own
- * 8 sample rows, exchange C rows and the next state through distributed shared memory and never
+ * run the whole mode range of a call as ONE persistent kernel -- clusters of 16 CTAs each own
+ * 16 sample rows, exchange C rows and the next state through distributed shared memory and never
  * return to the host between modes (the two-kernels-per-mode chain is latency-bound there).
- * Results are bit-identical to the per-mode kernels.  Default on; MPS_SMALL_CHAIN=0 or
- * enable = 0 turns it off. */
-int mps_set_small_chain(mps_ctx* ctx, int enable);
-/* 1 when mps_sample_range over [m_begin, m_end) would take the small-chain kernel, else 0. */
-int mps_small_chain_eligible(const mps_ctx* ctx, int m_begin, int m_end);
+ * Results are bit-identical to the per-mode kernels.  mode 0: off; 1: whenever eligible;
+ * 2 (default): when its latency model beats the per-mode kernels' for the call's n (one to a few
+ * waves of 16-row groups).  MPS_SMALL_CHAIN=0 / =1 set modes 0 / 1 at context creation. */
+int mps_set_small_chain(mps_ctx* ctx, int mode);
+/* 1 when mps_sample_range over [m_begin, m_end) with n samples would take the small-chain kernel. */
+int mps_small_chain_eligible(const mps_ctx* ctx, int m_begin, int m_end, int n);
 /* Teacher forcing (the oracle's forced=, the pattern of gbsemu's forced path, sampler.py:394-416):
  * when enabled, mps_sample / mps_sample_range read sample b's outcome at mode m from counts
  * (an INPUT, left unchanged) instead of drawing it, and still return the normalised marginals

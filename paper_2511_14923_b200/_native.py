@@ -58,7 +58,7 @@ def _declare(L):
     L.mps_set_gemm_mode.argtypes = [c_void_p, c_int]
     L.mps_set_lanes.argtypes = [c_void_p, c_int]
     L.mps_set_small_chain.argtypes = [c_void_p, c_int]
-    L.mps_small_chain_eligible.argtypes = [c_void_p, c_int, c_int]
+    L.mps_small_chain_eligible.argtypes = [c_void_p, c_int, c_int, c_int]
     L.mps_set_sum_planes.argtypes = [c_void_p, c_int]
     L.mps_set_forced.argtypes = [c_void_p, c_int]
     L.mps_site_gemm_c64.argtypes = [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_uint64]

@@ -212,7 +212,7 @@ struct mps_ctx {
   bool forced = false;                              // teacher forcing: outcomes read from counts
   // small chains (chi <= 128, chi D <= 1024, 3M): the whole mode loop in one persistent cluster
   // kernel (chain_small.cuh); its per-site tensor maps + bond dims live in chain_meta
-  bool small_chain = true;
+  int small_chain = 2;  // 0 off, 1 always when eligible, 2 auto (when the cost model prefers it)
   bool chain_dirty = true;
   DevBuf<uint8_t> chain_meta;
   // host->HBM site streaming: 2-slot ring filled on a copy stream ahead of the GEMMs
@@ -758,13 +758,61 @@ static cudaError_t launch_c64_gemm(const float* ahi, const float* alo, const flo
 }
 
 // ---- small chains: the whole mode loop in one persistent cluster launch (chain_small.cuh) ----
-static bool small_chain_ok(const mps_ctx* c, int m_begin, int m_end) {
-  if (!c->small_chain || c->dtype != MPS_C128 || c->gemm_mode != 3) return false;
+static void (*small_chain_kernel_for(int D))(ChainArgs) {
+  return D == 10 ? small_chain_kernel<10> : D == 4 ? small_chain_kernel<4> : small_chain_kernel<0>;
+}
+
+// co-resident 16-CTA clusters of the instantiation for D (0: none fit -> per-mode kernels)
+static int small_chain_capacity(int D) {
+  void (*kern)(ChainArgs) = small_chain_kernel_for(D);
+  static std::map<void*, int> cap;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cap.find((void*)kern);
+  if (it != cap.end()) return it->second;
+  int num = 0;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SC_SMEM) == cudaSuccess &&
+      cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+    cudaLaunchConfig_t q = {};
+    q.gridDim = dim3(SC_CL * 32);
+    q.blockDim = dim3(SC_THREADS);
+    q.dynamicSmemBytes = SC_SMEM;
+    cudaLaunchAttribute a[1];
+    a[0].id = cudaLaunchAttributeClusterDimension;
+    a[0].val.clusterDim.x = SC_CL;
+    a[0].val.clusterDim.y = 1;
+    a[0].val.clusterDim.z = 1;
+    q.attrs = a;
+    q.numAttrs = 1;
+    if (cudaOccupancyMaxActiveClusters(&num, kern, &q) != cudaSuccess) num = 0;
+  }
+  cudaGetLastError();
+  cap.emplace((void*)kern, num);
+  return num;
+}
+
+// Whether a call of n samples over [m_begin, m_end) takes the small-chain kernel.  Auto mode
+// compares two latency models fitted to the C1/C2 sweeps (profiles/r01_small_chain_crossover.txt):
+// the fused kernel costs ~3.5 us + its 16-row K1 slice (~2.4 TFLOP/s per cluster) per mode and per
+// wave of co-resident clusters; the per-mode kernels ~13 us per mode or their K1 work at ~20 TFLOP/s.
+// Both paths give the same bits, so the choice only moves time.
+static bool small_chain_ok(const mps_ctx* c, int m_begin, int m_end, int n) {
+  if (!c->small_chain || c->dtype != MPS_C128 || c->gemm_mode != 3 || n < 1) return false;
   for (int m = m_begin; m < m_end; ++m) {
     const Site& s = c->sites[m];
     if (s.host || !s.chain || s.chi_l > SC_KMAX || s.chi_r * c->D > SC_NMAX) return false;
   }
-  return true;
+  const int cap = small_chain_capacity(c->D);
+  if (cap < 1) return false;
+  if (c->small_chain == 1) return true;
+  const int waves = ((n + SC_CL - 1) / SC_CL + cap - 1) / cap;
+  double t_chain = 0.0, t_mode = 0.0;
+  for (int m = m_begin; m < m_end; ++m) {
+    const double fl = 8.0 * c->sites[m].chi_l * (double)c->sites[m].chi_r * c->D;  // per sample row
+    t_chain += waves * (3.5e-6 + SC_CL * fl / 2.4e12);
+    t_mode += std::max(13e-6, n * fl / 20e12);
+  }
+  return t_chain <= t_mode;
 }
 
 // per-site chain-layout pointers and chi_0..chi_M in device memory
@@ -788,43 +836,10 @@ static cudaError_t chain_meta_upload(mps_ctx* c) {
   return e;
 }
 
-static void (*small_chain_kernel_for(int D))(ChainArgs) {
-  return D == 10 ? small_chain_kernel<10> : D == 4 ? small_chain_kernel<4> : small_chain_kernel<0>;
-}
-
 static cudaError_t launch_small_chain(mps_ctx* c, const ChainArgs& P, cudaStream_t st) {
   void (*kern)(ChainArgs) = small_chain_kernel_for(c->D);
-  static std::map<void*, int> max_clusters;  // co-resident 8-CTA clusters per instantiation
-  static std::mutex mu;
-  int mc;
-  {
-    std::lock_guard<std::mutex> lk(mu);
-    auto it = max_clusters.find((void*)kern);
-    if (it == max_clusters.end()) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SC_SMEM);
-      if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      if (e != cudaSuccess) return e;
-      cudaLaunchConfig_t q = {};
-      q.gridDim = dim3(SC_CL * 32);
-      q.blockDim = dim3(SC_THREADS);
-      q.dynamicSmemBytes = SC_SMEM;
-      cudaLaunchAttribute a[1];
-      a[0].id = cudaLaunchAttributeClusterDimension;
-      a[0].val.clusterDim.x = SC_CL;
-      a[0].val.clusterDim.y = 1;
-      a[0].val.clusterDim.z = 1;
-      q.attrs = a;
-      q.numAttrs = 1;
-      int num = 0;
-      if (cudaOccupancyMaxActiveClusters(&num, kern, &q) != cudaSuccess) {
-        cudaGetLastError();
-        num = 0;
-      }
-      it = max_clusters.emplace((void*)kern, num).first;
-    }
-    mc = it->second;
-  }
-  if (mc < 1) return cudaErrorNotSupported;  // no 16-CTA cluster fits: the caller takes the per-mode path
+  const int mc = small_chain_capacity(c->D);
+  if (mc < 1) return cudaErrorNotSupported;
   const int groups = (P.n + SC_CL - 1) / SC_CL;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(SC_CL * std::min(groups, mc));
@@ -884,7 +899,7 @@ int mps_create(int n_dev, const int* dev_ids, int layout, mps_ctx** out) {
     const char* e = getenv("MPS_DRAW_RING");
     if (e && e[0] == '0') c->draw_ring = false;
     e = getenv("MPS_SMALL_CHAIN");
-    if (e && e[0] == '0') c->small_chain = false;
+    if (e && (e[0] == '0' || e[0] == '1')) c->small_chain = e[0] - '0';
   }
   *out = c;
   return MPS_OK;
@@ -1178,7 +1193,7 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
     return MPS_OK;
   };
 
-  if (small_chain_ok(c, m_begin, m_end)) {
+  if (small_chain_ok(c, m_begin, m_end, n)) {
     CU(c, chain_meta_upload(c), "chain metadata");
     ChainArgs P;
     P.sites = reinterpret_cast<const double2* const*>(c->chain_meta.p);
@@ -1215,7 +1230,7 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
     }
     const cudaError_t le = launch_small_chain(c, P, st);
     if (le == cudaErrorNotSupported) {
-      c->small_chain = false;  // this GPU cannot host the clusters: per-mode kernels from now on
+      c->small_chain = 0;  // this GPU cannot host the clusters: per-mode kernels from now on
       if (c->profile & 1) c->event_pool.insert(c->event_pool.end(), {rg.a, rg.b});
     } else {
       CU(c, le, "small_chain launch");
@@ -1706,9 +1721,10 @@ int mps_set_sum_planes(mps_ctx* c, int enable) {
   return MPS_OK;
 }
 
-int mps_set_small_chain(mps_ctx* c, int enable) {
+int mps_set_small_chain(mps_ctx* c, int mode) {
   if (!c) return MPS_ERR_VALIDATION;
-  c->small_chain = enable != 0;
+  if (mode < 0 || mode > 2) return fail(c, MPS_ERR_VALIDATION, "small-chain mode must be 0, 1 or 2, got %d", mode);
+  c->small_chain = mode;
   return MPS_OK;
 }
 
@@ -1718,11 +1734,11 @@ int mps_debug_chain_trace(long long* out) {
 }
 #endif
 
-int mps_small_chain_eligible(const mps_ctx* c, int m_begin, int m_end) {
+int mps_small_chain_eligible(const mps_ctx* c, int m_begin, int m_end, int n) {
   if (!c || m_begin < 0 || m_end > c->M || m_begin >= m_end) return 0;
   for (int m = m_begin; m < m_end; ++m)
     if (!c->sites[m].loaded) return 0;
-  return small_chain_ok(c, m_begin, m_end) ? 1 : 0;
+  return small_chain_ok(c, m_begin, m_end, n) ? 1 : 0;
 }
 
 int mps_set_lanes(mps_ctx* c, int lanes) {

@@ -215,15 +215,14 @@ class MpsSampler:
         """Concurrent row-block chains per call (mps_set_lanes); results do not depend on it."""
         _native.check(self.L.mps_set_lanes(self.ctx, int(lanes)), self.ctx)
 
-    def set_small_chain(self, enable: bool):
-        """Whole-chain persistent cluster kernel for small chains (mps_set_small_chain); results
-        are bit-identical with it on or off."""
-        _native.check(self.L.mps_set_small_chain(self.ctx, int(bool(enable))), self.ctx)
+    def set_small_chain(self, mode):
+        """Whole-chain persistent cluster kernel for small chains (mps_set_small_chain): False / 0
+        off, True / 1 whenever eligible, 2 automatic (default).  Results are bit-identical."""
+        _native.check(self.L.mps_set_small_chain(self.ctx, int(mode)), self.ctx)
 
-    @property
-    def small_chain_active(self) -> bool:
-        """Whether a call over this context's sites runs the small-chain kernel."""
-        return bool(self.L.mps_small_chain_eligible(self.ctx, *self.sites_range))
+    def small_chain_active(self, n: int) -> bool:
+        """Whether a call of n samples over this context's sites runs the small-chain kernel."""
+        return bool(self.L.mps_small_chain_eligible(self.ctx, *self.sites_range, int(n)))
 
     def set_gemm_mode(self, mode: int):
         """K1 complex product: 3 (3M, default) or 4 (4M)."""

@@ -79,6 +79,7 @@ def test_small_chain_oracle_parity_c2(c2_sites):
     n, M = 300, 16
     cfg = MpsSamplerConfig(N=n, seed=5, alpha_sigma=0.5, batch_size=n)
     with MpsSampler(MPS(c2_sites)) as eng:
+        eng.set_small_chain(True)  # n = 300 is past the automatic crossover (two-plus waves of groups)
         res = eng.sample(cfg, return_marginals=True)
         assert eng.kernel_launches <= 3
     u = stream_uniforms(5, 0, n, M)
@@ -143,9 +144,23 @@ def test_small_chain_state_out_stays_in_bounds(c2_sites, n):
     counts = torch.zeros((n, M), dtype=torch.int32, device="cuda")
     status = torch.zeros(n, dtype=torch.uint8, device="cuda")
     with MpsSampler(mps, sites_range=(0, cut), layout=1) as s0:
-        assert s0.small_chain_active
+        assert s0.small_chain_active(n)
         s0.set_streams(1, 0.5)
         s0.run(0, n, counts, state_out=big[:n], status=status)
     torch.cuda.synchronize()
     assert bool((big[n:] == 7.0 + 3.0j).all())
     assert bool((big[:n] != 7.0 + 3.0j).all())
+
+
+def test_small_chain_auto_choice(c2_sites, c1_sites):
+    """Automatic mode takes the fused kernel for one wave of 16-row groups and the per-mode kernels
+    once the batch is large enough for them to win (both give the same bits)."""
+    with MpsSampler(MPS(c2_sites)) as eng:
+        assert eng.small_chain_active(100)
+        assert not eng.small_chain_active(1024)
+        eng.set_small_chain(True)
+        assert eng.small_chain_active(1024)
+        eng.set_small_chain(False)
+        assert not eng.small_chain_active(100)
+    with MpsSampler(MPS(c1_sites)) as eng:
+        assert eng.small_chain_active(300) and not eng.small_chain_active(4096)
