@@ -4,15 +4,15 @@
 //
 // Eligible shapes: complex128, 3M product mode, every site chi_l <= 128 and chi_r D <= 1024.
 //
-// A cluster of 8 CTAs owns a group of 8 sample rows (one DMMA row fragment) and walks every
-// mode m of [m_begin, m_end) for it without leaving the kernel:
-//   K1    CTA r computes C[rows, its 1/8 of the chi_r D columns] = V . Gamma^[m] with the 3M
+// A cluster of 16 CTAs (non-portable size) owns a group of 16 sample rows (two DMMA row fragments)
+// and walks every mode m of [m_begin, m_end) for it without leaving the kernel:
+//   K1    CTA r computes C[16 rows, its 1/16 of the chi_r D columns] = V . Gamma^[m] with the 3M
 //         DMMA product of site_gemm3m_kernel — same fragments, same k order, same epilogue
 //         expression, operand sums formed with the same DADD — so C is bit-identical to the
-//         per-mode chain.  Gamma streams through a 6-stage ring of 1-D bulk copies (one per
-//         stage) from a copy of the site pre-arranged in the ring's swizzled fragment layout
-//         (chain_site_kernel); a producer warp runs the ring ahead across modes, so the next
-//         site lands while this mode draws.
+//         per-mode chain (8 compute warps, one 8-column fragment each).  Gamma streams through a
+//         6-slot ring (2 k-stages per slot, one 1-D bulk copy per k-stage) from a copy of the
+//         site pre-arranged in the ring's swizzled fragment layout (chain_site_kernel); a producer
+//         warp runs the ring ahead across modes, so the next site lands while this mode draws.
 //   xchg  each lane st.async's its C entries straight into the shared memory of the row's owner
 //         (CTA r owns row r), completing on the owner's mbarrier: no cluster-wide barrier.
 //   K2+K3 CTA r runs displace_draw_kernel's pass 1 / draw / pass 2 on its row from shared memory
@@ -33,7 +33,7 @@ constexpr int SC_CL = 16;                         // CTAs per cluster == sample 
 constexpr int SC_MF = SC_CL / 8;                  // DMMA row fragments per group
 constexpr int SC_KMAX = 128;                      // chi_l bound
 constexpr int SC_NMAX = 1024;                     // chi_r * D bound (complex columns)
-constexpr int SC_FMAX = SC_NMAX / 8 / SC_CL;      // 8-column fragments per CTA (16)
+constexpr int SC_FMAX = SC_NMAX / 8 / SC_CL;      // 8-column fragments per CTA (8)
 constexpr int SC_FW = SC_FMAX / 8;                // per compute warp (1)
 #ifndef SC_KS_DEF  // tuning knob of tools/chain_trace.py
 #define SC_KS_DEF 2
