@@ -392,55 +392,17 @@ __global__ void __launch_bounds__(SC_THREADS, 1) small_chain_kernel(const __grid
         }
         sc_bar_compute();  // red[][] complete
         if (tid == 0) SC_STAMP(0, q, 5);
-        if (warp == 0) {
-          // displace_draw_kernel's thread-0 draw, spread over lanes k < D with every floating-point
-          // operation kept: p_k summed over warps in order, each lane forms Ptot and its own prefix
-          // run_k with the serial loop's sequence of adds, divides once; the count, the min
-          // distance (fmin is exact) and the zero-probability walk-back become ballots.
-          if (lane < D) {
-            double sacc = 0.0;
-#pragma unroll
-            for (int w = 0; w < DRAW_THREADS / 32; ++w) sacc += red[w][lane];
-            p_s[lane] = sacc;
-          }
-          __syncwarp();
-          double Ptot = 0.0, run = 0.0;
-          for (int k = 0; k < D; ++k) {
-            const double pv = p_s[k];
-            Ptot += pv;
-            if (k <= lane) run += pv;
-          }
-          const uint8_t st0 = st_s;
-          uint8_t stt = st0;
-          int ksel = -1;
-          const unsigned pos = __ballot_sync(0xffffffffu, lane < D && p_s[lane] > 0.0);
-          if (!(Ptot > 0.0) || !isfinite(Ptot)) {
-            stt |= ST_FAILED;
-          } else if (A.forced) {
-            ksel = __shfl_sync(0xffffffffu, k_pref, 0);
-            if (ksel < 0 || ksel >= D) {
-              stt |= ST_FAILED;
-              ksel = -1;
-            }
-          } else {
-            const double u = __shfl_sync(0xffffffffu, u_pref, 0);
-            const double cdf = (lane == D - 1) ? 1.0 : run / Ptot;
-            const int cnt = __popc(__ballot_sync(0xffffffffu, lane < D && cdf <= u));
-            double mind = (lane < D - 1) ? fabs(cdf - u) : 1e300;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) mind = fmin(mind, __shfl_xor_sync(0xffffffffu, mind, o));
-            ksel = cnt < D - 1 ? cnt : D - 1;
-            const unsigned below = pos & ((2u << ksel) - 1u);  // while (ksel > 0 && !(p[ksel] > 0)) --ksel
-            ksel = below ? 31 - __clz(below) : 0;
-            if (mind <= A.tie_eps) stt |= ST_FLAGGED;
-          }
-          if (A.marg && lane < D) A.marg[crow * D + lane] = (ksel >= 0) ? p_s[lane] / Ptot : 0.0;
+        if (warp == 0) {  // the draw (draw_row_warp, as displace_draw_kernel; u / forced k prefetched)
+          const RowDraw r = draw_row_warp(red, DRAW_THREADS / 32, p_s, D, st_s, A.forced != 0,
+                                          __shfl_sync(0xffffffffu, k_pref, 0), __shfl_sync(0xffffffffu, u_pref, 0),
+                                          A.tie_eps);
+          if (A.marg && lane < D) A.marg[crow * D + lane] = (r.k >= 0) ? p_s[lane] / r.Ptot : 0.0;
           if (lane == 0) {
-            st_s = stt;
-            A.status[b] = stt;
-            if (!A.forced) A.counts[crow] = ksel;
-            k_s = ksel;
-            scale_s = (ksel >= 0 && p_s[ksel] > 0.0) ? 1.0 / sqrt(p_s[ksel]) : 0.0;
+            st_s = r.status;
+            A.status[b] = r.status;
+            if (!A.forced) A.counts[crow] = r.k;
+            k_s = r.k;
+            scale_s = (r.k >= 0 && p_s[r.k] > 0.0) ? 1.0 / sqrt(p_s[r.k]) : 0.0;
           }
         }
         sc_bar_compute();

@@ -250,6 +250,57 @@ __device__ __forceinline__ float2 disp_row_f(const float2* T, int D, int k, cons
   return e;
 }
 
+// The draw of one sample row (the sampler.py:692-697 rule; teacher-forced: the given outcome),
+// run by ALL 32 lanes of one warp.  Every floating-point operation of the serial form is kept:
+// lane k < D sums p_k over the row's warp partials red[w][k] in warp order, every lane forms Ptot
+// and its own prefix run_k with the serial loop's sequence of adds and divides once; the count,
+// the min distance to a CDF boundary (fmin is exact) and the zero-probability walk-back
+// (while (k > 0 && !(p[k] > 0)) --k) become ballots.  Writes p_s[0..D); returns the outcome
+// (-1: failed), the updated status bits and Ptot in every lane.
+struct RowDraw {
+  int k;
+  uint8_t status;
+  double Ptot;
+};
+__device__ inline RowDraw draw_row_warp(const double (*red)[DMAX], int nwarps, double* p_s, int D, uint8_t st0,
+                                        bool forced, int k_forced, double u, double tie_eps) {
+  const int lane = threadIdx.x & 31;
+  if (lane < D) {
+    double sacc = 0.0;
+    for (int w = 0; w < nwarps; ++w) sacc += red[w][lane];
+    p_s[lane] = sacc;
+  }
+  __syncwarp();
+  double Ptot = 0.0, run = 0.0;
+  for (int k = 0; k < D; ++k) {
+    const double pv = p_s[k];
+    Ptot += pv;
+    if (k <= lane) run += pv;
+  }
+  RowDraw r{-1, st0, Ptot};
+  const unsigned pos = __ballot_sync(0xffffffffu, lane < D && p_s[lane] > 0.0);
+  if (!(Ptot > 0.0) || !isfinite(Ptot)) {
+    r.status |= ST_FAILED;
+  } else if (forced) {
+    r.k = k_forced;
+    if (r.k < 0 || r.k >= D) {
+      r.status |= ST_FAILED;
+      r.k = -1;
+    }
+  } else {
+    const double cdf = (lane == D - 1) ? 1.0 : run / Ptot;
+    const int cnt = __popc(__ballot_sync(0xffffffffu, lane < D && cdf <= u));
+    double mind = (lane < D - 1) ? fabs(cdf - u) : 1e300;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mind = fmin(mind, __shfl_xor_sync(0xffffffffu, mind, o));
+    const int kc = cnt < D - 1 ? cnt : D - 1;
+    const unsigned below = pos & ((2u << kc) - 1u);
+    r.k = below ? 31 - __clz(below) : 0;
+    if (mind <= tie_eps) r.status |= ST_FLAGGED;
+  }
+  return r;
+}
+
 // RING: the C row streams through a 2-slot shared-memory ring of 128-j chunks filled by 1-D TMA
 // bulk copies (mbarrier per slot), for both passes; loads in flight cost no registers, so the
 // kernel stops being bound on global-load latency.  Each thread still owns j = tid + 128 c, so
@@ -402,59 +453,24 @@ __global__ void __launch_bounds__(DRAW_THREADS, C64 ? 8 : 4)
     if (lane == 0) red[warp][k] = (double)v;
   }
   __syncthreads();
-  if (tid < D) {  // fixed order over warps
-    double s = 0.0;
-#pragma unroll
-    for (int w = 0; w < DRAW_THREADS / 32; ++w) s += red[w][tid];
-    p_s[tid] = s;
-  }
-  __syncthreads();
-
-  // ---- draw (sampler.py:692-697 rule on the normalised cdf) ----
-  if (tid == 0) {
-    double P = 0.0;
-    for (int k = 0; k < D; ++k) P += p_s[k];
-    uint8_t st = A.status[b];
-    int ksel = -1;
-    if (!(P > 0.0) || !isfinite(P)) {
-      st |= ST_FAILED;
-    } else if (A.forced) {
-      // teacher forcing (the oracle's forced=, sampler.py:394-416): follow the given outcome; an
-      // out-of-range outcome fails the sample, a zero-probability one zeroes the state (the next
-      // mode then fails), exactly as the oracle's chain does
-      ksel = A.counts[crow];
-      if (ksel < 0 || ksel >= D) {
-        st |= ST_FAILED;
-        ksel = -1;
-      }
-    } else {
-      const double u = A.u ? A.u[(long long)b * A.ld_u + A.m]
-                           : philox_double(numpy_key0(A.seed), gi / 64, (gi % 64) * (uint64_t)A.M + A.m);
-      double run = 0.0, mind = 1e300;
-      int cnt = 0;
-      for (int k = 0; k < D; ++k) {
-        run += p_s[k];
-        const double cdf = (k == D - 1) ? 1.0 : run / P;
-        cnt += (cdf <= u);
-        if (k < D - 1) mind = fmin(mind, fabs(cdf - u));
-      }
-      ksel = cnt < D - 1 ? cnt : D - 1;
-      while (ksel > 0 && !(p_s[ksel] > 0.0)) --ksel;
-      if (mind <= A.tie_eps) st |= ST_FLAGGED;
+  if (warp == 0) {  // the draw, on warp 0 (draw_row_warp: the serial rule's exact operations)
+    const long long ui = (long long)b * A.ld_u + A.m;
+    const double u = A.forced ? 0.0
+                     : A.u   ? A.u[ui]
+                             : philox_double(numpy_key0(A.seed), gi / 64, (gi % 64) * (uint64_t)A.M + A.m);
+    const RowDraw r = draw_row_warp(red, DRAW_THREADS / 32, p_s, D, A.status[b], A.forced != 0,
+                                    A.forced ? A.counts[crow] : 0, u, A.tie_eps);
+    if (A.marg && lane < D) A.marg[crow * D + lane] = (r.k >= 0) ? p_s[lane] / r.Ptot : 0.0;
+    if (lane == 0) {
+      A.status[b] = r.status;
+      if (!A.forced) A.counts[crow] = r.k;
+      k_s = r.k;
+      scale_s = (r.k >= 0 && p_s[r.k] > 0.0) ? 1.0 / sqrt(p_s[r.k]) : 0.0;
     }
-    A.status[b] = st;
-    if (!A.forced) A.counts[crow] = ksel;
-    k_s = ksel;
-    scale_s = (ksel >= 0 && p_s[ksel] > 0.0) ? 1.0 / sqrt(p_s[ksel]) : 0.0;
-    red[0][0] = P;  // red[] is free again: its reads finished before the last barrier
   }
   __syncthreads();
   const int ks = k_s;
   const double scale = scale_s;
-  if (A.marg && tid < D) {
-    const double P = red[0][0];
-    A.marg[crow * D + tid] = (ks >= 0) ? p_s[tid] / P : 0.0;
-  }
 
   // ---- pass 2: gather + renormalise ----
   for (int cidx = 0; cidx < nchunks; ++cidx) {

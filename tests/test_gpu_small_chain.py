@@ -37,7 +37,7 @@ def _same(a, b):
 
 @pytest.mark.parametrize("M,chi,D,n", [(8, 16, 4, 100), (16, 100, 10, 100), (16, 100, 10, 1000), (7, 7, 3, 37),
                                        (9, 40, 2, 257), (5, 128, 8, 61), (3, 1, 16, 9), (1, 1, 7, 5),
-                                       (6, 64, 16, 130)])
+                                       (6, 64, 16, 130), (5, 128, 1, 33), (4, 9, 7, 1000)])
 def test_small_chain_bit_identical_device_streams(M, chi, D, n):
     mps = MPS(orc.random_mps(M, chi, D, seed=M + chi))
     cfg = MpsSamplerConfig(N=n, seed=11, alpha_sigma=0.5, batch_size=n)
