@@ -1,6 +1,7 @@
 """Small end-to-end run for compute-sanitizer (one tool per gpurun call):
 C1 and C2-sized chains in complex128 (3M with sum planes, 4M, lanes 1 and 2) and complex64,
-a pipeline-stage split, and every K1 tile config on a ragged shape."""
+a pipeline-stage split, the small-chain kernel forced on a ragged stage split (state_in / state_out
+views of larger buffers), and every K1 tile config on a ragged shape."""
 import sys
 from pathlib import Path
 
@@ -24,6 +25,21 @@ for M, chi, D, N, n in ((8, 16, 4, 130, 100), (6, 100, 10, 70, 70)):
     with MpsSampler(MPS(sites)) as eng:
         eng.set_gemm_mode(4)
         eng.sample(MpsSamplerConfig(N=N, seed=3, alpha_sigma=0.5, batch_size=n))
+sites = orc.random_mps(9, 100, 10, seed=2)
+for n in (37, 100):
+    big_in = torch.zeros((n + 16, 100), dtype=torch.complex128, device="cuda")
+    big_out = torch.zeros((n + 16, 100), dtype=torch.complex128, device="cuda")
+    counts = torch.zeros((n, 9), dtype=torch.int32, device="cuda")
+    status = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    with MpsSampler(MPS(sites), sites_range=(0, 4), layout=1) as s0, \
+            MpsSampler(MPS(sites), sites_range=(4, 9), layout=1) as s1:
+        for e in (s0, s1):
+            e.set_small_chain(1)
+            e.set_streams(5, 0.5)
+        s0.run(0, n, counts, state_out=big_in[:n], status=status)
+        s1.run(0, n, counts, state_in=big_in[:n], status=status)
+    torch.cuda.synchronize()
+    assert bool((big_in[n:] == 0).all())
 g = torch.Generator(device="cuda").manual_seed(0)
 V = torch.randn(37, 21, dtype=torch.complex128, device="cuda", generator=g)
 G = torch.randn(21, 45, dtype=torch.complex128, device="cuda", generator=g)
