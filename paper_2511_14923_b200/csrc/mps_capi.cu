@@ -18,6 +18,7 @@
 #include <mutex>
 #include <tuple>
 #include <cstring>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -320,6 +321,23 @@ static void (*draw_kernel_for(int D, bool c64, bool ring))(DrawArgs) {
                                                                    : displace_draw_kernel<0, false, false>;
 }
 
+// Kernel attributes bind to the current device's copy of a kernel: set each (kernel, device, attr)
+// once, so a process driving several GPUs configures every one of them.
+static cudaError_t set_attr_once(const void* kern, cudaFuncAttribute attr, int value) {
+  static std::set<std::tuple<const void*, int, int>> done;
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count(std::make_tuple(kern, dev, (int)attr))) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(kern, attr, value);
+  if (e == cudaSuccess) done.insert(std::make_tuple(kern, dev, (int)attr));
+  return e;
+}
+static cudaError_t set_smem_once(const void* kern, int bytes) {
+  return set_attr_once(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
 // K1 operands of one launch.  Vs / tgs (the sum planes) may be null: the 3M kernel then
 // forms the sums with DADDs; both paths give bit-identical C.
 struct GemmOps {
@@ -338,28 +356,17 @@ struct GemmOps {
 // every bit of C) is config-independent; the autotuner only changes speed.
 template <class Cfg, int MODE, bool SUMS>
 static cudaError_t launch_cfg_impl(const GemmOps& o, cudaStream_t st) {
-  static bool configured = false;
   CUtensorMap tv, tvs;
   if (!make_tmap(&tv, o.V, o.n, 2 * (uint64_t)o.K, 16 * (uint64_t)o.K, Cfg::BM)) return cudaErrorInvalidValue;
   dim3 grid((o.n + Cfg::BM - 1) / Cfg::BM, (2 * o.N + Cfg::BN_R - 1) / Cfg::BN_R);
   const int KT = (o.K + Cfg::BK_C - 1) / Cfg::BK_C;
   if constexpr (MODE == 4) {
-    if (!configured) {
-      cudaError_t e = cudaFuncSetAttribute(site_gemm_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           Cfg::SMEM_BYTES);
-      if (e != cudaSuccess) return e;
-      configured = true;
-    }
+    if (cudaError_t e = set_smem_once((const void*)site_gemm_kernel<Cfg>, Cfg::SMEM_BYTES)) return e;
     return launch_pdl(site_gemm_kernel<Cfg>, grid, dim3(Cfg::THREADS), Cfg::SMEM_BYTES, st, tv, *o.tg, o.C, o.n, o.N,
                       KT, o.ldc);
   } else {
     using S = Sums3M<Cfg, SUMS>;
-    if (!configured) {
-      cudaError_t e = cudaFuncSetAttribute(site_gemm3m_kernel<Cfg, SUMS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           S::SMEM_BYTES);
-      if (e != cudaSuccess) return e;
-      configured = true;
-    }
+    if (cudaError_t e = set_smem_once((const void*)site_gemm3m_kernel<Cfg, SUMS>, S::SMEM_BYTES)) return e;
     if constexpr (SUMS) {
       if (!make_tmap(&tvs, o.Vs, o.n, (uint64_t)o.K, 8 * (uint64_t)o.ld_vs, Cfg::BM, 8)) return cudaErrorInvalidValue;
     } else {
@@ -523,13 +530,7 @@ template <int S, int CM, int CN>
 static cudaError_t launch_ozaki_cl(const int8_t* a_planes, int n_pad, const int* ea, const int8_t* b_planes, int b_pad,
                                    const int* eb, int ld, double2* C, int n, int K, int N, cudaStream_t st) {
   using Cfg = OzCfg<S, CM, CN>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(ozaki_gemm_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Cfg::SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  if (cudaError_t e = set_smem_once((const void*)ozaki_gemm_kernel<Cfg>, Cfg::SMEM_BYTES)) return e;
   // grid padded to whole clusters: padding CTAs read padding rows (n_pad, b_pad are multiples of 256) and
   // store nothing
   dim3 grid(round_up((n + Cfg::BM - 1) / Cfg::BM, CM), round_up((2 * N + Cfg::BN - 1) / Cfg::BN, CN));
@@ -564,13 +565,7 @@ template <int S, int MP>
 static cudaError_t launch_ozaki2(const int8_t* a_planes, int n_pad, const int* ea, const int8_t* b_planes, int b_pad,
                                  const int* eb, int ld, double2* C, int n, int K, int N, cudaStream_t st) {
   using Cfg = Oz2Cfg<S, MP>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(ozaki2_gemm_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Cfg::SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  if (cudaError_t e = set_smem_once((const void*)ozaki2_gemm_kernel<Cfg>, Cfg::SMEM_BYTES)) return e;
   const int mtiles = round_up((n + Cfg::BM - 1) / Cfg::BM, MP);
   dim3 grid(2 * mtiles, (2 * N + Cfg::BN - 1) / Cfg::BN);
   const int KS = ld / Cfg::BK;
@@ -672,13 +667,7 @@ using C64P128 = C64Cfg<128, 3>;
 template <class Cfg>
 static cudaError_t launch_c64_persistent(const float* ahi, const float* alo, const float* bhi, const float* blo, int ld,
                                          float* C, int n, int K, int N, long long ldc_f, cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(c64_gemm_persistent_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Cfg::SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  if (cudaError_t e = set_smem_once((const void*)c64_gemm_persistent_kernel<Cfg>, Cfg::SMEM_BYTES)) return e;
   CUtensorMap tah, tal, tbh, tbl;
   const uint64_t cols = 2 * (uint64_t)K, pitch = 4 * (uint64_t)ld;
   if (!make_tmap(&tah, ahi, n, cols, pitch, Cfg::BM, 32, true) || !make_tmap(&tal, alo, n, cols, pitch, Cfg::BM, 32, true) ||
@@ -714,16 +703,8 @@ static cudaError_t launch_c64_gemm(const float* ahi, const float* alo, const flo
   if (choice == 1) return launch_c64_persistent<C64P256>(ahi, alo, bhi, blo, ld, C, n, K, N, ldc_f, st);
   if (choice == 2) return launch_c64_persistent<C64P128>(ahi, alo, bhi, blo, ld, C, n, K, N, ldc_f, st);
   using Cfg = C64Big;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(c64_gemm_kernel<Cfg, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Cfg::SMEM_BYTES);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(c64_gemm_kernel<Cfg, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               Cfg::SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  if (cudaError_t e = set_smem_once((const void*)c64_gemm_kernel<Cfg, false>, Cfg::SMEM_BYTES)) return e;
+  if (cudaError_t e = set_smem_once((const void*)c64_gemm_kernel<Cfg, true>, Cfg::SMEM_BYTES)) return e;
   const int mtiles = (n + Cfg::BM - 1) / Cfg::BM;
   const bool mc = c64_multicast_enabled() && mtiles >= 2;
   CUtensorMap tah, tal, tbh, tbl;
@@ -762,17 +743,21 @@ static void (*small_chain_kernel_for(int D))(ChainArgs) {
   return D == 10 ? small_chain_kernel<10> : D == 4 ? small_chain_kernel<4> : small_chain_kernel<0>;
 }
 
-// co-resident 16-CTA clusters of the instantiation for D (0: none fit -> per-mode kernels)
+// co-resident 16-CTA clusters of the instantiation for D on the current device (0: none fit)
 static int small_chain_capacity(int D) {
   void (*kern)(ChainArgs) = small_chain_kernel_for(D);
-  static std::map<void*, int> cap;
+  static std::map<std::pair<void*, int>, int> cap;
   static std::mutex mu;
-  std::lock_guard<std::mutex> lk(mu);
-  auto it = cap.find((void*)kern);
-  if (it != cap.end()) return it->second;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cap.find({(void*)kern, dev});
+    if (it != cap.end()) return it->second;
+  }
   int num = 0;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SC_SMEM) == cudaSuccess &&
-      cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+  if (set_smem_once((const void*)kern, SC_SMEM) == cudaSuccess &&
+      set_attr_once((const void*)kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
     cudaLaunchConfig_t q = {};
     q.gridDim = dim3(SC_CL * 32);
     q.blockDim = dim3(SC_THREADS);
@@ -787,7 +772,8 @@ static int small_chain_capacity(int D) {
     if (cudaOccupancyMaxActiveClusters(&num, kern, &q) != cudaSuccess) num = 0;
   }
   cudaGetLastError();
-  cap.emplace((void*)kern, num);
+  std::lock_guard<std::mutex> lk(mu);
+  cap[{(void*)kern, dev}] = num;
   return num;
 }
 
@@ -1440,16 +1426,7 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
         const bool ring = c->draw_ring && ((size_t)N * esz) % 16 == 0;
         const size_t ring_bytes = ring ? 2 * (size_t)DRAW_THREADS * D * esz : 0;
         void (*dk)(DrawArgs) = draw_kernel_for(D, c64, ring);
-        if (ring) {
-          static bool attr_set[2][3] = {};
-          const int di = D == 10 ? 0 : D == 4 ? 1 : 2;
-          if (!attr_set[c64][di]) {
-            CU(c, cudaFuncSetAttribute(dk, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       2 * DRAW_THREADS * DMAX * 16),
-               "draw ring smem");
-            attr_set[c64][di] = true;
-          }
-        }
+        if (ring) CU(c, set_smem_once((const void*)dk, 2 * DRAW_THREADS * DMAX * 16), "draw ring smem");
         CU(c, launch_pdl(dk, dim3(nl), dim3(DRAW_THREADS), ring_bytes, lst[l], a), "displace_draw launch");
       }
       c->launches++;
