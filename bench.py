@@ -366,12 +366,13 @@ def run_pipelined(args, rank, world, local, W, K, config, dims):
         kernel_name = "c64_gemm_kernel (K1, tcgen05 kind::tf32, 3xTF32)"
         bound_note = "achieved counts executed tensor flops (3 passes x 8 per complex MAC)"
     elif args.gemm == "ozaki":
-        # 28 int8 digit products (diagonals i + j < 7) of the real-doubled product per complex MAC;
+        # S(S+1)/2 int8 digit products (diagonals i + j < S; 28 at S = 7) of the real-doubled product per complex MAC;
         # the roofline is the measured kind::i8 issue rate
-        achieved, peak = 28.0 * achieved, 4510.5
+        achieved, peak = args.oz_digits * (args.oz_digits + 1) / 2.0 * achieved, 4510.5
         peak_src = "profiles/r01_umma_probe.jsonl (kind::i8 M=128 N=128 issue-rate probe), TOP/s"
-        kernel_name = "ozaki2_gemm_kernel (K1, complex128 emulated on INT8 tcgen05, 7 digits, CTA pairs)"
-        bound_note = "achieved counts executed int8 tensor ops (28 digit products x 8 per complex MAC)"
+        kernel_name = f"ozaki2_gemm_kernel (K1, complex128 emulated on INT8 tcgen05, {args.oz_digits} digits, CTA pairs)"
+        bound_note = (f"achieved counts executed int8 tensor ops ({args.oz_digits * (args.oz_digits + 1) // 2} digit "
+                      "products x 8 per complex MAC)")
     step_flops = sum(site_flops(dims, D, n))
     whole_tf = K * step_flops / (ms / 1e3) / 1e12
     ok = not bool((status[W:] & 1).any().item())
@@ -431,6 +432,7 @@ def run_stage(args, local, W, K, config, dims):
     eng = MpsSampler(mps, device=local, sites_range=(mb, me), layout=1)
     eng.set_lanes(args.lanes)
     eng.set_gemm_mode({"3m": 3, "4m": 4, "ozaki": 8}[args.gemm])
+    eng.set_ozaki_digits(args.oz_digits)
     eng.set_streams(0, sigma)
     cdt = torch.complex64 if args.dtype == "c64" else torch.complex128
     gen = torch.Generator(device=dev)
@@ -496,9 +498,10 @@ def run_stage(args, local, W, K, config, dims):
         peak_src = f"dense TF32 = 1/2 of {src} bf16 {bf16:.0f} TFLOP/s"
         kernel_name = "c64_gemm_kernel (K1, tcgen05 kind::tf32, 3xTF32; achieved = executed tensor flops)"
     elif args.gemm == "ozaki":
-        achieved, peak = 28.0 * achieved, 4510.5
+        achieved, peak = args.oz_digits * (args.oz_digits + 1) / 2.0 * achieved, 4510.5
         peak_src = "profiles/r01_umma_probe.jsonl (kind::i8 M=128 N=128 issue-rate probe), TOP/s"
-        kernel_name = "ozaki2_gemm_kernel (K1, INT8 tcgen05; achieved = executed int8 ops, 28 per algorithmic flop)"
+        kernel_name = (f"ozaki2_gemm_kernel (K1, INT8 tcgen05; achieved = executed int8 ops, "
+                       f"{args.oz_digits * (args.oz_digits + 1) // 2} per algorithmic flop)")
     stage_flops = sum(site_flops(dims, D, n)[mb:me])
     value = K * n / (ms / 1e3)
     T = (N_total + n - 1) // n
@@ -546,6 +549,8 @@ def main():
                     help="keep the sites in pinned host memory and stream them into HBM every step")
     ap.add_argument("--gemm", default="3m", choices=["3m", "4m", "ozaki"],
                     help="complex128 K1: 3M / 4M on the FP64 DMMA pipe, or fp64 emulated on INT8 tcgen05")
+    ap.add_argument("--oz-digits", type=int, default=7, choices=[5, 6, 7],
+                    help="--gemm ozaki: digits of 7 bits per operand (7: ~1e-13 of the row scales, 6: ~1e-11)")
     ap.add_argument("--dtype", default="c128", choices=["c128", "c64"],
                     help="c64: complex64 chain, K1 on tcgen05 (3xTF32), parity 1e-4")
     ap.add_argument("--layout", default="auto", choices=["auto", "sharded", "pipelined"],
@@ -572,7 +577,7 @@ def main():
 
     dims = bond_dims(M, chi, D)
     config = {"workload": f"{args.config}: {desc}", "M": M, "chi": chi, "D": D, "n": n, "lanes": args.lanes,
-              "gemm": args.gemm,
+              "gemm": args.gemm if args.gemm != "ozaki" else f"ozaki (S={args.oz_digits})",
               "sites_in": "host, streamed per step" if args.stream_sites else "HBM",
               "alpha": "CN(0,%.3g)" % (sigma * sigma), "sites": "random row-orthonormal, seed 0",
               "layout": "sample-sharded" if world > 1 else "single GPU",
@@ -645,6 +650,7 @@ def main():
     eng = MpsSampler(mps, device=local, stream_sites=args.stream_sites)
     eng.set_lanes(args.lanes)
     eng.set_gemm_mode({"3m": 3, "4m": 4, "ozaki": 8}[args.gemm])
+    eng.set_ozaki_digits(args.oz_digits)
     small_chain = eng.small_chain_active(n)  # whole chain in one persistent launch (chi <= 128, small n)
     config["path"] = "small_chain_kernel (one launch per step)" if small_chain else "per-mode K1 + K2/K3 kernels"
     torch.cuda.synchronize()
@@ -806,12 +812,13 @@ def main():
         kernel_name = "c64_gemm_kernel (K1, tcgen05 kind::tf32, 3xTF32)"
         bound_note = "achieved counts executed tensor flops (3 passes x 8 per complex MAC)"
     elif args.gemm == "ozaki":
-        # 28 int8 digit products (diagonals i + j < 7) of the real-doubled product per complex MAC;
+        # S(S+1)/2 int8 digit products (diagonals i + j < S; 28 at S = 7) of the real-doubled product per complex MAC;
         # the roofline is the measured kind::i8 issue rate
-        achieved, peak = 28.0 * achieved, 4510.5
+        achieved, peak = args.oz_digits * (args.oz_digits + 1) / 2.0 * achieved, 4510.5
         peak_src = "profiles/r01_umma_probe.jsonl (kind::i8 M=128 N=128 issue-rate probe), TOP/s"
-        kernel_name = "ozaki2_gemm_kernel (K1, complex128 emulated on INT8 tcgen05, 7 digits, CTA pairs)"
-        bound_note = "achieved counts executed int8 tensor ops (28 digit products x 8 per complex MAC)"
+        kernel_name = f"ozaki2_gemm_kernel (K1, complex128 emulated on INT8 tcgen05, {args.oz_digits} digits, CTA pairs)"
+        bound_note = (f"achieved counts executed int8 tensor ops ({args.oz_digits * (args.oz_digits + 1) // 2} digit "
+                      "products x 8 per complex MAC)")
     step_flops = sum(site_flops(dims, D, n))
     whole_tf = world * K * step_flops / (ms / 1e3) / 1e12
 

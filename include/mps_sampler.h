@@ -184,6 +184,9 @@ int mps_set_sum_planes(mps_ctx* ctx, int enable);
  * ~1e-13 of the row scales; opt-in).  Results of the modes differ at rounding level; each is
  * deterministic across batch sizes and GPU counts. */
 int mps_set_gemm_mode(mps_ctx* ctx, int mode);
+/* Digits per operand of gemm mode 8 (Ozaki): 7 (default, ~1e-13 of the row scales), 6 (25% fewer
+ * INT8 products, ~1e-11) or 5. */
+int mps_set_ozaki_digits(mps_ctx* ctx, int S);
 /* complex128 K1 emulated on the INT8 tensor cores (Ozaki scheme with S = 5..7 digits):
  * C (n x N) = V (n x K) . G (K x N), all complex128.  Test/benchmark entry (slices per call). */
 int mps_site_gemm_ozaki(const void* V, const void* G, void* C, int n, int K, int N, int S, uint64_t stream);

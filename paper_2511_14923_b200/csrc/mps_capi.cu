@@ -1734,6 +1734,13 @@ int mps_set_gemm_mode(mps_ctx* c, int mode) {
   return MPS_OK;
 }
 
+int mps_set_ozaki_digits(mps_ctx* c, int S) {
+  if (!c) return MPS_ERR_VALIDATION;
+  if (S < 5 || S > OZ_MAX_S) return fail(c, MPS_ERR_VALIDATION, "Ozaki digits must lie in [5, %d], got %d", OZ_MAX_S, S);
+  c->oz_S = S;  // the sites' digit planes are re-sliced on the next gemm-mode-8 call
+  return MPS_OK;
+}
+
 int mps_set_gemm_config(mps_ctx* c, int cfg) {
   if (!c) return MPS_ERR_VALIDATION;
   if (cfg < -2 || cfg >= N_GEMM_CFGS) return fail(c, MPS_ERR_VALIDATION, "gemm config %d outside [-2, %d)", cfg,

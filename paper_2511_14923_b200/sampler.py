@@ -224,6 +224,10 @@ class MpsSampler:
         """Whether a call of n samples over this context's sites runs the small-chain kernel."""
         return bool(self.L.mps_small_chain_eligible(self.ctx, *self.sites_range, int(n)))
 
+    def set_ozaki_digits(self, S: int):
+        """Digits per operand of gemm mode 8 (mps_set_ozaki_digits): 7 (default), 6 or 5."""
+        _native.check(self.L.mps_set_ozaki_digits(self.ctx, int(S)), self.ctx)
+
     def set_gemm_mode(self, mode: int):
         """K1 complex product: 3 (3M, default) or 4 (4M)."""
         _native.check(self.L.mps_set_gemm_mode(self.ctx, int(mode)), self.ctx)

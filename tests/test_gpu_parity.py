@@ -457,17 +457,19 @@ def chi4000_sites():
     return orc.random_mps(8, 4000, 10, seed=11)
 
 
-@pytest.mark.parametrize("mode", [3, 8])
-def test_chi4000_chain_parity(mode, chi4000_sites):
+@pytest.mark.parametrize("mode,digits", [(3, 7), (8, 7), (8, 6)])
+def test_chi4000_chain_parity(mode, digits, chi4000_sites):
     """The C4 bond dimension (chi = 4000: a 40000-column site, the global-memory draw path) in both
-    complex128 K1 products, against the oracle."""
+    complex128 K1 products (the INT8 one with 7 and with 6 Ozaki digits), against the oracle."""
     M, D, N = 8, 10, 48
     sites = chi4000_sites
     cfg = MpsSamplerConfig(N=N, seed=11, alpha_sigma=0.7, batch_size=N)
     with MpsSampler(MPS(sites)) as eng:
         eng.set_gemm_mode(mode)
+        eng.set_ozaki_digits(digits)
         res = eng.sample(cfg, return_marginals=True)
-    _check_parity(sites, res, stream_uniforms(11, 0, N, M), alpha=alpha_stream(11, 0, N, M, 0.7))
+    err = _check_parity(sites, res, stream_uniforms(11, 0, N, M), alpha=alpha_stream(11, 0, N, M, 0.7))
+    print(f"chi=4000 mode {mode} digits {digits}: max |dp| = {err:.2e}")
 
 
 # ------------------------------------------------------------------ complex64 (tcgen05)
@@ -648,12 +650,14 @@ def test_chain_parity_ozaki(c2_sites):
     assert err < 1e-12
 
 
-def test_ozaki_chi1000_and_invariance():
+@pytest.mark.parametrize("digits", [7, 6])
+def test_ozaki_chi1000_and_invariance(digits):
     M, chi, D, N = 5, 1000, 10, 192
     sites = orc.random_mps(M, chi, D, seed=9)
     outs = []
     with MpsSampler(MPS(sites)) as eng:
         eng.set_gemm_mode(8)
+        eng.set_ozaki_digits(digits)
         for lanes, B in ((1, 192), (2, 192), (1, 64)):
             eng.set_lanes(lanes)
             outs.append(eng.sample(MpsSamplerConfig(N=N, seed=9, alpha_sigma=0.7, batch_size=B),
