@@ -53,6 +53,8 @@ def main():
         nxt = c[q + 1, 0] if q + 1 < a.M else c[q, 3]
         print(f"{q:4d} {c[q,1]-c[q,0]:6d} {c[q,2]-c[q,1]:5d} {c[q,3]-c[q,2]:5d} {nxt-c[q,3]:5d}")
     print("total cycles", c[a.M - 1, 3] - c[0, 0])
+    print("of which waiting for the previous mode's states (V) before the K1 loop:",
+          [int(c[q, 7] - c[q, 0]) for q in range(a.M)])
     print("GEMM cycles thread 0 spent waiting for ring data, per mode:", list(buf[1, :a.M, 0] // 3))
     q = min(5, a.M - 2)
     print(f"draw of mode {q}: pass1 {c[q,4]-c[q,2]}  reduce {c[q,5]-c[q,4]}  draw {c[q,6]-c[q,5]}  "
