@@ -238,6 +238,7 @@ __global__ void __launch_bounds__(SC_THREADS, 1) small_chain_kernel(const __grid
       }
       sc_bar_compute();
 
+      if (tid == 0) SC_STAMP(0, q, 7);
       // ---- K1: 3M DMMA over this CTA's fragments (site_gemm3m_kernel's inner loop, DADD sums) ----
       const int fbase = warp * SC_FW;
       double t1[SC_MF][SC_FW][2], t2[SC_MF][SC_FW][2], t3[SC_MF][SC_FW][2];
