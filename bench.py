@@ -351,7 +351,7 @@ def run_pipelined(args, rank, world, local, W, K, config, dims):
     gemm_flops_avg = prof["gemm_flops"] / max(prof["gemm_launches"], 1)
     achieved = gemm_flops_avg / (gemm_ms_avg / 1e3) / 1e12 if gemm_ms_avg > 0 else 0.0
     kernel_name = {"3m": "site_gemm3m_kernel (K1, FP64 DMMA, 3M)", "4m": "site_gemm_kernel (K1, FP64 DMMA, 4M)",
-                   "ozaki": "ozaki2_gemm_kernel (K1, fp64 emulated on INT8 tcgen05, 7 digits)"}[args.gemm]
+                   "ozaki": f"ozaki2_gemm_kernel (K1, fp64 emulated on INT8 tcgen05, {args.oz_digits} digits)"}[args.gemm]
     bound_note = None
     if args.gemm == "3m":
         bound_note = ("achieved counts algorithmic flops (8 per complex MAC, SURVEY.md §8d); the 3M product executes "
@@ -491,7 +491,7 @@ def run_stage(args, local, W, K, config, dims):
     gemm_flops_avg = prof["gemm_flops"] / max(prof["gemm_launches"], 1)
     achieved = gemm_flops_avg / (gemm_ms_avg / 1e3) / 1e12 if gemm_ms_avg > 0 else 0.0
     kernel_name = {"3m": "site_gemm3m_kernel (K1, FP64 DMMA, 3M)", "4m": "site_gemm_kernel (K1, FP64 DMMA, 4M)",
-                   "ozaki": "ozaki2_gemm_kernel (K1, fp64 emulated on INT8 tcgen05, 7 digits)"}[args.gemm]
+                   "ozaki": f"ozaki2_gemm_kernel (K1, fp64 emulated on INT8 tcgen05, {args.oz_digits} digits)"}[args.gemm]
     if args.dtype == "c64":
         bf16, src = measured_bf16()
         achieved, peak = 3.0 * achieved, bf16 / 2.0
@@ -776,14 +776,36 @@ def main():
         k1_ms = pa["gemm_ms"] / max(pa["gemm_launches"], 1)
         k1_tf = (pa["gemm_flops"] / max(pa["gemm_launches"], 1)) / (k1_ms / 1e3) / 1e12 if k1_ms > 0 else 0.0
         i8_peak = 4510.5  # TOP/s: profiles/r01_umma_probe.jsonl, kind::i8 M=128 N=128 issue-rate probe
-        alt = {"gemm": "ozaki_gemm (complex128 K1 emulated on INT8 tcgen05: 7 digits of 7 bits, "
-                       "~1e-13 of the row scales; mps_set_gemm_mode 8)",
+        S = args.oz_digits
+        npr = S * (S + 1) // 2
+        alt = {"gemm": f"ozaki_gemm (complex128 K1 emulated on INT8 tcgen05: {S} digits of 7 bits, "
+                       f"{'~1e-13' if S == 7 else '~1e-11' if S == 6 else '~1e-9'} of the row scales; mps_set_gemm_mode 8)",
                "value": world * K * n / (ms_alt / 1e3), "unit": "samples/s", "ms_per_step": ms_alt / K,
                "lanes": LANES["ozaki"],
                "valid_outputs": ok_alt,
                "k1": {"ms_per_launch": k1_ms, "algorithmic_tflops": k1_tf, "vs_fp64_dmma_peak": k1_tf / fp64_peak()[0],
-                      "executed_int8_tops": 28.0 * k1_tf, "int8_frac": 28.0 * k1_tf / i8_peak,
+                      "executed_int8_tops": npr * k1_tf, "int8_frac": npr * k1_tf / i8_peak,
                       "int8_peak_source": "profiles/r01_umma_probe.jsonl (kind::i8 N=128, 4510 TOP/s)"}}
+        if S == 7:
+            # the 6-digit variant (21 INT8 products instead of 28; marginals ~7e-12 from the oracle at
+            # chi = 1000 and 4000, tests/test_gpu_parity.py), same inputs, timed the same way
+            eng.set_gemm_mode(8)
+            eng.set_ozaki_digits(6)
+            eng.set_lanes(LANES["ozaki"])
+            for s in range(W):
+                step(s)
+            barrier()
+            a0.record(stream)
+            for s in range(W, W + K):
+                step(s)
+            a1.record(stream)
+            barrier()
+            ms6 = dist_max(a0.elapsed_time(a1), dev)
+            alt["value_6_digits"] = world * K * n / (ms6 / 1e3)
+            alt["valid_outputs_6_digits"] = not bool((status[W:] & 1).any().item())
+            eng.set_ozaki_digits(7)
+            eng.set_lanes(args.lanes)
+            eng.set_gemm_mode({"3m": 3, "4m": 4}[args.gemm])
     peak, peak_src = fp64_peak()
     traffic, traffic_note = ncu_traffic(args.config, n)
     if args.dtype == "c64":
@@ -792,7 +814,7 @@ def main():
     gemm_flops_avg = prof["gemm_flops"] / max(prof["gemm_launches"], 1)
     achieved = gemm_flops_avg / (gemm_ms_avg / 1e3) / 1e12 if gemm_ms_avg > 0 else 0.0
     kernel_name = {"3m": "site_gemm3m_kernel (K1, FP64 DMMA, 3M)", "4m": "site_gemm_kernel (K1, FP64 DMMA, 4M)",
-                   "ozaki": "ozaki2_gemm_kernel (K1, fp64 emulated on INT8 tcgen05, 7 digits)"}[args.gemm]
+                   "ozaki": f"ozaki2_gemm_kernel (K1, fp64 emulated on INT8 tcgen05, {args.oz_digits} digits)"}[args.gemm]
     bound_note = None
     if args.gemm == "3m":
         bound_note = ("achieved counts algorithmic flops (8 per complex MAC, SURVEY.md §8d); the 3M product executes "
