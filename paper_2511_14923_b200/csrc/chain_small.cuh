@@ -224,6 +224,12 @@ __global__ void __launch_bounds__(SC_THREADS, 1) small_chain_kernel(const __grid
         ++vph;
       }
       if (tid == 0) {
+        // Why no cluster barrier per mode: a peer's C entries for step q+1 need that peer's K1(q+1), which
+        // needs every row's v'(q+1) (or, at a group start, follows the peer's draw(q), which needed this
+        // CTA's K1(q) entries) -- so they land only after this point; the expects below therefore
+        // precede every transaction they count.  C rows alternate between two buffers (step parity):
+        // step q+2 can only be written after this CTA's own draw(q) has sent v'(q+1) or, at a group
+        // start, after its K1(q+1) -- both after draw(q) stopped reading buffer q & 1.
         if (q + 1 < nsteps) {  // expect the next step's C row and (inside a group) its V tile
           const int m1 = P.m_begin + (q + 1) % nmodes;
           mbar_arrive_expect_tx(&c_full[(q + 1) & 1], (uint32_t)F_of(m1) * 128u);
