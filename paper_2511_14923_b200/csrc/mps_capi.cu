@@ -228,10 +228,12 @@ struct mps_ctx {
   DevBuf<float> ones_hi, ones_lo, in_hi, in_lo;
   DevBuf<double> ones_sum, in_sum;
   // workspaces
-  DevBuf<double2> ones, alpha_d, disp_d;
-  DevBuf<double> u_d, marg_d;
-  DevBuf<int32_t> counts_d;
-  DevBuf<uint8_t> status_d;
+  DevBuf<double2> ones;
+  // host arrays of a call, packed: [u | alpha | disp | counts | marginals | status] (256-B aligned
+  // fields) in a pinned host buffer and its device twin, moved by one H2D and one D2H copy
+  DevBuf<uint8_t> io_d;
+  uint8_t* io_h = nullptr;
+  size_t io_h_cap = 0;
   // live kernel timing (mps_profile): event pairs bracketing each launch on its stream
   int profile = 0;  // bit 0: time K1 launches, bit 1: time K2+K3 launches
   struct Rec {
@@ -1105,77 +1107,74 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
     for (int m = m_begin; m < m_end; ++m) CU(c, ozaki_prepare_site(c->sites[m], D, c->oz_S), "Ozaki site digits");
   }
 
-  // ---- inputs: stage host arrays on the device ----
-  const double* u_dev = uniforms;
-  int64_t ldu = ld_u;
-  if (uniforms && !is_device_ptr(uniforms)) {
-    CU(c, c->u_d.ensure((size_t)n * ld_u), "alloc uniforms");
-    CU(c, cudaMemcpyAsync(c->u_d.p, uniforms, (size_t)n * ld_u * sizeof(double), cudaMemcpyHostToDevice, st), "H2D u");
-    u_dev = c->u_d.p;
-  }
-  const double2* alpha_dev = (const double2*)alpha;
-  if (alpha && !is_device_ptr(alpha)) {
-    CU(c, c->alpha_d.ensure((size_t)n * M), "alloc alpha");
-    CU(c, cudaMemcpyAsync(c->alpha_d.p, alpha, (size_t)n * M * sizeof(double2), cudaMemcpyHostToDevice, st), "H2D alpha");
-    alpha_dev = c->alpha_d.p;
-  }
-  const double2* disp_dev = (const double2*)disp;
-  if (disp && !is_device_ptr(disp)) {
-    CU(c, c->disp_d.ensure((size_t)n * M * D * D), "alloc disp");
-    CU(c, cudaMemcpyAsync(c->disp_d.p, disp, (size_t)n * M * D * D * sizeof(double2), cudaMemcpyHostToDevice, st),
-       "H2D disp");
-    disp_dev = c->disp_d.p;
-  }
+  // ---- inputs: host arrays are packed into one pinned buffer and moved by ONE H2D copy (and the
+  //      host outputs come back by one D2H): at C1/C2 sizes a call pays per-copy API latency, not
+  //      bytes ----
+  const bool u_host = uniforms && !is_device_ptr(uniforms);
+  const bool alpha_host = alpha && !is_device_ptr(alpha);
+  const bool disp_host = disp && !is_device_ptr(disp);
   const bool counts_host = !is_device_ptr(counts);
   const bool marg_host = marginals && !is_device_ptr(marginals);
   const bool status_host = status && !is_device_ptr(status);
-  int32_t* counts_dev = counts;
-  if (counts_host) {
-    CU(c, c->counts_d.ensure((size_t)n * ld_c), "alloc counts");
-    counts_dev = c->counts_d.p;
+  const bool status_own = !status || status_host;  // the library's status row (zeroed or copied in)
+  size_t io_off = 0;
+  auto field = [&](bool on, size_t bytes) {
+    const size_t o = io_off;
+    if (on) io_off += (bytes + 255) & ~(size_t)255;
+    return o;
+  };
+  const size_t o_u = field(u_host, (size_t)n * ld_u * sizeof(double));
+  const size_t o_a = field(alpha_host, (size_t)n * M * sizeof(double2));
+  const size_t o_d = field(disp_host, (size_t)n * M * D * D * sizeof(double2));
+  const size_t o_io = io_off;  // outputs (and in-out fields) from here on
+  const size_t o_c = field(counts_host, (size_t)n * ld_c * sizeof(int32_t));
+  const size_t o_m = field(marg_host, (size_t)n * ld_c * D * sizeof(double));
+  const size_t o_s = field(status_own, (size_t)n);
+  const size_t io_total = io_off;
+  if (io_total > 0) {
+    CU(c, c->io_d.ensure(io_total), "alloc staging");
+    if (c->io_h_cap < io_total) {
+      if (c->io_h) cudaFreeHost(c->io_h);
+      c->io_h = nullptr;
+      c->io_h_cap = 0;
+      CU(c, cudaMallocHost(&c->io_h, io_total), "alloc pinned staging");
+      c->io_h_cap = io_total;
+    }
   }
-  double* marg_dev = marginals;
-  if (marg_host) {
-    CU(c, c->marg_d.ensure((size_t)n * ld_c * D), "alloc marginals");
-    marg_dev = c->marg_d.p;
-  }
-  uint8_t* status_dev = status;
-  if (!status || status_host) {
-    CU(c, c->status_d.ensure((size_t)n), "alloc status");
-    status_dev = c->status_d.p;
-    if (status_host)
-      CU(c, cudaMemcpyAsync(status_dev, status, n, cudaMemcpyHostToDevice, st), "H2D status");
-    else
-      CU(c, cudaMemsetAsync(status_dev, 0, n, st), "memset status");
-  }
-  if (counts_host && (m_end - m_begin < M || c->forced)) {
-    // partial range into host arrays: keep the untouched columns (forced: the outcomes are inputs)
-    CU(c, cudaMemcpyAsync(counts_dev, counts, (size_t)n * ld_c * sizeof(int32_t), cudaMemcpyHostToDevice, st),
-       "H2D counts");
-  }
-  if (marg_host && m_end - m_begin < M) {
-    CU(c, cudaMemcpyAsync(marg_dev, marginals, (size_t)n * ld_c * D * sizeof(double), cudaMemcpyHostToDevice, st),
-       "H2D marginals");
-  }
+  uint8_t* const hb = c->io_h;
+  uint8_t* const db = c->io_d.p;
+  const bool counts_in = counts_host && (m_end - m_begin < M || c->forced);  // untouched columns / forced outcomes
+  const bool marg_in = marg_host && m_end - m_begin < M;
+  if (u_host) memcpy(hb + o_u, uniforms, (size_t)n * ld_u * sizeof(double));
+  if (alpha_host) memcpy(hb + o_a, alpha, (size_t)n * M * sizeof(double2));
+  if (disp_host) memcpy(hb + o_d, disp, (size_t)n * M * D * D * sizeof(double2));
+  if (counts_in) memcpy(hb + o_c, counts, (size_t)n * ld_c * sizeof(int32_t));
+  if (marg_in) memcpy(hb + o_m, marginals, (size_t)n * ld_c * D * sizeof(double));
+  if (status_host) memcpy(hb + o_s, status, n);
+  // inputs, plus the in-out tail when any of it carries data in.  Every call that copies from the
+  // pinned buffer synchronises before returning (host inputs or host outputs), so the next call may
+  // refill it; a library-owned status row is zeroed on the device instead (no host staging).
+  const size_t h2d = (status_host || counts_in || marg_in) ? io_total : o_io;
+  if (h2d > 0) CU(c, cudaMemcpyAsync(db, hb, h2d, cudaMemcpyHostToDevice, st), "H2D inputs");
+  if (!status) CU(c, cudaMemsetAsync(db + o_s, 0, n, st), "zero status");
+  const double* u_dev = u_host ? reinterpret_cast<const double*>(db + o_u) : uniforms;
+  const int64_t ldu = ld_u;
+  const double2* alpha_dev = alpha_host ? reinterpret_cast<const double2*>(db + o_a) : (const double2*)alpha;
+  const double2* disp_dev = disp_host ? reinterpret_cast<const double2*>(db + o_d) : (const double2*)disp;
+  int32_t* counts_dev = counts_host ? reinterpret_cast<int32_t*>(db + o_c) : counts;
+  double* marg_dev = marg_host ? reinterpret_cast<double*>(db + o_m) : marginals;
+  uint8_t* status_dev = status_own ? db + o_s : status;
 
-  // ---- outputs back to the host ----
+  // ---- outputs back to the host: one D2H of the in-out tail, then host copies ----
+  const bool host_out = counts_host || marg_host || status_host;
+  const bool host_in = u_host || alpha_host || disp_host;
   auto finish = [&]() -> int {
-    bool sync = false;
-    if (counts_host) {
-      CU(c, cudaMemcpyAsync(counts, counts_dev, (size_t)n * ld_c * sizeof(int32_t), cudaMemcpyDeviceToHost, st), "D2H counts");
-      sync = true;
-    }
-    if (marg_host) {
-      CU(c, cudaMemcpyAsync(marginals, marg_dev, (size_t)n * ld_c * D * sizeof(double), cudaMemcpyDeviceToHost, st),
-         "D2H marginals");
-      sync = true;
-    }
-    if (status_host) {
-      CU(c, cudaMemcpyAsync(status, status_dev, n, cudaMemcpyDeviceToHost, st), "D2H status");
-      sync = true;
-    }
-    if (sync || uniforms != u_dev || alpha != (const void*)alpha_dev || disp != (const void*)disp_dev)
-      CU(c, cudaStreamSynchronize(st), "stream sync");
+    if (host_out) CU(c, cudaMemcpyAsync(hb + o_io, db + o_io, io_total - o_io, cudaMemcpyDeviceToHost, st), "D2H outputs");
+    // host inputs: the pinned staging is reused by the next call
+    if (host_out || host_in) CU(c, cudaStreamSynchronize(st), "stream sync");
+    if (counts_host) memcpy(counts, hb + o_c, (size_t)n * ld_c * sizeof(int32_t));
+    if (marg_host) memcpy(marginals, hb + o_m, (size_t)n * ld_c * D * sizeof(double));
+    if (status_host) memcpy(status, hb + o_s, n);
     return MPS_OK;
   };
 
@@ -1538,12 +1537,8 @@ void mps_destroy(mps_ctx* c) {
   }
   if (c->copy_st) cudaStreamDestroy(c->copy_st);
   c->ones.release();
-  c->alpha_d.release();
-  c->disp_d.release();
-  c->u_d.release();
-  c->marg_d.release();
-  c->counts_d.release();
-  c->status_d.release();
+  c->io_d.release();
+  if (c->io_h) cudaFreeHost(c->io_h);
   c->chain_meta.release();
   for (auto& r : c->recs) {
     cudaEventDestroy(r.a);
