@@ -254,48 +254,55 @@ __global__ void __launch_bounds__(SC_THREADS, 1) small_chain_kernel(const __grid
         for (int j = 0; j < SC_FW; ++j)
 #pragma unroll
           for (int e = 0; e < 2; ++e) t1[mf][j][e] = t2[mf][j][e] = t3[mf][j][e] = 0.0;
-      for (int kt0 = 0; kt0 < KT; kt0 += SC_KS, ++sidx) {
-        const int slot = sidx % SC_STAGES, nks = min(SC_KS, KT - kt0);
-#ifdef SC_TRACE
-        const long long w0 = clock64();
-#endif
-        mbar_wait(&full[slot], (sidx / SC_STAGES) & 1);
-#ifdef SC_TRACE
-        if (tid == 0 && blockIdx.x == 0 && q < 256) sc_trace[1][q][0] += clock64() - w0;
-#endif
-#pragma unroll
-        for (int ks = 0; ks < SC_KS; ++ks) {
-        if (ks >= nks) break;
-        const int kt = kt0 + ks;
-        const uint8_t* st = smem + slot * SC_STAGE_BYTES + ks * fc * 1024;
+      // one k stage (two DMMA k steps) of this warp's fragment, in site_gemm3m_kernel's per-accumulator
+      // k order.  The fragment test is hoisted out of the loop: a branch around mma.sync inside the
+      // loop costs a WARPSYNC per step and keeps the scheduler from overlapping one step's LDS with
+      // the previous step's DMMAs.
+      auto kstage = [&](const uint8_t* st, int kt) {
 #pragma unroll
         for (int step = 0; step < 2; ++step) {
           const int i = 2 * t + step;
+          const double2 w = *reinterpret_cast<const double2*>(st + fbase * 1024 + i * 128 + ((g ^ i) << 4));
           double2 v[SC_MF];
-          double as[SC_MF];
+#pragma unroll
+          for (int mf = 0; mf < SC_MF; ++mf)
+            v[mf] = *reinterpret_cast<const double2*>(Vt + (8 * mf + g) * SC_VP + (8 * kt + i) * 16);
+          const double ws = __dadd_rn(w.x, w.y);
 #pragma unroll
           for (int mf = 0; mf < SC_MF; ++mf) {
-            v[mf] = *reinterpret_cast<const double2*>(Vt + (8 * mf + g) * SC_VP + (8 * kt + i) * 16);
-            as[mf] = __dadd_rn(v[mf].x, v[mf].y);
-          }
-#pragma unroll
-          for (int nf = 0; nf < SC_FW; ++nf) {
-            const int fi = fbase + nf;
-            if (fi < fc) {
-              const double2 w = *reinterpret_cast<const double2*>(st + fi * 1024 + i * 128 + ((g ^ i) << 4));
-              const double ws = __dadd_rn(w.x, w.y);
-#pragma unroll
-              for (int mf = 0; mf < SC_MF; ++mf) {
-                dmma_8x8x4(t1[mf][nf][0], t1[mf][nf][1], v[mf].x, w.x);
-                dmma_8x8x4(t2[mf][nf][0], t2[mf][nf][1], v[mf].y, w.y);
-                dmma_8x8x4(t3[mf][nf][0], t3[mf][nf][1], as[mf], ws);
-              }
-            }
+            dmma_8x8x4(t1[mf][0][0], t1[mf][0][1], v[mf].x, w.x);
+            dmma_8x8x4(t2[mf][0][0], t2[mf][0][1], v[mf].y, w.y);
+            dmma_8x8x4(t3[mf][0][0], t3[mf][0][1], __dadd_rn(v[mf].x, v[mf].y), ws);
           }
         }
+      };
+      if (fbase < fc) {
+        for (int kt0 = 0; kt0 < KT; kt0 += SC_KS, ++sidx) {
+          const int slot = sidx % SC_STAGES;
+#ifdef SC_TRACE
+          const long long w0 = clock64();
+#endif
+          mbar_wait(&full[slot], (sidx / SC_STAGES) & 1);
+#ifdef SC_TRACE
+          if (tid == 0 && blockIdx.x == 0 && q < 256) sc_trace[1][q][0] += clock64() - w0;
+#endif
+          const uint8_t* st = smem + slot * SC_STAGE_BYTES;
+          if (kt0 + SC_KS <= KT) {
+#pragma unroll
+            for (int ks = 0; ks < SC_KS; ++ks) kstage(st + ks * fc * 1024, kt0 + ks);
+          } else {
+            for (int ks = 0; kt0 + ks < KT; ++ks) kstage(st + ks * fc * 1024, kt0 + ks);
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[slot]);
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[slot]);
+      } else {  // no fragment in this mode: keep the ring's slot accounting
+        for (int kt0 = 0; kt0 < KT; kt0 += SC_KS, ++sidx) {
+          const int slot = sidx % SC_STAGES;
+          mbar_wait(&full[slot], (sidx / SC_STAGES) & 1);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[slot]);
+        }
       }
       SC_STAMP(0, q, 1);
       // epilogue: row 8 mf + g of the group is owned by CTA 8 mf + g — st.async the entries there
