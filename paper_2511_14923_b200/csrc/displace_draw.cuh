@@ -314,12 +314,24 @@ __device__ inline RowDraw draw_row_warp(const double (*red)[DMAX], int nwarps, d
 // bulk copies (mbarrier per slot), for both passes; loads in flight cost no registers, so the
 // kernel stops being bound on global-load latency.  Each thread still owns j = tid + 128 c, so
 // the reduction order (and every result bit) is the same with and without the ring.
+// ring slots of the draw kernel's C-row stream (a CTA keeps RING_SLOTS - 1 chunk loads in flight
+// while it works on one); the c64 chunks are half the bytes, so it affords a deeper ring
+#ifndef DRAW_SLOTS_C128
+#define DRAW_SLOTS_C128 2
+#endif
+#ifndef DRAW_SLOTS_C64
+#define DRAW_SLOTS_C64 2
+#endif
+template <bool C64>
+__host__ __device__ constexpr int draw_ring_slots() { return C64 ? DRAW_SLOTS_C64 : DRAW_SLOTS_C128; }
+
 template <int DT, bool C64, bool RING>
 __global__ void __launch_bounds__(DRAW_THREADS, C64 ? 8 : 4)
     displace_draw_kernel(DrawArgs A) {
   using ElemT = typename std::conditional<C64, float2, double2>::type;
   extern __shared__ __align__(16) uint8_t ring_smem[];
-  __shared__ uint64_t ring_bar[2];
+  constexpr int NS = draw_ring_slots<C64>();
+  __shared__ uint64_t ring_bar[NS];
   __shared__ double2 T[DMAX * DMAX];
   __shared__ float2 Tf[C64 ? DMAX * DMAX : 1];
   __shared__ double red[DRAW_THREADS / 32][DMAX];
@@ -338,27 +350,26 @@ __global__ void __launch_bounds__(DRAW_THREADS, C64 ? 8 : 4)
   const int nchunks = (A.chi_r + DRAW_THREADS - 1) / DRAW_THREADS;
   const int chunk_elems = DRAW_THREADS * D;
 
-  // ring: chunk u (of the 2 * nchunks loads, pass 1 then pass 2) goes to slot u & 1
+  // ring: chunk u (of the 2 * nchunks loads, pass 1 then pass 2) goes to slot u % NS
   auto ring_issue = [&](int u) {
     const int c = u % nchunks;
     const int j0 = c * DRAW_THREADS;
     const int nj = min(DRAW_THREADS, A.chi_r - j0);
     const uint32_t bytes = (uint32_t)(nj * D * (int)sizeof(ElemT));
-    uint64_t* bar = &ring_bar[u & 1];
+    uint64_t* bar = &ring_bar[u % NS];
     mbar_arrive_expect_tx(bar, bytes);
-    bulk_load_1d(ring_smem + (size_t)(u & 1) * chunk_elems * sizeof(ElemT), Crow + (long long)j0 * D, bytes, bar);
+    bulk_load_1d(ring_smem + (size_t)(u % NS) * chunk_elems * sizeof(ElemT), Crow + (long long)j0 * D, bytes, bar);
   };
   auto ring_slot = [&](int u) -> const ElemT* {
-    mbar_wait(&ring_bar[u & 1], (u >> 1) & 1);
-    return reinterpret_cast<const ElemT*>(ring_smem) + (size_t)(u & 1) * chunk_elems;
+    mbar_wait(&ring_bar[u % NS], (u / NS) & 1);
+    return reinterpret_cast<const ElemT*>(ring_smem) + (size_t)(u % NS) * chunk_elems;
   };
 
   // ---- displacement matrix for (b, m): inputs only, so it runs before the PDL wait and
   //      overlaps the tail of the site GEMM that produces C ----
   griddep_launch_dependents();
   if (RING && tid == 0) {
-    mbar_init(&ring_bar[0], 1);
-    mbar_init(&ring_bar[1], 1);
+    for (int i = 0; i < NS; ++i) mbar_init(&ring_bar[i], 1);
     fence_barrier_init();
   }
   const bool ident = !(A.disp || A.alpha || A.alpha_sigma >= 0.0);
@@ -383,7 +394,8 @@ __global__ void __launch_bounds__(DRAW_THREADS, C64 ? 8 : 4)
   // with one chunk the row stays in slot 0 for pass 2 (no re-load); else loads 0 and 1 go out now
   if (RING && tid == 0 && !dead) {
     ring_issue(0);
-    if (nchunks > 1) ring_issue(1);
+    if (nchunks > 1)
+      for (int u = 1; u < NS && u < 2 * nchunks; ++u) ring_issue(u);
   }
   __syncthreads();
 
@@ -450,7 +462,7 @@ __global__ void __launch_bounds__(DRAW_THREADS, C64 ? 8 : 4)
     }
     if (RING && nchunks > 1) {
       __syncthreads();  // every thread is done with this slot
-      if (tid == 0 && cidx + 2 < 2 * nchunks) ring_issue(cidx + 2);  // pass 1's next chunk, or pass 2's first
+      if (tid == 0 && cidx + NS < 2 * nchunks) ring_issue(cidx + NS);  // pass 1's next chunk, or pass 2's first
     }
   }
 #pragma unroll
@@ -525,7 +537,7 @@ __global__ void __launch_bounds__(DRAW_THREADS, C64 ? 8 : 4)
     }
     if (RING && nchunks > 1) {
       __syncthreads();
-      if (tid == 0 && nchunks + cidx + 2 < 2 * nchunks) ring_issue(nchunks + cidx + 2);
+      if (tid == 0 && nchunks + cidx + NS < 2 * nchunks) ring_issue(nchunks + cidx + NS);
     }
   }
 }

@@ -1423,9 +1423,10 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
         // the C row streams through a shared-memory TMA ring when its bytes are 16-B granular
         const size_t esz = c64 ? 8 : 16;
         const bool ring = c->draw_ring && ((size_t)N * esz) % 16 == 0;
-        const size_t ring_bytes = ring ? 2 * (size_t)DRAW_THREADS * D * esz : 0;
+        const size_t ring_bytes =
+            ring ? (size_t)(c64 ? draw_ring_slots<true>() : draw_ring_slots<false>()) * DRAW_THREADS * D * esz : 0;
         void (*dk)(DrawArgs) = draw_kernel_for(D, c64, ring);
-        if (ring) CU(c, set_smem_once((const void*)dk, 2 * DRAW_THREADS * DMAX * 16), "draw ring smem");
+        if (ring) CU(c, set_smem_once((const void*)dk, 4 * DRAW_THREADS * DMAX * 16), "draw ring smem");
         CU(c, launch_pdl(dk, dim3(nl), dim3(DRAW_THREADS), ring_bytes, lst[l], a), "displace_draw launch");
       }
       c->launches++;
