@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--chi", type=int, default=100)
     ap.add_argument("--D", type=int, default=10)
     ap.add_argument("--n", type=int, default=100)
+    ap.add_argument("--sigma", type=float, default=0.5, help="alpha sigma (negative: no displacement)")
     ap.add_argument("-D", dest="defs", action="append", default=[], help="extra -D for the trace build")
     a = ap.parse_args()
     lib = Path("/tmp/libmps_trace.so")
@@ -39,7 +40,7 @@ def main():
 
     mps = MPS.random(a.M, a.chi, a.D, seed=0)
     with MpsSampler(mps) as eng:
-        cfg = MpsSamplerConfig(N=a.n, seed=0, alpha_sigma=0.5, batch_size=a.n)
+        cfg = MpsSamplerConfig(N=a.n, seed=0, alpha_sigma=a.sigma if a.sigma >= 0 else None, batch_size=a.n)
         for _ in range(3):
             eng.sample(cfg)
         torch.cuda.synchronize()
