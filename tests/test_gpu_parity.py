@@ -752,3 +752,29 @@ def test_forced_evaluation_vs_oracle(c2_sites, mode):
     assert np.allclose(lp, ev2["logp"][:10])
     p1 = chain_joint_probability(MPS(c2_sites), rand[3], cfg, index=3)
     assert np.isclose(np.log(p1), ev2["logp"][3], rtol=1e-12) if p1 > 0 else ev2["logp"][3] == -np.inf
+
+
+@pytest.mark.parametrize("chain", [0, 1])
+def test_stage_split_into_host_arrays(c2_sites, chain):
+    """Partial mode ranges writing into HOST counts / marginals / status: the untouched columns of
+    the caller's arrays survive the packed host staging (one H2D + one D2H per call), and the two
+    stages together equal the single-context chain."""
+    N, M, cut = 130, 16, 9
+    mps = MPS(c2_sites)
+    cfg = MpsSamplerConfig(N=N, seed=12, alpha_sigma=0.5, batch_size=N)
+    with MpsSampler(mps) as eng:
+        full = eng.sample(cfg, return_marginals=True)
+    counts = np.full((N, M), -7, dtype=np.int32)
+    marg = np.full((N, M, 10), -1.0)
+    status = np.zeros(N, dtype=np.uint8)
+    state = torch.empty((N, mps.bond_dims[cut]), dtype=torch.complex128, device="cuda")
+    with MpsSampler(mps, sites_range=(0, cut), layout=1) as s0, MpsSampler(mps, sites_range=(cut, M), layout=1) as s1:
+        for e in (s0, s1):
+            e.set_streams(12, 0.5)
+            e.set_small_chain(chain)
+        s0.run(0, N, counts, state_out=state, marginals=marg, status=status)
+        assert (counts[:, cut:] == -7).all() and (marg[:, cut:] == -1.0).all()
+        s1.run(0, N, counts, state_in=state, marginals=marg, status=status)
+    assert np.array_equal(counts, full["counts"])
+    assert np.array_equal(marg, full["marginals"])
+    assert np.array_equal(status, full["status"])
