@@ -410,13 +410,13 @@ __global__ void __launch_bounds__(SC_THREADS, 1) small_chain_kernel(const __grid
           const RowDraw r = draw_row_warp(red, DRAW_THREADS / 32, p_s, D, st_s, A.forced != 0,
                                           __shfl_sync(0xffffffffu, k_pref, 0), __shfl_sync(0xffffffffu, u_pref, 0),
                                           A.tie_eps);
-          if (A.marg && lane < D) A.marg[crow * D + lane] = r.marg;
+          if (A.marg && lane < D) A.marg[crow * D + lane] = (r.k >= 0) ? p_s[lane] / r.Ptot : 0.0;
           if (lane == 0) {
             st_s = r.status;
             A.status[b] = r.status;
             if (!A.forced) A.counts[crow] = r.k;
             k_s = r.k;
-            scale_s = r.scale;
+            scale_s = (r.k >= 0 && p_s[r.k] > 0.0) ? 1.0 / sqrt(p_s[r.k]) : 0.0;
           }
         }
         sc_bar_compute();

@@ -261,8 +261,6 @@ struct RowDraw {
   int k;
   uint8_t status;
   double Ptot;
-  double marg;   // lane k < D: the normalised marginal p_k / Ptot (0 for a failed draw)
-  double scale;  // 1 / sqrt(p_k) of the drawn k (0 when none): the renormalisation of pass 2
 };
 __device__ inline RowDraw draw_row_warp(const double (*red)[DMAX], int nwarps, double* p_s, int D, uint8_t st0,
                                         bool forced, int k_forced, double u, double tie_eps) {
@@ -279,13 +277,8 @@ __device__ inline RowDraw draw_row_warp(const double (*red)[DMAX], int nwarps, d
     Ptot += pv;
     if (k <= lane) run += pv;
   }
-  // the three long-latency operations of every lane up front (independent, so they overlap)
-  const double pk = lane < D ? p_s[lane] : 0.0;
-  const double cdf = (lane == D - 1) ? 1.0 : run / Ptot;
-  const double mk = pk / Ptot;
-  const double sk = pk > 0.0 ? 1.0 / sqrt(pk) : 0.0;
-  RowDraw r{-1, st0, Ptot, 0.0, 0.0};
-  const unsigned pos = __ballot_sync(0xffffffffu, lane < D && pk > 0.0);
+  RowDraw r{-1, st0, Ptot};
+  const unsigned pos = __ballot_sync(0xffffffffu, lane < D && p_s[lane] > 0.0);
   if (!(Ptot > 0.0) || !isfinite(Ptot)) {
     r.status |= ST_FAILED;
   } else if (forced) {
@@ -295,6 +288,7 @@ __device__ inline RowDraw draw_row_warp(const double (*red)[DMAX], int nwarps, d
       r.k = -1;
     }
   } else {
+    const double cdf = (lane == D - 1) ? 1.0 : run / Ptot;
     const int cnt = __popc(__ballot_sync(0xffffffffu, lane < D && cdf <= u));
     double mind = (lane < D - 1) ? fabs(cdf - u) : 1e300;
 #pragma unroll
@@ -304,9 +298,6 @@ __device__ inline RowDraw draw_row_warp(const double (*red)[DMAX], int nwarps, d
     r.k = below ? 31 - __clz(below) : 0;
     if (mind <= tie_eps) r.status |= ST_FLAGGED;
   }
-  r.marg = r.k >= 0 ? mk : 0.0;
-  const double sel = __shfl_sync(0xffffffffu, sk, r.k >= 0 ? r.k : 0);
-  r.scale = r.k >= 0 ? sel : 0.0;
   return r;
 }
 
@@ -481,12 +472,12 @@ __global__ void __launch_bounds__(DRAW_THREADS, C64 ? 8 : 4)
                              : philox_double(numpy_key0(A.seed), gi / 64, (gi % 64) * (uint64_t)A.M + A.m);
     const RowDraw r = draw_row_warp(red, DRAW_THREADS / 32, p_s, D, A.status[b], A.forced != 0,
                                     A.forced ? A.counts[crow] : 0, u, A.tie_eps);
-    if (A.marg && lane < D) A.marg[crow * D + lane] = r.marg;
+    if (A.marg && lane < D) A.marg[crow * D + lane] = (r.k >= 0) ? p_s[lane] / r.Ptot : 0.0;
     if (lane == 0) {
       A.status[b] = r.status;
       if (!A.forced) A.counts[crow] = r.k;
       k_s = r.k;
-      scale_s = r.scale;
+      scale_s = (r.k >= 0 && p_s[r.k] > 0.0) ? 1.0 / sqrt(p_s[r.k]) : 0.0;
     }
   }
   __syncthreads();
