@@ -115,18 +115,86 @@ def site_flops(dims, D, n):
     return [8.0 * n * dims[m] * dims[m + 1] * D + 8.0 * n * dims[m + 1] * D * D for m in range(len(dims) - 1)]
 
 
+def parity_spot_check(eng, mps, m_begin, m_end, first, n_chk, stream, sigma, uniforms=None, alpha=None,
+                      state_in=None, ref_counts=None, gemm_mode=None, tol=1e-10):
+    """Parity of the bench's own run against the oracle (the checker, never the thing timed):
+    n_chk samples starting at global index `first` through sites [m_begin, m_end) of the bench's
+    device-resident sites, with marginals; the oracle follows the GPU's realised path
+    (teacher-forced) and also runs free on the same uniforms / alpha / input state.  Returns the
+    JSON "parity" object (north_star bar: marginals within 1e-10 relative, counts identical except
+    flagged near-ties).  ref_counts: the timed run's counts of those rows, which must equal these."""
+    import torch
+
+    from oracle import mps_oracle as orc
+    from paper_2511_14923_b200 import alpha_stream as a_stream, stream_uniforms as u_stream
+
+    dev = torch.device("cuda", eng.device)
+    M, D = eng.M, eng.D
+    t0 = time.perf_counter()
+    cnt = torch.zeros((n_chk, M), dtype=torch.int32, device=dev)
+    st = torch.zeros(n_chk, dtype=torch.uint8, device=dev)
+    marg = torch.zeros((n_chk, M, D), dtype=torch.float64, device=dev)
+    u_all = u_stream(0, first, n_chk, M) if uniforms is None else uniforms.cpu().numpy()
+    a_all = a_stream(0, first, n_chk, M, sigma) if alpha is None else alpha.cpu().numpy()
+    eng.run(first, n_chk, cnt, m_begin=m_begin, m_end=m_end,
+            uniforms=None if uniforms is None else uniforms, alpha=None if alpha is None else alpha,
+            state_in=state_in, marginals=marg, status=st, stream=stream)
+    torch.cuda.synchronize(dev)
+    cnt_h, st_h, marg_h = cnt.cpu().numpy(), st.cpu().numpy(), marg.cpu().numpy()
+    sites = [np.asarray(mps.sites[m].resolve_conj().cpu().numpy() if isinstance(mps.sites[m], torch.Tensor)
+                        else mps.sites[m], dtype=np.complex128) for m in range(m_begin, m_end)]
+    cols = slice(m_begin, m_end)
+    v0 = None if state_in is None else state_in.cpu().numpy().astype(np.complex128)
+    forced = orc.sample_chain(sites, u_all[:, cols], alpha=a_all[:, cols], forced=cnt_h[:, cols],
+                              return_marginals=True, state_in=v0)
+    free = orc.sample_chain(sites, u_all[:, cols], alpha=a_all[:, cols], state_in=v0)
+    pg, pc = marg_h[:, cols], forced["marginals"]
+    d = np.abs(pg - pc)
+    big = pc > 1e-12
+    rel = float((d[big] / pc[big]).max()) if big.any() else 0.0
+    flagged = (st_h & 2) != 0
+    mism = (cnt_h[:, cols] != free["counts"]).any(axis=1) & ~flagged & ~free["flagged"]
+    ortho = 0.0
+    for m in sorted({m_begin, m_begin + 1, (m_begin + m_end) // 2, m_end - 1} & set(range(m_begin, m_end))):
+        G = mps.sites[m] if isinstance(mps.sites[m], torch.Tensor) else torch.from_numpy(np.asarray(mps.sites[m])).to(dev)
+        A = G.reshape(G.shape[0], -1)
+        eye = torch.eye(A.shape[0], dtype=A.dtype, device=A.device)
+        ortho = max(ortho, float((A @ A.conj().T - eye).abs().max().item()))
+    same = None if ref_counts is None else bool(np.array_equal(ref_counts[:, cols], cnt_h[:, cols]))
+    site_tol = 1e-12 if tol <= 1e-9 else 1e-5  # complex64 sites are orthonormal to fp32 rounding
+    ok = bool(d.max() <= tol and rel <= tol and not mism.any() and not (st_h & 1).any() and ortho < site_tol
+              and same is not False)
+    return {"ok": ok, "n_checked": int(n_chk), "modes": [int(m_begin), int(m_end)], "max_abs_dp": float(d.max()),
+            "max_rel_dp": rel, "tolerance": tol, "rel_floor": 1e-12, "n_marginals_above_floor": int(big.sum()),
+            "counts_mismatch_unflagged": int(mism.sum()), "n_flagged": int(flagged.sum()),
+            "same_as_timed_run": same, "site_orthonormality_max": ortho,
+            "gemm_mode": gemm_mode, "oracle": "oracle.sample_chain teacher-forced along the GPU path + free run",
+            "seconds": time.perf_counter() - t0}
+
+
 # ---------------------------------------------------------------------------------------------
 # CPU leg (oracle; only here and in tests)
 # ---------------------------------------------------------------------------------------------
 
 
-class CpuBaseline:
-    """The NumPy oracle (batched BLAS ZGEMM chain, all host cores) on a bounded sample.
+def host_site_fast(rng, chi_l, chi_r, D):
+    """Row-orthonormal complex128 site for the CPU leg at large chi: Cholesky-QR of a complex
+    Gaussian (Gamma.reshape(chi_l, chi_r D) = L^-1 Z^H with L L^H = Z^H Z), orthonormal to ~1e-14.
+    The oracle's exact QR recipe (oracle.random_site) takes ~9 s per chi = 1000 site on the host;
+    the CPU leg's time does not depend on the site values, only on their shapes."""
+    import scipy.linalg as sl
 
-    c1/c2: the whole chain, n samples through all M sites.  Larger configs: n_cpu samples
-    through a block of full-chi sites (a column slice of one site when a site exceeds
-    ~1 GB of host memory), the oracle's per-mode step as in sample_chain; the per-sample
-    time is extrapolated to all M sites by algorithmic flops.  Sites are generated once."""
+    Z = rng.standard_normal((chi_r * D, chi_l)) + 1j * rng.standard_normal((chi_r * D, chi_l))
+    Lc = np.linalg.cholesky(Z.conj().T @ Z)
+    return np.ascontiguousarray(sl.solve_triangular(Lc, Z.conj().T, lower=True).reshape(chi_l, chi_r, D))
+
+
+class CpuBaseline:
+    """The NumPy oracle (oracle.sample_chain: batched BLAS ZGEMM chain on all host cores) timed on
+    REAL steps: each step is a micro-batch of samples through ALL M sites (no extrapolation) for the
+    sample-sharded configs c1-c3.  c1/c2 use the oracle's own sites; c3's 64 sites (10 GB) are
+    generated row-orthonormal by Cholesky-QR (host_site_fast).  The pipelined configs c4/c5 do not
+    fit host memory: there a block of full-chi sites is timed and extrapolated by flops."""
 
     def __init__(self, cfg_name):
         from oracle import mps_oracle as orc
@@ -141,12 +209,16 @@ class CpuBaseline:
             self.cores = max([i.get("num_threads", 1) for i in threadpool_info()] or [os.cpu_count() or 1])
         except Exception:
             self.cores = os.cpu_count() or 1
-        self.full = M * chi * chi * D * 16 <= 2e9
+        t0 = time.perf_counter()
+        self.full = M * chi * chi * D * 16 <= 16e9
         if self.full:
-            self.sites = orc.random_mps(M, chi, D, seed=0)
-            self.n_cpu = n
-            self.u = orc.stream_uniforms(0, 0, n, M)
-            self.al = orc.alpha_stream(0, 0, n, M, sigma)
+            if chi <= 128:
+                self.sites, self.site_note = orc.random_mps(M, chi, D, seed=0), "the oracle's sites (seed 0)"
+            else:
+                rng = np.random.default_rng(0)
+                self.sites = [host_site_fast(rng, self.dims[m], self.dims[m + 1], D) for m in range(M)]
+                self.site_note = "row-orthonormal sites by Cholesky-QR (seed 0)"
+            self.setup_s = time.perf_counter() - t0
             return
         mid = M // 2
         site_bytes = 16.0 * chi * chi * D
@@ -154,30 +226,54 @@ class CpuBaseline:
         self.block = list(range(mid, mid + self.S))
         self.slice_cols = chi if site_bytes <= 1e9 else max(1, int(1e9 / (16.0 * chi * D)))
         rng = np.random.default_rng(0)
-        if self.slice_cols == chi and site_bytes <= 2e8:
-            self.sites = [orc.random_site(0, m, self.dims[m], self.dims[m + 1], D) for m in self.block]
-        else:  # timing stand-in of the same shape (QR of a multi-GB site on the host is not the workload)
-            self.sites = [(rng.standard_normal((chi, self.slice_cols, D)) + 1j * rng.standard_normal(
-                (chi, self.slice_cols, D))) / np.sqrt(2.0 * chi * D) for _ in self.block]
+        self.sites = [(rng.standard_normal((chi, self.slice_cols, D)) + 1j * rng.standard_normal(
+            (chi, self.slice_cols, D))) / np.sqrt(2.0 * chi * D) for _ in self.block]
         self.n_cpu = 256
         self.u = orc.stream_uniforms(0, 0, self.n_cpu, self.S)
         self.al = orc.alpha_stream(0, 0, self.n_cpu, self.S, sigma)
         v0 = rng.standard_normal((self.n_cpu, chi)) + 1j * rng.standard_normal((self.n_cpu, chi))
         self.v0 = v0 / np.linalg.norm(v0, axis=1, keepdims=True)
+        self.setup_s = time.perf_counter() - t0
+
+    def step(self, first, n):
+        """One real step: samples first..first+n-1 through all M sites; returns seconds."""
+        orc = self.orc
+        u = orc.stream_uniforms(0, first, n, self.M)
+        al = orc.alpha_stream(0, first, n, self.M, self.sigma)
+        t0 = time.perf_counter()
+        orc.sample_chain(self.sites, u, alpha=al)
+        return time.perf_counter() - t0
+
+    def size_step(self, budget_s):
+        """Samples per step so one full-chain step takes about budget_s (a multiple of 16, at most
+        the config's n), from a timed 16-sample step."""
+        if not self.full:
+            return self.n_cpu
+        t16 = self.step(0, 16)
+        return int(max(16, min(self.n, (budget_s / max(t16, 1e-9)) * 16 // 16 * 16)))
+
+    def describe(self, n_step, reps):
+        if n_step >= self.n:
+            what = f"{reps} full steps of n = {n_step} samples through all {self.M} sites"
+        else:
+            what = (f"{reps} steps of {n_step} samples (of the config's n = {self.n}) through all {self.M} sites "
+                    f"(real steps, no extrapolation)")
+        return what + f"; {self.site_note}; oracle.sample_chain (numpy BLAS, {self.cores} threads)"
 
     def run(self, target_s=15.0):
-        """Returns (samples/s, cores, sample description)."""
+        """Returns (samples/s, cores, sample description) over about target_s of CPU time."""
         orc, D = self.orc, self.D
-        reps, t = 0, 0.0
         if self.full:
-            while t < target_s and reps < 100:
-                t0 = time.perf_counter()
-                orc.sample_chain(self.sites, self.u, alpha=self.al)
-                t += time.perf_counter() - t0
+            n_step = self.size_step(target_s / 2)
+            reps, t, done = 0, 0.0, 0
+            while reps < 2 or (t < target_s and reps < 100):
+                t += self.step(done, n_step)
+                done += n_step
                 reps += 1
-            return reps * self.n_cpu / t, self.cores, f"full chain, {reps} x {self.n_cpu} samples through all {self.M} sites"
+            return done / t, self.cores, self.describe(n_step, reps)
         n_cpu = self.n_cpu
         rows = np.arange(n_cpu)
+        reps, t = 0, 0.0
         while t < target_s and reps < 50:
             t0 = time.perf_counter()
             v = self.v0
@@ -275,23 +371,24 @@ def run_pipelined(args, rank, world, local, W, K, config, dims):
     counts = torch.empty((nsteps, n, M), dtype=torch.int32, device=dev)
     status = torch.zeros((nsteps, n), dtype=torch.uint8, device=dev)
     cdt = torch.complex64 if args.dtype == "c64" else torch.complex128
-    y = torch.empty((n, dims[me]), dtype=cdt, device=dev) if rank < world - 1 else None
     c_host = torch.empty((n, me - mb), dtype=torch.int32).pin_memory()
 
     def stage_for(offset, copy_out=False):
-        def stage(t, x):
+        def stage(t, x, out):
+            # the stage's last draw kernel writes the hand-off state straight into the send buffer
             s_ = offset + t
-            eng.run(s_ * n, n, counts[s_], m_begin=mb, m_end=me, state_in=x, state_out=y, status=status[s_],
+            eng.run(s_ * n, n, counts[s_], m_begin=mb, m_end=me, state_in=x, state_out=out, status=status[s_],
                     stream=stream.cuda_stream)
             if copy_out:
                 c_host.copy_(counts[s_, :, mb:me], non_blocking=True)
-            return y
         return stage
 
     hp = None
     if args.handoff == "p2p" and world > 1:  # fused hand-off: the draw kernel writes into the next GPU
         host_group = dist.new_group(backend="gloo") if BACKEND == "nccl" else None
-        hp = P2PHandoff(rank, world, n * dims[mb] * (8 if args.dtype == "c64" else 16), host_group=host_group)
+        hp = P2PHandoff.create(rank, world, n * dims[mb] * (8 if args.dtype == "c64" else 16), host_group=host_group)
+        if hp is None and rank == 0:
+            print("[bench] peer-memory hand-off unavailable: NCCL send/recv instead", file=sys.stderr, flush=True)
 
     def pipe(offset, count, copy_out=False):
         if hp is not None:
@@ -506,6 +603,15 @@ def run_stage(args, local, W, K, config, dims):
     value = K * n / (ms / 1e3)
     T = (N_total + n - 1) // n
     ok = not bool((status[W:] & 1).any().item())
+    # parity of this stage's kernels at full chi: its first two sites, 16 samples of step W fed the same
+    # input state, against the oracle (sites copied to the host: ~2 x 2.6 GB at C4, 2 x 16 GB at C5)
+    eng.set_lanes(args.lanes)
+    n_chk = min(16, n)
+    parity = parity_spot_check(eng, mps, mb, min(mb + 2, me), W * n, n_chk, stream.cuda_stream, sigma,
+                               state_in=x[W][:n_chk].contiguous() if mb > 0 else None,
+                               ref_counts=counts[W][:n_chk].cpu().numpy(), gemm_mode=args.gemm,
+                               tol=1e-4 if args.dtype == "c64" else 1e-10)
+    ok = ok and parity["ok"]
     cfg = dict(config, layout=f"one stage of a {G}-stage mode pipeline, measured alone on one B200",
                l2="inputs larger than L2 (stage sites %.1f GB streamed per step)" % (block_bytes / 1e9),
                stage=g, stage_blocks=blocks, stage_sites=[mb, me], stage_site_bytes=block_bytes,
@@ -527,7 +633,7 @@ def run_stage(args, local, W, K, config, dims):
                      "frac": achieved / peak if peak else None, "traffic": None, "kernel": kernel_name,
                      "peak_source": peak_src, "per_launch": {"ms": gemm_ms_avg, "algorithmic_flops": gemm_flops_avg},
                      "stage_chain_tflops": K * stage_flops / (ms / 1e3) / 1e12},
-        "clocks": ck, "valid_outputs": ok, "setup_s": setup_s,
+        "clocks": ck, "valid_outputs": ok, "parity": parity, "setup_s": setup_s,
     }
     eng.close()
     return line
@@ -564,12 +670,28 @@ def main():
                     help="micro-batch size (default: the config's batch n); with --lanes L it runs as L "
                          "concurrent chains of n / L rows; per-sample results do not depend on either")
     args = ap.parse_args()
+    if args.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: a bare `bench.py --gpus N` re-executes itself under torchrun (the
+        # driver's own launch for N > 1), so --gpus can never silently measure one GPU
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+        print("[bench] re-executing under torchrun: " + " ".join(cmd), file=sys.stderr, flush=True)
+        os.execv(sys.executable, cmd)
     args.lanes = args.lanes or LANES[args.gemm]
     W = max(args.warmup, 3)
     K = args.steps if args.steps is not None else {"c1": 20000, "c2": 10000}.get(args.config, 10)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = 0 if ONE_GPU else int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one process per GPU")
     M, chi, D, n, sigma, N_total, desc = CONFIGS[args.config]
     if args.n and args.stage_of == 0:  # micro-batch override for the sample-sharded / pipelined runs
         n = args.n
@@ -585,23 +707,35 @@ def main():
                   sum(a * b for a, b in zip(dims[:-1], dims[1:])) * D * 16 / 1e9)}
 
     if args.impl == "reference":
-        # The reference ships no MPS sampler; its arm is the CPU oracle
-        # restating PAPER.md:58-66 on the host cores, rank 0 only.
+        # The reference ships no MPS sampler; its arm is the CPU oracle restating
+        # PAPER.md:58-66, timed on the host cores (all BLAS threads), rank 0 only.  Every step is a
+        # REAL micro-batch through all M sites, sized so the W + K steps take a few minutes; the
+        # line's ms_per_step is the measured median step time.
         if rank != 0:
             return
-        steps = []
         cpu = CpuBaseline(args.config)
-        if args.steps is None:  # the c1/c2 GPU defaults (10^4 steps) would take hours on the host
-            K = min(K, 10)
+        budget = float(os.environ.get("MPS_REF_BUDGET_S", "240"))
+        n_step = cpu.size_step(budget / (W + K)) if cpu.full else cpu.n_cpu
+        times, rates = [], []
+        first = 0
         for i in range(W + K):
-            v, cores, sample = cpu.run(target_s=max(1.0, 60.0 / (W + K)))
+            if cpu.full:
+                dt = cpu.step(first, n_step)
+                first += n_step
+                v = n_step / dt
+            else:
+                v, _, _ = cpu.run(target_s=max(1.0, budget / (W + K)))
+                dt = n_step / v
             if i >= W:
-                steps.append(v)
-        v = float(np.median(steps))
+                times.append(dt)
+                rates.append(v)
+        v = float(np.median(rates))
+        sample = cpu.describe(n_step, K) if cpu.full else cpu.run(target_s=0.0)[2]
         line = {"metric": METRIC, "value": v, "unit": "samples/s", "impl": "reference", "n_gpus": world, "steps": K,
-                "warmup": W, "ms_per_step": 1000.0 * n / v, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "c128", "data": "synthetic", "config": config,
-                "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cores, "kind": "port", "sample": sample},
+                "warmup": W, "ms_per_step": 1000.0 * float(np.median(times)), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic", "config": config,
+                "step_samples": n_step, "setup_s": cpu.setup_s,
+                "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cpu.cores, "kind": "port", "sample": sample},
                 "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
@@ -615,6 +749,8 @@ def main():
     layout = args.layout
     if layout == "auto":
         layout = "sharded" if site_bytes * 1.5 < HBM_USABLE else "pipelined"
+    if not ONE_GPU and torch.cuda.device_count() < world:
+        raise SystemExit(f"{world} ranks but only {torch.cuda.device_count()} visible GPU(s)")
     torch.cuda.set_device(local)
     if args.stage_of > 0:
         if world > 1 or not 0 <= args.stage < args.stage_of:
@@ -626,6 +762,17 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(BACKEND)
+        # communicator evidence for the driver: every rank's device, gathered on rank 0
+        me = {"rank": rank, "local_rank": local, "device": torch.cuda.get_device_name(local),
+              "pci_bus_id": torch.cuda.get_device_properties(local).pci_bus_id
+              if hasattr(torch.cuda.get_device_properties(local), "pci_bus_id") else None}
+        ranks = [None] * world
+        dist.all_gather_object(ranks, me)
+        config["ranks"] = ranks
+        config["backend"] = BACKEND
+        if rank == 0:
+            print(f"[bench] {BACKEND} process group up: world={world}, devices "
+                  + ", ".join(f"r{r['rank']}:cuda:{r['local_rank']}" for r in ranks), file=sys.stderr, flush=True)
     if layout == "pipelined":
         if site_bytes / world > HBM_USABLE:
             if rank == 0:
@@ -652,7 +799,7 @@ def main():
     eng.set_gemm_mode({"3m": 3, "4m": 4, "ozaki": 8}[args.gemm])
     eng.set_ozaki_digits(args.oz_digits)
     small_chain = eng.small_chain_active(n)  # whole chain in one persistent launch (chi <= 128, small n)
-    config["path"] = "small_chain_kernel (one launch per step)" if small_chain else "per-mode K1 + K2/K3 kernels"
+    path = "small_chain_kernel (one launch per step)" if small_chain else "per-mode K1 + K2/K3 kernels"
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t_setup
     stream = torch.cuda.Stream(dev)  # explicit stream: events and kernels share it
@@ -719,31 +866,42 @@ def main():
     ms = dist_max(e0.elapsed_time(e1), dev)
     value = world * K * n / (ms / 1e3)
 
-    # e2e: host (pinned) uniforms + alpha in, counts out, through the same C ABI call
-    u_host = [torch.from_numpy(stream_uniforms(0, block_index(s), n, M)).pin_memory() for s in range(nsteps)]
-    a_host = [torch.from_numpy(alpha_stream(0, block_index(s), n, M, sigma)).pin_memory() for s in range(nsteps)]
-    c_host = torch.empty((n, M), dtype=torch.int32).pin_memory()
-    st_host = torch.zeros(n, dtype=torch.uint8).pin_memory()
+    # e2e: host (pinned) uniforms + alpha in, counts + status out, through the same C ABI call, every
+    # step's H2D and D2H inside the timed region.  The K steps are ONE call over K n samples with
+    # micro-batch n (mps_set_micro_batch): each micro-batch's inputs go up and its counts come down on
+    # the copy engines while the neighbouring micro-batches compute, one host synchronisation per call.
+    e2e_first = (rank * (W + K)) * n  # this rank's contiguous index block for the e2e run
 
-    def step_e2e(s):
-        st_host.zero_()
-        eng.run(block_index(s), n, c_host.numpy(), uniforms=u_host[s].numpy(), alpha=a_host[s].numpy(),
-                status=st_host.numpy(), stream=stream.cuda_stream)
+    def host_block(first, count):
+        u = torch.from_numpy(stream_uniforms(0, first, count, M)).pin_memory()
+        a = torch.from_numpy(alpha_stream(0, first, count, M, sigma)).pin_memory()
+        return u, a, torch.empty((count, M), dtype=torch.int32).pin_memory(), torch.zeros(count, dtype=torch.uint8).pin_memory()
 
-    for s in range(W):
-        step_e2e(s)
+    eng.set_micro_batch(n)
+    uw, aw, cw, sw = host_block(e2e_first, W * n)
+    ue, ae, ce, se = host_block(e2e_first + W * n, K * n)
+    eng.run(e2e_first, W * n, cw.numpy(), uniforms=uw.numpy(), alpha=aw.numpy(), status=sw.numpy(),
+            stream=stream.cuda_stream)
     barrier()
     e2 = torch.cuda.Event(enable_timing=True)
     e3 = torch.cuda.Event(enable_timing=True)
     e2.record(stream)
-    for s in range(W, W + K):
-        step_e2e(s)
+    eng.run(e2e_first + W * n, K * n, ce.numpy(), uniforms=ue.numpy(), alpha=ae.numpy(), status=se.numpy(),
+            stream=stream.cuda_stream)
     e3.record(stream)
     barrier()
+    eng.set_micro_batch(0)
     ms_e2e = dist_max(e2.elapsed_time(e3), dev)
     e2e = world * K * n / (ms_e2e / 1e3)
+    e2e_ok = bool((ce >= 0).all().item()) and not bool((se & 1).any().item())
 
-    ok = bool((counts[W:] >= 0).all().item()) and not bool((status[W:] & 1).any().item())
+    ok = bool((counts[W:] >= 0).all().item()) and not bool((status[W:] & 1).any().item()) and e2e_ok
+    # parity of this run's own outputs: the first samples of timed step W against the oracle
+    n_chk = min(32, n)
+    parity = parity_spot_check(eng, mps, 0, M, block_index(W), n_chk, stream.cuda_stream, sigma,
+                               uniforms=u_dev[W][:n_chk], alpha=a_dev[W][:n_chk],
+                               ref_counts=counts[W][:n_chk].cpu().numpy(), gemm_mode=args.gemm)
+    ok = ok and parity["ok"]
 
     # Same run, same inputs, K1 emulated on the INT8 tensor cores (gemm mode 8, Ozaki, ~1e-13):
     # reported next to the FP64-DMMA headline (the path the north star names) as "alt_gemm".
@@ -848,9 +1006,12 @@ def main():
         "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
         "data": "synthetic (random row-orthonormal sites from seeds, counter-stream uniforms and alpha)",
-        "config": config,
+        "config": config, "path": path,
         "e2e": {"value": e2e, "unit": "samples/s", "h2d_bytes_per_step": n * M * (8 + 16) + n,
-                "d2h_bytes_per_step": n * M * 4 + n},
+                "d2h_bytes_per_step": n * M * 4 + n,
+                "how": "one C-ABI call over the K steps' K n samples from pinned host arrays, micro-batch n: "
+                       "per step an H2D of its uniforms + alpha + status and a D2H of its counts + status, "
+                       "overlapping the neighbouring steps' kernels; one host synchronisation"},
         "gpu_launches": int(launches),
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_note": traffic_note,
@@ -870,6 +1031,7 @@ def main():
                       if prof["draw_ms"] > 0 else None}},
         "clocks": ck,
         "valid_outputs": ok,
+        "parity": parity,
         "setup_s": setup_s,
     }
     if alt is not None:

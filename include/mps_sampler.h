@@ -65,7 +65,10 @@ extern "C" {
 /* mps_set_site flags */
 #define MPS_SITE_HOST 0          /* gamma is host memory: copied into context-owned HBM */
 #define MPS_SITE_DEVICE_COPY 1   /* gamma is device memory: copied */
-#define MPS_SITE_DEVICE_BORROW 2 /* gamma is device memory: borrowed, caller keeps it alive */
+#define MPS_SITE_DEVICE_BORROW 2 /* gamma is device memory: borrowed, caller keeps it alive AND
+                                    unchanged -- the context derives private copies from it at
+                                    load time (3M sum plane, small-chain layout, INT8 digit planes),
+                                    so an in-place edit must be followed by mps_set_site again */
 #define MPS_SITE_HOST_STREAM 3   /* gamma is host memory, kept there (pinned via cudaHostRegister
                                     unless already pinned; caller keeps it alive) and streamed
                                     into a 2-slot HBM ring on a copy stream ahead of each GEMM:
@@ -98,7 +101,10 @@ int mps_set_site(mps_ctx* ctx, int m, int chi_l, int chi_r, int D,
 /* Seed the on-device counter streams (used when uniforms / alpha are NULL):
  * uniforms of sample i are _stream_uniforms(seed, i, M) bit-for-bit
  * (sampler.py:109-125); alpha_sigma >= 0 enables on-device alpha ~ CN(0, sigma^2)
- * from the alpha stream (oracle decision 7); alpha_sigma < 0 disables it. */
+ * from the alpha stream (oracle decision 7); alpha_sigma < 0 disables it.
+ * seed must be < 2^63 (MPS_ERR_VALIDATION otherwise): numpy turns larger seeds in a
+ * key list into float64, which collapses the alpha stream's block keys; the raw
+ * uniform stream (mps_stream_uniforms) keeps numpy's behaviour for any seed. */
 int mps_set_streams(mps_ctx* ctx, uint64_t seed, double alpha_sigma);
 
 /* Sample n paths (global sample indices first_index .. first_index+n-1)
@@ -157,6 +163,11 @@ int mps_set_gemm_config(mps_ctx* ctx, int cfg);
  * to the caller's stream) so one block's draw kernels and GEMM tails overlap another's
  * GEMMs.  Per-sample results are identical for any lane count. */
 int mps_set_lanes(mps_ctx* ctx, int lanes);
+/* Micro-batch size for calls with host arrays (0, the default: a call is one micro-batch).  With
+ * micro > 0, a mps_sample / mps_sample_range call of n > micro samples runs as micro-batches of
+ * `micro` rows whose host<->device copies (copy-engine streams) overlap the neighbouring
+ * micro-batches' kernels, with one host synchronisation per call; results are identical. */
+int mps_set_micro_batch(mps_ctx* ctx, int micro);
 /* Small chains (complex128, 3M product mode, every site chi_l <= 128 and chi_r * D <= 1024):
  * run the whole mode range of a call as ONE persistent kernel -- clusters of 16 CTAs each own
  * 16 sample rows, exchange C rows and the next state through distributed shared memory and never
@@ -232,6 +243,12 @@ int mps_displacement(const void* alpha, int count, int D, void* out, uint64_t st
  * numpy Philox / _stream_uniforms. */
 int mps_stream_uniforms(uint64_t seed, int64_t first, int count, int M, double* out,
                         uint64_t stream);
+
+#ifdef SC_TRACE
+/* Debug builds only (-DSC_TRACE, tools/chain_trace.py): copy the small-chain kernel's clock64
+ * stamps of CTA 0 (2 x 256 x 8 long long: producer / owner side, per mode) to out. */
+int mps_debug_chain_trace(long long* out);
+#endif
 
 #ifdef __cplusplus
 }

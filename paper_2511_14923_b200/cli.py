@@ -18,7 +18,7 @@ import time
 import numpy as np
 
 from .errors import GbsError, ValidationError
-from .formats import load_counts, load_mps, save_clicks_text, save_counts, save_mps
+from .formats import load_counts_file, load_mps, save_clicks_text, save_counts, save_mps
 from .mps import MPS
 from .sampler import MpsSamplerConfig, batch_sample, chain_log_probability
 
@@ -72,7 +72,9 @@ def cmd_sample(args) -> int:
     config = MpsSamplerConfig(N=args.samples, seed=args.seed, alpha_sigma=args.alpha_sigma,
                               batch_size=args.batch_size, device=args.device)
     batch = batch_sample(config, mps)
-    save_counts(args.out, batch.counts, mps.D, seed=args.seed)
+    # the rows' sample indices and the displacement law travel with the counts, so `evaluate`
+    # scores each row under its own streams (failed samples are dropped from batch.counts)
+    save_counts(args.out, batch.counts, mps.D, seed=args.seed, alpha_sigma=args.alpha_sigma, indices=batch.indices)
     outputs = [args.out]
     if args.clicks_out:
         save_clicks_text(args.clicks_out, batch.counts, seed=args.seed)
@@ -87,24 +89,63 @@ def cmd_sample(args) -> int:
     return 0
 
 
+def _sigma_arg(text):
+    """--alpha-sigma value: a float >= 0, or "none" for no displacement stream."""
+    if text.lower() == "none":
+        return None
+    v = float(text)
+    if not (v >= 0.0 and np.isfinite(v)):
+        raise argparse.ArgumentTypeError("alpha-sigma must be a finite number >= 0 or 'none'")
+    return v
+
+
+_UNSET = object()
+
+
 def cmd_evaluate(args) -> int:
-    """Log joint probability of each count row under the MPS (teacher-forced chain on the GPU;
-    row i is sample index start + i of the displacement stream)."""
+    """Log joint probability of each count row under the MPS (teacher-forced chain on the GPU).
+    Row i is scored under the streams of its own sample index and the displacement law the counts
+    were drawn with, both read from the counts file (v2); a v1 file carries neither, so then
+    --alpha-sigma and --start must be given explicitly."""
     t0 = time.perf_counter()
     mps = load_mps(args.mps, device="cuda" if args.device_sites else None)
-    counts, D, seed = load_counts(args.counts)
+    f = load_counts_file(args.counts)
+    counts, D, seed = f["counts"], f["D"], f["seed"]
     if D != mps.D or counts.shape[1] != mps.M:
         raise ValidationError(f"counts file (M={counts.shape[1]}, D={D}) does not match the MPS (M={mps.M}, D={mps.D})")
+    if args.alpha_sigma is not _UNSET:
+        sigma = args.alpha_sigma
+        if f["alpha_sigma"] != "unknown" and sigma != f["alpha_sigma"]:
+            raise ValidationError(f"--alpha-sigma {sigma} contradicts the counts file's {f['alpha_sigma']}")
+    elif f["alpha_sigma"] == "unknown":
+        raise ValidationError("the counts file does not record alpha_sigma (v1 file): pass --alpha-sigma "
+                              "(a number, or 'none' for no displacement)")
+    else:
+        sigma = f["alpha_sigma"]
+    if f["indices"] is not None:
+        if args.start is not None:
+            raise ValidationError("the counts file records each row's sample index; --start does not apply")
+        idx = f["indices"]
+    else:
+        if args.start is None:
+            raise ValidationError("the counts file does not record sample indices (v1 file): pass --start")
+        idx = args.start + np.arange(counts.shape[0], dtype=np.int64)
     config = MpsSamplerConfig(N=counts.shape[0], seed=seed if args.seed is None else args.seed,
-                              alpha_sigma=args.alpha_sigma, batch_size=args.batch_size, device=args.device)
+                              alpha_sigma=sigma, batch_size=args.batch_size, device=args.device)
     t1 = time.perf_counter()
-    logp = chain_log_probability(mps, counts, config, start=args.start)
+    logp = np.empty(counts.shape[0])
+    # rows with consecutive sample indices are evaluated as one run (one stream window each)
+    breaks = np.nonzero(np.diff(idx) != 1)[0] + 1
+    for lo, hi in zip(np.r_[0, breaks], np.r_[breaks, len(idx)]):
+        if hi > lo:
+            logp[lo:hi] = chain_log_probability(mps, counts[lo:hi], config, start=int(idx[lo]))
     dt = time.perf_counter() - t1
     np.save(args.out, logp)
     fin = np.isfinite(logp)
-    cfg = {k: v for k, v in vars(args).items() if k != "func"}
+    cfg = {k: (None if v is _UNSET else v) for k, v in vars(args).items() if k != "func"}
     _emit(_manifest("evaluate", cfg, [args.mps, args.counts], [args.out], t0, extra={
         "M": mps.M, "D": mps.D, "chi": mps.chi, "n": int(counts.shape[0]), "seed_used": config.seed,
+        "alpha_sigma_used": sigma, "counts_file_version": f["version"],
         "n_in_support": int(fin.sum()), "mean_logp": float(logp[fin].mean()) if fin.any() else None,
         "throughput_per_s": counts.shape[0] / dt if dt > 0 else 0.0,
     }))
@@ -136,8 +177,10 @@ def build_parser() -> argparse.ArgumentParser:
     e.add_argument("--mps", required=True)
     e.add_argument("--counts", required=True, help="counts file (.gmpc) from `sample`")
     e.add_argument("--seed", type=int, default=None, help="stream seed (default: the counts file's)")
-    e.add_argument("--start", type=int, default=0, help="sample index of the first row")
-    e.add_argument("--alpha-sigma", type=float, default=None)
+    e.add_argument("--start", type=int, default=None,
+                   help="sample index of the first row (v1 counts files only; v2 files record every row's index)")
+    e.add_argument("--alpha-sigma", type=_sigma_arg, default=_UNSET,
+                   help="displacement law (default: the counts file's; required for v1 files; 'none' = no displacement)")
     e.add_argument("--batch-size", type=int, default=None)
     e.add_argument("--device", type=int, default=0)
     e.add_argument("--device-sites", action="store_true")

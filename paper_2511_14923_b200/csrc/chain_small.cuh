@@ -157,7 +157,10 @@ __global__ void __launch_bounds__(SC_THREADS, 1) small_chain_kernel(const __grid
         const int f0 = rank * F / SC_CL, fc = (rank + 1) * F / SC_CL - f0;
         for (int kt = 0; kt < KT; kt += SC_KS, ++sidx) {
           const int slot = sidx % SC_STAGES, nks = min(SC_KS, KT - kt);
-          if (sidx >= SC_STAGES) mbar_wait(&empty[slot], ((sidx / SC_STAGES) - 1) & 1);
+          if (sidx >= SC_STAGES) {
+            mbar_wait(&empty[slot], ((sidx / SC_STAGES) - 1) & 1);
+            fence_proxy_async();  // the consumers' ld.shared of the slot before the bulk-copy refill
+          }
           mbar_arrive_expect_tx(&full[slot], (uint32_t)(nks * fc) * 1024u);
           if (fc)
             for (int ks = 0; ks < nks; ++ks)

@@ -453,7 +453,10 @@ __global__ void __launch_bounds__(DRAW_THREADS, C64 ? 8 : 4)
     }
     if (RING && nchunks > 1) {
       __syncthreads();  // every thread is done with this slot
-      if (tid == 0 && cidx + NS < 2 * nchunks) ring_issue(cidx + NS);  // pass 1's next chunk, or pass 2's first
+      if (tid == 0 && cidx + NS < 2 * nchunks) {
+        fence_proxy_async();  // those generic-proxy reads before the bulk-copy (async-proxy) refill
+        ring_issue(cidx + NS);  // pass 1's next chunk, or pass 2's first
+      }
     }
   }
 #pragma unroll
@@ -528,7 +531,10 @@ __global__ void __launch_bounds__(DRAW_THREADS, C64 ? 8 : 4)
     }
     if (RING && nchunks > 1) {
       __syncthreads();
-      if (tid == 0 && nchunks + cidx + NS < 2 * nchunks) ring_issue(nchunks + cidx + NS);
+      if (tid == 0 && nchunks + cidx + NS < 2 * nchunks) {
+        fence_proxy_async();
+        ring_issue(nchunks + cidx + NS);
+      }
     }
   }
 }

@@ -31,6 +31,7 @@
 
 using namespace mps;
 
+
 namespace {
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -227,6 +228,13 @@ struct mps_ctx {
   DevBuf<float2> lc32[MAX_LANES];                   // c64 C buffer
   DevBuf<float> ones_hi, ones_lo, in_hi, in_lo;
   DevBuf<double> ones_sum, in_sum;
+  // multi-micro-batch calls (mps_set_micro_batch): a call of n > micro samples with host arrays runs
+  // as micro-batches of `micro` rows whose H2D (cs_in) and D2H (cs_out) overlap the neighbouring
+  // micro-batches' compute; device slots are double-buffered, one host synchronisation per call
+  int micro = 0;
+  cudaStream_t cs_in = nullptr, cs_out = nullptr;
+  cudaEvent_t pe_in[2] = {}, pe_comp[2] = {}, pe_out = nullptr;
+  DevBuf<uint8_t> pipe_d;
   // workspaces
   DevBuf<double2> ones;
   // host arrays of a call, packed: [u | alpha | disp | counts | marginals | status] (256-B aligned
@@ -408,9 +416,10 @@ using G64x64 = GemmCfgT<64, 64, 2, 2, 4, 3>;
 using G32x128 = GemmCfgT<32, 128, 1, 4, 4, 2>;
 using G64x80 = GemmCfgT<64, 80, 4, 1, 4, 3>;    // 40 complex columns: whole D=10 groups, 4000 tiles at C3
 using G64x64w8 = GemmCfgT<64, 64, 4, 2, 4, 2>;  // 3M: 8 warps of 16 x 16 complex, 16 warps/SM
-// (a 32x64 tile with 2 x 2 warps of 16 x 16 complex, 4 CTAs/SM, was dropped: with the state sum planes
-//  and two concurrent lanes it intermittently produced wrong values in the upper 16 rows of a tile,
-//  ~5% of fresh-shape calls, tools/tune_race_probe.py; every other config ran 720 calls clean)
+// 32 x 64 tiles of 2 x 2 warps (16 x 16 complex each) at 4 CTAs/SM: the config that exposed the ring's
+// cross-proxy WAR race (a TMA refill landing before a slow warp's last ld.shared of the slot, ~1% of
+// chains with two lanes and sum planes; fixed by fence.proxy.async before every refill)
+using G32x64w4 = GemmCfgT<32, 64, 2, 2, 4, 4>;
 // deep rings for short K (chi_l ~ 100: 13 k-stages): most of K in flight at once, so a small-chi
 // GEMM costs ~one TMA round trip instead of one per ring refill (latency, not throughput, bound)
 using G16x32d8 = GemmCfgT<16, 32, 1, 1, 8, 4>;
@@ -426,7 +435,8 @@ static const GemmCfgInfo kGemm3[] = {
     cfg_info<G16x32, 3>("3m_16x32_w1x1_occ8"), cfg_info<G32x128, 3>("3m_32x128_w1x4_occ2"),
     cfg_info<G64x80, 3>("3m_64x80_w4x1_occ3"), cfg_info<G64x64w8, 3>("3m_64x64_w4x2_occ2"),
     cfg_info<G16x32d8, 3>("3m_16x32_w1x1_s8_occ4"),
-    cfg_info<G16x32d16, 3>("3m_16x32_w1x1_s16_occ2"), cfg_info<G32x64d8, 3>("3m_32x64_w2x2_s8_occ2")};
+    cfg_info<G16x32d16, 3>("3m_16x32_w1x1_s16_occ2"), cfg_info<G32x64d8, 3>("3m_32x64_w2x2_s8_occ2"),
+    cfg_info<G32x64w4, 3>("3m_32x64_w2x2_occ4")};
 constexpr int N_GEMM4 = sizeof(kGemm4) / sizeof(kGemm4[0]);
 constexpr int N_GEMM3 = sizeof(kGemm3) / sizeof(kGemm3[0]);
 constexpr int N_GEMM_CFGS = N_GEMM3 > N_GEMM4 ? N_GEMM3 : N_GEMM4;  // index bound for the API
@@ -873,6 +883,12 @@ int mps_create(int n_dev, const int* dev_ids, int layout, mps_ctx** out) {
     ok = cudaStreamCreateWithFlags(&c->lane_st[l], cudaStreamNonBlocking) == cudaSuccess &&
          cudaEventCreateWithFlags(&c->join_ev[l], cudaEventDisableTiming) == cudaSuccess;
   ok = ok && cudaStreamCreateWithFlags(&c->copy_st, cudaStreamNonBlocking) == cudaSuccess;
+  ok = ok && cudaStreamCreateWithFlags(&c->cs_in, cudaStreamNonBlocking) == cudaSuccess &&
+       cudaStreamCreateWithFlags(&c->cs_out, cudaStreamNonBlocking) == cudaSuccess &&
+       cudaEventCreateWithFlags(&c->pe_out, cudaEventDisableTiming) == cudaSuccess;
+  for (int w = 0; ok && w < 2; ++w)
+    ok = cudaEventCreateWithFlags(&c->pe_in[w], cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&c->pe_comp[w], cudaEventDisableTiming) == cudaSuccess;
   for (int w = 0; ok && w < 2; ++w) {
     ok = cudaEventCreateWithFlags(&c->slot_ready[w], cudaEventDisableTiming) == cudaSuccess;
     for (int l = 0; ok && l < mps_ctx::MAX_LANES; ++l)
@@ -1035,38 +1051,40 @@ int mps_set_site(mps_ctx* c, int m, int chi_l, int chi_r, int D, const void* gam
 int mps_set_streams(mps_ctx* c, uint64_t seed, double alpha_sigma) {
   if (!c) return MPS_ERR_VALIDATION;
   if (!(alpha_sigma == alpha_sigma)) return fail(c, MPS_ERR_VALIDATION, "alpha_sigma is NaN");
+  // numpy routes a key list holding an int >= 2^63 through float64: the uniform stream keeps that
+  // quirk (numpy_key0) but the alpha stream's [seed, 2^62 + i/64] keys would collapse, so refuse
+  if (seed >= (1ull << 63)) return fail(c, MPS_ERR_VALIDATION, "seed must be < 2^63, got %llu",
+                                        (unsigned long long)seed);
   c->seed = seed;
   c->alpha_sigma = alpha_sigma;
   return MPS_OK;
 }
 
-int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, int n, const double* uniforms,
-                     int64_t ld_u, const void* disp, const void* alpha, const void* state_in, void* state_out,
-                     int32_t* counts, int64_t ld_c, double* marginals, uint8_t* status, uint64_t stream) {
-  if (!c) return MPS_ERR_VALIDATION;
-  c->err.clear();
-  if (c->M == 0) return fail(c, MPS_ERR_VALIDATION, "context not configured");
-  if (m_begin < 0 || m_end > c->M || m_begin >= m_end)
-    return fail(c, MPS_ERR_VALIDATION, "mode range [%d, %d) invalid for M=%d", m_begin, m_end, c->M);
-  if (n < 0) return fail(c, MPS_ERR_VALIDATION, "n must be >= 0");
-  if (first_index < 0) return fail(c, MPS_ERR_VALIDATION, "first_index must be >= 0");
-  if (!counts) return fail(c, MPS_ERR_VALIDATION, "counts output is required");
-  if (ld_c < c->M || (uniforms && ld_u < c->M)) return fail(c, MPS_ERR_VALIDATION, "row strides must be >= M");
-  for (int m = m_begin; m < m_end; ++m)
-    if (!c->sites[m].loaded) return fail(c, MPS_ERR_VALIDATION, "site %d not loaded", m);
-  for (int m = m_begin + 1; m < m_end; ++m)
-    if (c->sites[m].chi_l != c->sites[m - 1].chi_r)
-      return fail(c, MPS_ERR_VALIDATION, "bond mismatch between sites %d and %d", m - 1, m);
-  if (n == 0) return MPS_OK;
-  if (!state_in && c->sites[m_begin].chi_l != 1)
-    return fail(c, MPS_ERR_VALIDATION, "state_in is required when chi_l of site %d is %d", m_begin,
-                c->sites[m_begin].chi_l);
-  if (state_in && !is_device_ptr(state_in)) return fail(c, MPS_ERR_VALIDATION, "state_in must be device memory");
-  if (state_out && !is_device_ptr(state_out)) return fail(c, MPS_ERR_VALIDATION, "state_out must be device memory");
+// Device-side pointers of one chain call (host arrays already staged by mps_sample_range).
+struct ChainIO {
+  const double* u;
+  int64_t ld_u;
+  const double2* alpha;
+  const double2* disp;
+  int32_t* counts;
+  int64_t ld_c;
+  double* marg;
+  uint8_t* status;
+};
 
-  cudaSetDevice(c->device);
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);  // 0 = legacy default stream
+// The mode loop of one micro-batch of n samples over sites [m_begin, m_end) on stream st: the
+// persistent small-chain kernel, or K1 + K2/K3 per mode over up to `lanes` row-block chains.
+// Every pointer in io is device memory; nothing here synchronises the host.
+static int run_chain(mps_ctx* c, int m_begin, int m_end, int64_t first_index, int n, const ChainIO& io,
+                     const void* state_in, void* state_out, cudaStream_t st) {
   const int M = c->M, D = c->D;
+  const double* u_dev = io.u;
+  const int64_t ldu = io.ld_u, ld_c = io.ld_c;
+  const double2* alpha_dev = io.alpha;
+  const double2* disp_dev = io.disp;
+  int32_t* counts_dev = io.counts;
+  double* marg_dev = io.marg;
+  uint8_t* status_dev = io.status;
   int chi_max = 1;
   for (int m = m_begin; m < m_end; ++m) chi_max = std::max(chi_max, std::max(c->sites[m].chi_l, c->sites[m].chi_r));
   size_t cmax = 0;
@@ -1107,76 +1125,6 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
     for (int m = m_begin; m < m_end; ++m) CU(c, ozaki_prepare_site(c->sites[m], D, c->oz_S), "Ozaki site digits");
   }
 
-  // ---- inputs: host arrays are packed into one pinned buffer and moved by ONE H2D copy (and the
-  //      host outputs come back by one D2H): at C1/C2 sizes a call pays per-copy API latency, not
-  //      bytes ----
-  const bool u_host = uniforms && !is_device_ptr(uniforms);
-  const bool alpha_host = alpha && !is_device_ptr(alpha);
-  const bool disp_host = disp && !is_device_ptr(disp);
-  const bool counts_host = !is_device_ptr(counts);
-  const bool marg_host = marginals && !is_device_ptr(marginals);
-  const bool status_host = status && !is_device_ptr(status);
-  const bool status_own = !status || status_host;  // the library's status row (zeroed or copied in)
-  size_t io_off = 0;
-  auto field = [&](bool on, size_t bytes) {
-    const size_t o = io_off;
-    if (on) io_off += (bytes + 255) & ~(size_t)255;
-    return o;
-  };
-  const size_t o_u = field(u_host, (size_t)n * ld_u * sizeof(double));
-  const size_t o_a = field(alpha_host, (size_t)n * M * sizeof(double2));
-  const size_t o_d = field(disp_host, (size_t)n * M * D * D * sizeof(double2));
-  const size_t o_io = io_off;  // outputs (and in-out fields) from here on
-  const size_t o_c = field(counts_host, (size_t)n * ld_c * sizeof(int32_t));
-  const size_t o_m = field(marg_host, (size_t)n * ld_c * D * sizeof(double));
-  const size_t o_s = field(status_own, (size_t)n);
-  const size_t io_total = io_off;
-  if (io_total > 0) {
-    CU(c, c->io_d.ensure(io_total), "alloc staging");
-    if (c->io_h_cap < io_total) {
-      if (c->io_h) cudaFreeHost(c->io_h);
-      c->io_h = nullptr;
-      c->io_h_cap = 0;
-      CU(c, cudaMallocHost(&c->io_h, io_total), "alloc pinned staging");
-      c->io_h_cap = io_total;
-    }
-  }
-  uint8_t* const hb = c->io_h;
-  uint8_t* const db = c->io_d.p;
-  const bool counts_in = counts_host && (m_end - m_begin < M || c->forced);  // untouched columns / forced outcomes
-  const bool marg_in = marg_host && m_end - m_begin < M;
-  if (u_host) memcpy(hb + o_u, uniforms, (size_t)n * ld_u * sizeof(double));
-  if (alpha_host) memcpy(hb + o_a, alpha, (size_t)n * M * sizeof(double2));
-  if (disp_host) memcpy(hb + o_d, disp, (size_t)n * M * D * D * sizeof(double2));
-  if (counts_in) memcpy(hb + o_c, counts, (size_t)n * ld_c * sizeof(int32_t));
-  if (marg_in) memcpy(hb + o_m, marginals, (size_t)n * ld_c * D * sizeof(double));
-  if (status_host) memcpy(hb + o_s, status, n);
-  // inputs, plus the in-out tail when any of it carries data in.  Every call that copies from the
-  // pinned buffer synchronises before returning (host inputs or host outputs), so the next call may
-  // refill it; a library-owned status row is zeroed on the device instead (no host staging).
-  const size_t h2d = (status_host || counts_in || marg_in) ? io_total : o_io;
-  if (h2d > 0) CU(c, cudaMemcpyAsync(db, hb, h2d, cudaMemcpyHostToDevice, st), "H2D inputs");
-  if (!status) CU(c, cudaMemsetAsync(db + o_s, 0, n, st), "zero status");
-  const double* u_dev = u_host ? reinterpret_cast<const double*>(db + o_u) : uniforms;
-  const int64_t ldu = ld_u;
-  const double2* alpha_dev = alpha_host ? reinterpret_cast<const double2*>(db + o_a) : (const double2*)alpha;
-  const double2* disp_dev = disp_host ? reinterpret_cast<const double2*>(db + o_d) : (const double2*)disp;
-  int32_t* counts_dev = counts_host ? reinterpret_cast<int32_t*>(db + o_c) : counts;
-  double* marg_dev = marg_host ? reinterpret_cast<double*>(db + o_m) : marginals;
-  uint8_t* status_dev = status_own ? db + o_s : status;
-
-  // ---- outputs back to the host: one D2H of the in-out tail, then host copies ----
-  const bool host_out = counts_host || marg_host || status_host;
-  const bool host_in = u_host || alpha_host || disp_host;
-  auto finish = [&]() -> int {
-    if (host_out) CU(c, cudaMemcpyAsync(hb + o_io, db + o_io, io_total - o_io, cudaMemcpyDeviceToHost, st), "D2H outputs");
-    // host inputs: the pinned staging is reused by the next call
-    if (host_out || host_in) CU(c, cudaStreamSynchronize(st), "stream sync");
-    if (counts_host) memcpy(counts, hb + o_c, (size_t)n * ld_c * sizeof(int32_t));
-    if (marg_host) memcpy(marginals, hb + o_m, (size_t)n * ld_c * D * sizeof(double));
-    if (status_host) memcpy(status, hb + o_s, n);
-    return MPS_OK;
-  };
 
   if (small_chain_ok(c, m_begin, m_end, n)) {
     CU(c, chain_meta_upload(c), "chain metadata");
@@ -1214,17 +1162,20 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
       cudaEventRecord(rg.a, st);
     }
     const cudaError_t le = launch_small_chain(c, P, st);
-    if (le == cudaErrorNotSupported) {
-      c->small_chain = 0;  // this GPU cannot host the clusters: per-mode kernels from now on
+    if (le != cudaSuccess) {
+      // the launch did not happen (no co-resident 16-CTA cluster fits right now: other kernels or
+      // MPS clients hold the SMs, cudaErrorClusterOutOfResources / NotSupported ...): the per-mode
+      // kernels give the same bits, so fall back to them for this and later calls
+      cudaGetLastError();
+      c->small_chain = 0;
       if (c->profile & 1) c->event_pool.insert(c->event_pool.end(), {rg.a, rg.b});
     } else {
-      CU(c, le, "small_chain launch");
       c->launches++;
       if (c->profile & 1) {
         cudaEventRecord(rg.b, st);
         c->recs.push_back(rg);
       }
-      return finish();
+      return MPS_OK;
     }
   }
 
@@ -1452,6 +1403,231 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
     CU(c, cudaStreamWaitEvent(st, c->join_ev[0], 0), "copy join wait");
   }
 
+  return MPS_OK;
+}
+
+// One call over n samples with host arrays, as micro-batches of c->micro rows: micro-batch t's inputs
+// go up on cs_in while t-1 computes on st, its outputs come down on cs_out while t+1 computes.  Host
+// arrays that are pinned are copied directly; pageable ones are packed into (inputs) / unpacked from
+// (outputs) the context's pinned staging for the whole call.  Device input/output slots are
+// double-buffered: the H2D of t waits for the compute of t-2.  One host synchronisation per call.
+// Results are bit-identical to the single-shot path (per-sample results do not depend on the split).
+static bool is_pinned_host(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+static int sample_pipelined(mps_ctx* c, int m_begin, int m_end, int64_t first_index, int n, const double* uniforms,
+                            int64_t ld_u, const void* disp, const void* alpha, const void* state_in, void* state_out,
+                            int32_t* counts, int64_t ld_c, double* marginals, uint8_t* status, cudaStream_t st) {
+  const int M = c->M, D = c->D, nb = c->micro;
+  const int chi0 = c->sites[m_begin].chi_l, chiM = c->sites[m_end - 1].chi_r;
+  // fields: host pointer, bytes per row, device-or-host, direction (in / out)
+  struct Field {
+    const uint8_t* hin;  // host source (inputs)
+    uint8_t* hout;       // host destination (outputs)
+    size_t row;          // bytes per sample row
+    bool in, out;        // host -> device, device -> host
+    bool pinned;
+    size_t stage_off;    // offset in the pinned whole-call staging (pageable arrays)
+    size_t slot_off;     // offset in a device slot
+  };
+  const bool counts_in = (m_end - m_begin < M || c->forced);
+  const bool marg_in = m_end - m_begin < M;
+  Field f[6];
+  const void* dptr[6] = {uniforms, alpha, disp, counts, marginals, status};
+  const size_t rows[6] = {(size_t)ld_u * 8, (size_t)M * 16, (size_t)M * D * D * 16, (size_t)ld_c * 4,
+                          (size_t)ld_c * D * 8, 1};
+  bool host[6];
+  for (int i = 0; i < 6; ++i) host[i] = dptr[i] && !is_device_ptr(dptr[i]);
+  size_t stage_bytes = 0, slot_bytes = 0;
+  for (int i = 0; i < 6; ++i) {
+    Field& x = f[i];
+    x.row = rows[i];
+    x.in = host[i] && (i < 3 || (i == 3 && counts_in) || (i == 4 && marg_in) || i == 5);
+    x.out = host[i] && i >= 3;
+    x.hin = (const uint8_t*)dptr[i];
+    x.hout = (uint8_t*)dptr[i];
+    x.pinned = host[i] && is_pinned_host(dptr[i]);
+    x.stage_off = stage_bytes;
+    if (host[i] && !x.pinned) stage_bytes += ((size_t)n * x.row + 255) & ~(size_t)255;
+    x.slot_off = slot_bytes;
+    if (host[i] || (i == 5 && !status)) slot_bytes += ((size_t)nb * x.row + 255) & ~(size_t)255;
+  }
+  CU(c, c->pipe_d.ensure(2 * slot_bytes), "alloc micro-batch slots");
+  if (stage_bytes > c->io_h_cap) {
+    if (c->io_h) cudaFreeHost(c->io_h);
+    c->io_h = nullptr;
+    c->io_h_cap = 0;
+    CU(c, cudaMallocHost(&c->io_h, stage_bytes), "alloc pinned staging");
+    c->io_h_cap = stage_bytes;
+  }
+  for (int i = 0; i < 6; ++i)  // pageable inputs: pack once for the whole call
+    if (f[i].in && !f[i].pinned) memcpy(c->io_h + f[i].stage_off, f[i].hin, (size_t)n * f[i].row);
+  auto hsrc = [&](int i, size_t r0) -> const uint8_t* {
+    return (f[i].pinned ? f[i].hin : c->io_h + f[i].stage_off) + r0 * f[i].row;
+  };
+  auto hdst = [&](int i, size_t r0) -> uint8_t* {
+    return (f[i].pinned ? f[i].hout : c->io_h + f[i].stage_off) + r0 * f[i].row;
+  };
+  // the copy streams start after everything already queued on st (the caller's prior work)
+  CU(c, cudaEventRecord(c->fork_ev, st), "fork");
+  CU(c, cudaStreamWaitEvent(c->cs_in, c->fork_ev, 0), "fork wait");
+  CU(c, cudaStreamWaitEvent(c->cs_out, c->fork_ev, 0), "fork wait");
+  const int T = (n + nb - 1) / nb;
+  for (int t = 0; t < T; ++t) {
+    const int w = t & 1;
+    const size_t r0 = (size_t)t * nb;
+    const int nt = std::min(nb, n - (int)r0);
+    uint8_t* slot = c->pipe_d.p + (size_t)w * slot_bytes;
+    if (t >= 2) CU(c, cudaStreamWaitEvent(c->cs_in, c->pe_comp[w], 0), "slot free");
+    for (int i = 0; i < 6; ++i)
+      if (f[i].in)
+        CU(c, cudaMemcpyAsync(slot + f[i].slot_off, hsrc(i, r0), (size_t)nt * f[i].row, cudaMemcpyHostToDevice,
+                              c->cs_in), "H2D micro-batch");
+    CU(c, cudaEventRecord(c->pe_in[w], c->cs_in), "inputs ready");
+    CU(c, cudaStreamWaitEvent(st, c->pe_in[w], 0), "inputs wait");
+    ChainIO io;
+    io.u = !uniforms ? nullptr : host[0] ? (const double*)(slot + f[0].slot_off) : uniforms + r0 * ld_u;
+    io.ld_u = ld_u;
+    io.alpha = !alpha ? nullptr : host[1] ? (const double2*)(slot + f[1].slot_off) : (const double2*)alpha + r0 * M;
+    io.disp = !disp ? nullptr : host[2] ? (const double2*)(slot + f[2].slot_off)
+                                         : (const double2*)disp + r0 * M * D * D;
+    io.counts = host[3] ? (int32_t*)(slot + f[3].slot_off) : counts + r0 * ld_c;
+    io.ld_c = ld_c;
+    io.marg = !marginals ? nullptr : host[4] ? (double*)(slot + f[4].slot_off) : marginals + r0 * ld_c * D;
+    io.status = (!status || host[5]) ? slot + f[5].slot_off : status + r0;
+    if (!status) CU(c, cudaMemsetAsync(io.status, 0, nt, st), "zero status");
+    const void* sin = state_in ? (const double2*)state_in + r0 * chi0 : nullptr;
+    void* sout = state_out ? (void*)((double2*)state_out + r0 * chiM) : nullptr;
+    if (c->dtype == MPS_C64) {
+      sin = state_in ? (const void*)((const float2*)state_in + r0 * chi0) : nullptr;
+      sout = state_out ? (void*)((float2*)state_out + r0 * chiM) : nullptr;
+    }
+    if (int rc = run_chain(c, m_begin, m_end, first_index + (int64_t)r0, nt, io, sin, sout, st)) return rc;
+    CU(c, cudaEventRecord(c->pe_comp[w], st), "compute done");
+    CU(c, cudaStreamWaitEvent(c->cs_out, c->pe_comp[w], 0), "outputs wait");
+    for (int i = 3; i < 6; ++i)
+      if (f[i].out)
+        CU(c, cudaMemcpyAsync(hdst(i, r0), slot + f[i].slot_off, (size_t)nt * f[i].row, cudaMemcpyDeviceToHost,
+                              c->cs_out), "D2H micro-batch");
+  }
+  CU(c, cudaEventRecord(c->pe_out, c->cs_out), "outputs done");
+  CU(c, cudaStreamWaitEvent(st, c->pe_out, 0), "join");
+  CU(c, cudaStreamSynchronize(st), "stream sync");
+  for (int i = 3; i < 6; ++i)  // pageable outputs: unpack once
+    if (f[i].out && !f[i].pinned) memcpy(f[i].hout, c->io_h + f[i].stage_off, (size_t)n * f[i].row);
+  return MPS_OK;
+}
+
+int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, int n, const double* uniforms,
+                     int64_t ld_u, const void* disp, const void* alpha, const void* state_in, void* state_out,
+                     int32_t* counts, int64_t ld_c, double* marginals, uint8_t* status, uint64_t stream) {
+  if (!c) return MPS_ERR_VALIDATION;
+  c->err.clear();
+  if (c->M == 0) return fail(c, MPS_ERR_VALIDATION, "context not configured");
+  if (m_begin < 0 || m_end > c->M || m_begin >= m_end)
+    return fail(c, MPS_ERR_VALIDATION, "mode range [%d, %d) invalid for M=%d", m_begin, m_end, c->M);
+  if (n < 0) return fail(c, MPS_ERR_VALIDATION, "n must be >= 0");
+  if (first_index < 0) return fail(c, MPS_ERR_VALIDATION, "first_index must be >= 0");
+  if (!counts) return fail(c, MPS_ERR_VALIDATION, "counts output is required");
+  if (ld_c < c->M || (uniforms && ld_u < c->M)) return fail(c, MPS_ERR_VALIDATION, "row strides must be >= M");
+  for (int m = m_begin; m < m_end; ++m)
+    if (!c->sites[m].loaded) return fail(c, MPS_ERR_VALIDATION, "site %d not loaded", m);
+  for (int m = m_begin + 1; m < m_end; ++m)
+    if (c->sites[m].chi_l != c->sites[m - 1].chi_r)
+      return fail(c, MPS_ERR_VALIDATION, "bond mismatch between sites %d and %d", m - 1, m);
+  if (n == 0) return MPS_OK;
+  if (!state_in && c->sites[m_begin].chi_l != 1)
+    return fail(c, MPS_ERR_VALIDATION, "state_in is required when chi_l of site %d is %d", m_begin,
+                c->sites[m_begin].chi_l);
+  if (state_in && !is_device_ptr(state_in)) return fail(c, MPS_ERR_VALIDATION, "state_in must be device memory");
+  if (state_out && !is_device_ptr(state_out)) return fail(c, MPS_ERR_VALIDATION, "state_out must be device memory");
+
+  cudaSetDevice(c->device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);  // 0 = legacy default stream
+  const int M = c->M, D = c->D;
+  // ---- inputs: host arrays are packed into one pinned buffer and moved by ONE H2D copy (and the
+  //      host outputs come back by one D2H): at C1/C2 sizes a call pays per-copy API latency, not
+  //      bytes ----
+  const bool u_host = uniforms && !is_device_ptr(uniforms);
+  const bool alpha_host = alpha && !is_device_ptr(alpha);
+  const bool disp_host = disp && !is_device_ptr(disp);
+  const bool counts_host = !is_device_ptr(counts);
+  const bool marg_host = marginals && !is_device_ptr(marginals);
+  const bool status_host = status && !is_device_ptr(status);
+  const bool status_own = !status || status_host;  // the library's status row (zeroed or copied in)
+  if (c->micro > 0 && n > c->micro && (u_host || alpha_host || disp_host || counts_host || marg_host || status_host))
+    return sample_pipelined(c, m_begin, m_end, first_index, n, uniforms, ld_u, disp, alpha, state_in, state_out,
+                            counts, ld_c, marginals, status, st);
+  size_t io_off = 0;
+  auto field = [&](bool on, size_t bytes) {
+    const size_t o = io_off;
+    if (on) io_off += (bytes + 255) & ~(size_t)255;
+    return o;
+  };
+  const size_t o_u = field(u_host, (size_t)n * ld_u * sizeof(double));
+  const size_t o_a = field(alpha_host, (size_t)n * M * sizeof(double2));
+  const size_t o_d = field(disp_host, (size_t)n * M * D * D * sizeof(double2));
+  const size_t o_io = io_off;  // outputs (and in-out fields) from here on
+  const size_t o_c = field(counts_host, (size_t)n * ld_c * sizeof(int32_t));
+  const size_t o_m = field(marg_host, (size_t)n * ld_c * D * sizeof(double));
+  const size_t o_s = field(status_own, (size_t)n);
+  const size_t io_total = io_off;
+  if (io_total > 0) {
+    CU(c, c->io_d.ensure(io_total), "alloc staging");
+    if (c->io_h_cap < io_total) {
+      if (c->io_h) cudaFreeHost(c->io_h);
+      c->io_h = nullptr;
+      c->io_h_cap = 0;
+      CU(c, cudaMallocHost(&c->io_h, io_total), "alloc pinned staging");
+      c->io_h_cap = io_total;
+    }
+  }
+  uint8_t* const hb = c->io_h;
+  uint8_t* const db = c->io_d.p;
+  const bool counts_in = counts_host && (m_end - m_begin < M || c->forced);  // untouched columns / forced outcomes
+  const bool marg_in = marg_host && m_end - m_begin < M;
+  if (u_host) memcpy(hb + o_u, uniforms, (size_t)n * ld_u * sizeof(double));
+  if (alpha_host) memcpy(hb + o_a, alpha, (size_t)n * M * sizeof(double2));
+  if (disp_host) memcpy(hb + o_d, disp, (size_t)n * M * D * D * sizeof(double2));
+  if (counts_in) memcpy(hb + o_c, counts, (size_t)n * ld_c * sizeof(int32_t));
+  if (marg_in) memcpy(hb + o_m, marginals, (size_t)n * ld_c * D * sizeof(double));
+  if (status_host) memcpy(hb + o_s, status, n);
+  // inputs, plus the in-out tail when any of it carries data in.  Every call that copies from the
+  // pinned buffer synchronises before returning (host inputs or host outputs), so the next call may
+  // refill it; a library-owned status row is zeroed on the device instead (no host staging).
+  const size_t h2d = (status_host || counts_in || marg_in) ? io_total : o_io;
+  if (h2d > 0) CU(c, cudaMemcpyAsync(db, hb, h2d, cudaMemcpyHostToDevice, st), "H2D inputs");
+  if (!status) CU(c, cudaMemsetAsync(db + o_s, 0, n, st), "zero status");
+  ChainIO io;
+  io.u = u_host ? reinterpret_cast<const double*>(db + o_u) : uniforms;
+  io.ld_u = ld_u;
+  io.alpha = alpha_host ? reinterpret_cast<const double2*>(db + o_a) : (const double2*)alpha;
+  io.disp = disp_host ? reinterpret_cast<const double2*>(db + o_d) : (const double2*)disp;
+  io.counts = counts_host ? reinterpret_cast<int32_t*>(db + o_c) : counts;
+  io.ld_c = ld_c;
+  io.marg = marg_host ? reinterpret_cast<double*>(db + o_m) : marginals;
+  io.status = status_own ? db + o_s : status;
+
+  // ---- outputs back to the host: one D2H of the in-out tail, then host copies ----
+  const bool host_out = counts_host || marg_host || status_host;
+  const bool host_in = u_host || alpha_host || disp_host;
+  auto finish = [&]() -> int {
+    if (host_out) CU(c, cudaMemcpyAsync(hb + o_io, db + o_io, io_total - o_io, cudaMemcpyDeviceToHost, st), "D2H outputs");
+    // host inputs: the pinned staging is reused by the next call
+    if (host_out || host_in) CU(c, cudaStreamSynchronize(st), "stream sync");
+    if (counts_host) memcpy(counts, hb + o_c, (size_t)n * ld_c * sizeof(int32_t));
+    if (marg_host) memcpy(marginals, hb + o_m, (size_t)n * ld_c * D * sizeof(double));
+    if (status_host) memcpy(status, hb + o_s, n);
+    return MPS_OK;
+  };
+
+  if (int rc = run_chain(c, m_begin, m_end, first_index, n, io, state_in, state_out, st)) return rc;
   return finish();
 }
 
@@ -1537,6 +1713,14 @@ void mps_destroy(mps_ctx* c) {
       if (c->slot_free[w][l]) cudaEventDestroy(c->slot_free[w][l]);
   }
   if (c->copy_st) cudaStreamDestroy(c->copy_st);
+  if (c->cs_in) cudaStreamDestroy(c->cs_in);
+  if (c->cs_out) cudaStreamDestroy(c->cs_out);
+  for (int w = 0; w < 2; ++w) {
+    if (c->pe_in[w]) cudaEventDestroy(c->pe_in[w]);
+    if (c->pe_comp[w]) cudaEventDestroy(c->pe_comp[w]);
+  }
+  if (c->pe_out) cudaEventDestroy(c->pe_out);
+  c->pipe_d.release();
   c->ones.release();
   c->io_d.release();
   if (c->io_h) cudaFreeHost(c->io_h);
@@ -1712,6 +1896,13 @@ int mps_small_chain_eligible(const mps_ctx* c, int m_begin, int m_end, int n) {
   for (int m = m_begin; m < m_end; ++m)
     if (!c->sites[m].loaded) return 0;
   return small_chain_ok(c, m_begin, m_end, n) ? 1 : 0;
+}
+
+int mps_set_micro_batch(mps_ctx* c, int micro) {
+  if (!c) return MPS_ERR_VALIDATION;
+  if (micro < 0) return fail(c, MPS_ERR_VALIDATION, "micro-batch size must be >= 0, got %d", micro);
+  c->micro = micro;
+  return MPS_OK;
 }
 
 int mps_set_lanes(mps_ctx* c, int lanes) {

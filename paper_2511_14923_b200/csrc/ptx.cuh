@@ -30,6 +30,11 @@ __device__ __forceinline__ void fence_barrier_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
+// Orders this thread's prior generic-proxy shared-memory accesses -- including other threads'
+// accesses ordered before it by a barrier / mbarrier -- before its subsequent async-proxy ones
+// (TMA / bulk copies).  Required before a TMA refill overwrites a ring slot that threads read with
+// ld.shared: without it the refill can land before a slow warp's last loads of the slot
+// (measured: ~1% of chains at 4 CTAs/SM with two lanes).
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }

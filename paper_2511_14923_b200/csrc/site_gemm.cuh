@@ -145,6 +145,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     // by the time warp 0 finishes kt, so this wait rarely blocks.
     if (threadIdx.x == 0 && kt >= 1 && kt - 1 + Cfg::STAGES < KT) {
       mbar_wait(&empty[(kt - 1) % Cfg::STAGES], ((kt - 1) / Cfg::STAGES) & 1);
+      fence_proxy_async();  // the slot's generic-proxy reads before the TMA (async-proxy) refill
       issue(kt - 1 + Cfg::STAGES);
     }
   }
@@ -201,7 +202,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * S::STAGE_BYTES);
   uint64_t* empty = full + Cfg::STAGES;
   // stage layout: [V tile | Gamma boxes | Gamma-sum boxes | V-sum tile]
-  constexpr int OFF_B = Cfg::A_BYTES, OFF_BS = Cfg::STAGE_BYTES, OFF_AS = Cfg::STAGE_BYTES + S::BS_BYTES;
+  constexpr int OFF_A = 0, OFF_B = Cfg::A_BYTES, OFF_BS = Cfg::STAGE_BYTES, OFF_AS = Cfg::STAGE_BYTES + S::BS_BYTES;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -224,7 +225,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
   auto issue_v = [&](int kt) {  // the state (written by the previous kernel) (+ its sum plane)
     const int s = kt % Cfg::STAGES;
     uint8_t* st = smem + s * S::STAGE_BYTES;
-    tma_load_2d(st, &tmap_v, kt * 16, m0, &full[s]);
+    tma_load_2d(st + OFF_A, &tmap_v, kt * 16, m0, &full[s]);
     if constexpr (SUMS) tma_load_2d(st + OFF_AS, &tmap_vs, kt * 8, m0, &full[s]);
   };
 
@@ -265,7 +266,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     const int s = kt % Cfg::STAGES;
     mbar_wait(&full[s], (kt / Cfg::STAGES) & 1);
     const uint8_t* st = smem + s * S::STAGE_BYTES;
-    const uint8_t* As = st + (warp_m * Cfg::WM + g) * 128;
+    const uint8_t* As = st + OFF_A + (warp_m * Cfg::WM + g) * 128;
     const uint8_t* Bs = st + OFF_B + warp_n * NF * (Cfg::BK_C * 128);
     const uint8_t* Ass = st + OFF_AS + (warp_m * Cfg::WM + g) * 64;
     const uint8_t* Bss = st + OFF_BS;
@@ -313,6 +314,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     if (lane == 0) mbar_arrive(&empty[s]);
     if (threadIdx.x == 0 && kt >= 1 && kt - 1 + Cfg::STAGES < KT) {
       mbar_wait(&empty[(kt - 1) % Cfg::STAGES], ((kt - 1) / Cfg::STAGES) & 1);
+      // cross-proxy WAR: the warps' generic-proxy reads of this slot (ordered before us by the
+      // empty barrier) must be ordered before the async-proxy (TMA) writes that refill it
+      fence_proxy_async();
       issue_g(kt - 1 + Cfg::STAGES);
       issue_v(kt - 1 + Cfg::STAGES);
     }

@@ -50,13 +50,15 @@ def stage_blocks(bond_dims, D: int, world: int) -> list[tuple[int, int]]:
 
 
 def run_pipeline(stage_fn, n_micro: int, recv_like, send_like, rank: int, world: int, group=None):
-    """Drive one pipeline stage over `n_micro` micro-batches.
+    """Drive one pipeline stage over `n_micro` micro-batches (NCCL / gloo send-recv hand-off).
 
-    stage_fn(t, state_in) -> state_out: runs this stage's sites for micro-batch t;
-    state_in is None on stage 0, state_out is ignored on the last stage.
-    recv_like / send_like: callables returning an empty buffer for the incoming /
-    outgoing state (double-buffered).  Receives for t+1 are posted before stage t
-    computes, sends are asynchronous, so communication overlaps compute.
+    stage_fn(t, state_in, out) runs this stage's sites for micro-batch t and writes its output state
+    into `out`, the send buffer of micro-batch t (state_in is None on stage 0, out is None on the
+    last stage): the producing kernel fills the buffer that is sent, so there is no staging copy.
+    recv_like / send_like: callables returning an empty buffer for the incoming / outgoing state
+    (double-buffered).  Receives for t+1 are posted before stage t computes and sends are
+    asynchronous, so communication overlaps compute; a send buffer is reused only after its send
+    of micro-batch t-2 completed (for NCCL, ``wait`` orders the current stream after the send).
     """
     import torch.distributed as dist
 
@@ -74,12 +76,14 @@ def run_pipeline(stage_fn, n_micro: int, recv_like, send_like, rank: int, world:
             x = rbuf[t % 2]
             if t + 1 < n_micro:
                 rreq = dist.irecv(_as_real(rbuf[(t + 1) % 2]), src=prev, group=group)
-        y = stage_fn(t, x)
+        out = None
         if rank < world - 1:
             if sreq[t % 2] is not None:
                 sreq[t % 2].wait()
-            sbuf[t % 2].copy_(y)
-            sreq[t % 2] = dist.isend(_as_real(sbuf[t % 2]), dst=nxt, group=group)
+            out = sbuf[t % 2]
+        stage_fn(t, x, out)
+        if rank < world - 1:
+            sreq[t % 2] = dist.isend(_as_real(out), dst=nxt, group=group)
     for r in sreq:
         if r is not None:
             r.wait()
@@ -93,6 +97,21 @@ class P2PHandoff:
     directly into the mapped buffer (state_out = the peer pointer): no collective and no staging
     copy on the data path.  GPU-side ordering uses the events; the only host traffic is one tiny
     message per micro-batch and direction on a gloo group (which event record to wait on)."""
+
+    @classmethod
+    def create(cls, rank: int, world: int, recv_bytes: int, host_group=None):
+        """A P2PHandoff if EVERY rank could export and map its peer's buffers and events (CUDA IPC
+        over NVLink needs peer access between the two GPUs), else None on every rank, so the caller
+        falls back to the NCCL send/recv hand-off together."""
+        import torch.distributed as dist
+
+        hp = cls(rank, world, recv_bytes, host_group=host_group)  # runs the same collectives on every rank
+        oks = [None] * world
+        dist.all_gather_object(oks, hp.opened, group=host_group)
+        if all(oks):
+            return hp
+        hp.close()
+        return None
 
     def __init__(self, rank: int, world: int, recv_bytes: int, host_group=None):
         import ctypes
@@ -113,22 +132,28 @@ class P2PHandoff:
             _native.check(self.L.mps_ipc_event_create(ctypes.byref(ev), h))
             return ev.value, bytes(h)
 
-        if rank > 0:
-            mine["recv"], mine["consumed"] = [], []
-            for b in range(2):
-                p, h = ctypes.c_void_p(), H()
-                _native.check(self.L.mps_ipc_alloc(recv_bytes, ctypes.byref(p), h))
-                self.recv[b] = p.value
-                mine["recv"].append(bytes(h))
-                self.consumed[b], hb = new_event()
-                mine["consumed"].append(hb)
-        if rank < world - 1:
-            mine["filled"] = []
-            for b in range(2):
-                self.filled[b], hb = new_event()
-                mine["filled"].append(hb)
+        self.opened = False
+        try:  # export this rank's buffers / events; a failure still joins the all_gather below
+            if rank > 0:
+                mine["recv"], mine["consumed"] = [], []
+                for b in range(2):
+                    p, h = ctypes.c_void_p(), H()
+                    _native.check(self.L.mps_ipc_alloc(recv_bytes, ctypes.byref(p), h))
+                    self.recv[b] = p.value
+                    mine["recv"].append(bytes(h))
+                    self.consumed[b], hb = new_event()
+                    mine["consumed"].append(hb)
+            if rank < world - 1:
+                mine["filled"] = []
+                for b in range(2):
+                    self.filled[b], hb = new_event()
+                    mine["filled"].append(hb)
+        except Exception as e:  # noqa: BLE001 - reported through `opened` / create()
+            mine = {"error": str(e)}
         everyone = [None] * world
         dist.all_gather_object(everyone, mine, group=host_group)
+        if any("error" in e for e in everyone):
+            return
 
         def open_mem(hb):
             p = ctypes.c_void_p()
@@ -140,12 +165,17 @@ class P2PHandoff:
             _native.check(self.L.mps_ipc_event_open(H.from_buffer_copy(hb), ctypes.byref(ev)))
             return ev.value
 
-        if rank < world - 1:
-            nxt = everyone[rank + 1]
-            self.peer_recv = [open_mem(h) for h in nxt["recv"]]
-            self.peer_consumed = [open_event(h) for h in nxt["consumed"]]
-        if rank > 0:
-            self.peer_filled = [open_event(h) for h in everyone[rank - 1]["filled"]]
+        try:
+            if rank < world - 1:
+                nxt = everyone[rank + 1]
+                self.peer_recv = [open_mem(h) for h in nxt["recv"]]
+                self.peer_consumed = [open_event(h) for h in nxt["consumed"]]
+            if rank > 0:
+                self.peer_filled = [open_event(h) for h in everyone[rank - 1]["filled"]]
+            self.opened = True
+        except Exception:
+            # keep the collective schedule intact (create() agrees on the outcome with every rank)
+            self.opened = False
 
     def close(self):
         for p in self.peer_recv:
@@ -347,20 +377,25 @@ def sample_pipelined(config, mps_block, device: int | None = None, group=None, h
     cdt = torch.complex64 if mps_block.dtype == "complex64" else torch.complex128
     counts = torch.zeros((T * n, mps_block.M), dtype=torch.int32, device=dev)
     status = torch.zeros(T * n, dtype=torch.uint8, device=dev)
-    y = torch.empty((n, dims[me]), dtype=cdt, device=dev) if rank < world - 1 else None
     t0 = time.perf_counter()
     with MpsSampler(mps_block, device=dev, sites_range=(mb, me), layout=1) as eng:
         eng.set_streams(config.seed, config.alpha_sigma)
 
-        def stage(t, x):
-            # the last micro-batch may be short: pad to n rows (the padding samples are dropped)
-            eng.run(t * n, n, counts[t * n:(t + 1) * n], m_begin=mb, m_end=me, state_in=x, state_out=y,
+        def stage(t, x, out=None):
+            # the last micro-batch may be short: pad to n rows (the padding samples are dropped);
+            # the stage's last draw kernel writes the hand-off state straight into the send buffer
+            eng.run(t * n, n, counts[t * n:(t + 1) * n], m_begin=mb, m_end=me, state_in=x, state_out=out,
                     status=status[t * n:(t + 1) * n])
-            return y
 
+        hp = None
         if world > 1 and handoff == "p2p":
-            hp = P2PHandoff(rank, world, n * dims[mb] * (8 if cdt == torch.complex64 else 16),
-                            host_group=host_group if host_group is not None else group)
+            hp = P2PHandoff.create(rank, world, n * dims[mb] * (8 if cdt == torch.complex64 else 16),
+                                   host_group=host_group if host_group is not None else group)
+            if hp is None:
+                import warnings
+
+                warnings.warn("peer-memory hand-off unavailable between these GPUs: using NCCL send/recv")
+        if hp is not None:
             stream = torch.cuda.current_stream(dev).cuda_stream
 
             def stage_p2p(t, x, out):
@@ -382,7 +417,7 @@ def sample_pipelined(config, mps_block, device: int | None = None, group=None, h
                          group=group)
         else:
             for t in range(T):
-                stage(t, None)
+                stage(t, None, None)
         torch.cuda.synchronize(dev)
     local = counts[:, mb:me].contiguous()
     if world > 1:

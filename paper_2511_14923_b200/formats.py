@@ -8,8 +8,12 @@
   M sites, each chi_l*chi_r*D complex128 ('<c16', C order) | <Q checksum``.
   Sites are read one at a time (memory-mapped), so a stage can load just its
   block, straight to the device.
-* ``.gmpc`` — photon-count samples: ``b"GMPC" | <I version | <I M | <Q N |
-  <I D | <Q seed | N x M uint8 counts | <Q checksum``.
+* ``.gmpc`` — photon-count samples with the provenance needed to re-evaluate them:
+  v2 ``b"GMPC" | <I version=2 | <I M | <Q N | <I D | <Q seed | <d alpha_sigma (NaN = no
+  displacement stream) | <Q flags (bit 0: alpha_sigma recorded) | N x <Q sample index |
+  N x M uint8 counts | <Q checksum``.  Row i is sample ``index[i]`` of the counter streams
+  (failed samples are dropped by ``batch_sample``, so indices need not be contiguous).
+  v1 files (no alpha_sigma, no indices) still load; their provenance is reported unknown.
 * click text — ``counts > 0`` in the reference's own sample text format
   (sampler.py:772-778), so gbsemu's ``load_samples`` and benchmark statistics
   (benchmark.py:332-371) consume MPS samples unchanged.
@@ -112,33 +116,60 @@ def load_mps(path, block=None, device=None, verify: bool = True) -> MPS:
 # --------------------------------------------------------------------------- counts
 
 
-def save_counts(path, counts: np.ndarray, D: int, seed: int = 0) -> None:
+def save_counts(path, counts: np.ndarray, D: int, seed: int = 0, alpha_sigma: float | None = None,
+                indices=None) -> None:
+    """Write a v2 counts file; ``indices`` (default 0..N-1) are the rows' sample indices."""
     counts = np.asarray(counts)
     if counts.ndim != 2:
         raise ValidationError("counts must be N x M")
     if counts.size and (counts.min() < 0 or counts.max() >= D or D > 256):
         raise ValidationError("counts must lie in [0, D) with D <= 256")
     N, M = counts.shape
-    payload = _COUNTS_MAGIC + struct.pack("<IIQIQ", _VERSION, M, N, D, seed) + counts.astype(np.uint8).tobytes()
+    idx = np.arange(N, dtype="<u8") if indices is None else np.asarray(indices, dtype="<u8")
+    if idx.shape != (N,):
+        raise ValidationError(f"indices must have shape ({N},)")
+    a = float("nan") if alpha_sigma is None else float(alpha_sigma)
+    payload = (_COUNTS_MAGIC + struct.pack("<IIQIQdQ", 2, M, N, D, seed, a, 1) + idx.tobytes()
+               + counts.astype(np.uint8).tobytes())
     Path(path).write_bytes(payload + struct.pack("<Q", _bytesum(payload) & (2**64 - 1)))
 
 
-def load_counts(path) -> tuple[np.ndarray, int, int]:
-    """(counts N x M int32, D, seed) of a .gmpc file, checksum verified."""
+def load_counts_file(path) -> dict:
+    """A counts file, checksum verified: dict(counts N x M int32, D, seed, alpha_sigma (float,
+    None for "no displacement", or the string "unknown" for v1 files), indices (N,) int64 or
+    None for v1 files, version)."""
     data = Path(path).read_bytes()
     if len(data) < 40 or data[:4] != _COUNTS_MAGIC:
         raise ValidationError(f"{path} is not a counts file")
-    version, M, N, D, seed = struct.unpack("<IIQIQ", data[4:32])
-    if version != _VERSION:
+    (version,) = struct.unpack("<I", data[4:8])
+    if version == 1:
+        _, M, N, D, seed = struct.unpack("<IIQIQ", data[4:32])
+        off, alpha, idx = 32, "unknown", None
+    elif version == 2:
+        if len(data) < 56:
+            raise ValidationError(f"{path} has wrong length")
+        _, M, N, D, seed, a, flags = struct.unpack("<IIQIQdQ", data[4:48])
+        alpha = "unknown" if not flags & 1 else (None if np.isnan(a) else float(a))
+        off = 48 + 8 * N
+        idx = None
+    else:
         raise ValidationError(f"unsupported counts file version {version}")
-    end = 32 + N * M
+    end = off + N * M
     if len(data) != end + 8:
         raise ValidationError(f"{path} has wrong length")
     (checksum,) = struct.unpack("<Q", data[end:])
     if (_bytesum(data[:end]) & (2**64 - 1)) != checksum:
         raise ValidationError(f"{path} checksum mismatch")
-    counts = np.frombuffer(data[32:end], dtype=np.uint8).reshape(N, M).astype(np.int32)
-    return counts, int(D), int(seed)
+    if version == 2:
+        idx = np.frombuffer(data[48:off], dtype="<u8").astype(np.int64)
+    counts = np.frombuffer(data[off:end], dtype=np.uint8).reshape(N, M).astype(np.int32)
+    return dict(counts=counts, D=int(D), seed=int(seed), alpha_sigma=alpha, indices=idx, version=int(version))
+
+
+def load_counts(path) -> tuple[np.ndarray, int, int]:
+    """(counts N x M int32, D, seed) of a counts file, checksum verified."""
+    f = load_counts_file(path)
+    return f["counts"], f["D"], f["seed"]
 
 
 def save_clicks_text(path, counts: np.ndarray, seed: int = 0, method: str = "mps") -> None:

@@ -63,7 +63,9 @@ def device_site(seed: int, m: int, chi_l: int, chi_r: int, D: int, device="cuda"
     d = torch.diagonal(R)
     Q.mul_(d / d.abs())
     del R, d
-    out = Q.conj().T.reshape(chi_l, chi_r, D).contiguous()
+    # resolve_conj: for chi_l = 1 the transpose-reshape is a view, so torch would hand back Q's memory
+    # with only the lazy conjugate bit set -- the raw bytes the engine reads would be conj(Gamma)
+    out = Q.conj().T.reshape(chi_l, chi_r, D).resolve_conj().contiguous()
     del Q
     if out.numel() * 16 > 2**31:  # multi-GB sites (config 5): return the QR transients to the device
         torch.cuda.empty_cache()

@@ -91,6 +91,14 @@ class MpsSampleBatch:
         return (self.counts > 0).astype(np.uint8)
 
 
+def _materialised(x):
+    """torch tensors with a lazy conjugate / negative bit (x.conj(), views of them) store the
+    UNconjugated values: the C ABI reads raw memory, so inputs are resolved to physical values."""
+    if x is not None and hasattr(x, "is_conj") and (x.is_conj() or x.is_neg()):
+        return x.resolve_conj().resolve_neg()
+    return x
+
+
 def _ptr(x) -> int | None:
     if x is None:
         return None
@@ -98,6 +106,8 @@ def _ptr(x) -> int | None:
         return x
     if isinstance(x, np.ndarray):
         return x.ctypes.data
+    if x.is_conj() or x.is_neg():  # an output view with a lazy conjugate bit would be written wrongly
+        raise ValidationError("tensors with a lazy conjugate/negative bit must be resolved (resolve_conj())")
     return x.data_ptr()  # torch tensor
 
 
@@ -141,7 +151,7 @@ class MpsSampler:
                     if stream_sites:
                         self._keep.append(G)  # the library streams from this buffer on every call
                 else:
-                    G = G.contiguous()
+                    G = _materialised(G).contiguous()
                     flags = _native.MPS_SITE_DEVICE_BORROW if borrow else _native.MPS_SITE_DEVICE_COPY
                     if borrow:
                         self._keep.append(G)
@@ -160,6 +170,7 @@ class MpsSampler:
             alpha=None, state_in=None, state_out=None, marginals=None, status=None, stream=None):
         """One mps_sample_range call.  Arrays are numpy (host) or torch (device);
         full-width (column = absolute mode)."""
+        uniforms, disp, alpha, state_in = (_materialised(a) for a in (uniforms, disp, alpha, state_in))
         mb = self.sites_range[0] if m_begin is None else m_begin
         me = self.sites_range[1] if m_end is None else m_end
         ld_u = uniforms.shape[1] if uniforms is not None else self.M
@@ -210,6 +221,12 @@ class MpsSampler:
         logp = logp.cpu().numpy()
         logp[(st & _native.MPS_STATUS_FAILED) != 0] = -np.inf
         return dict(marginals=marg.cpu().numpy(), logp=logp, status=st)
+
+    def set_micro_batch(self, micro: int):
+        """Micro-batch size for calls with host arrays (mps_set_micro_batch; 0 = off): a call over more
+        samples runs as micro-batches whose host<->device copies overlap the neighbouring
+        micro-batches' kernels, with one synchronisation per call.  Results do not depend on it."""
+        _native.check(self.L.mps_set_micro_batch(self.ctx, int(micro)), self.ctx)
 
     def set_lanes(self, lanes: int):
         """Concurrent row-block chains per call (mps_set_lanes); results do not depend on it."""

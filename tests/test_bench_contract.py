@@ -27,6 +27,16 @@ def test_reference_arm_json_line():
     assert d["config"]["workload"].startswith("c1")
 
 
+def test_gpus_flag_must_match_world_size():
+    """--gpus N under a launcher with another WORLD_SIZE refuses instead of measuring the wrong N."""
+    import os
+
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--config", "c1", "--steps", "1"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert out.returncode != 0 and "WORLD_SIZE=1" in out.stderr
+
+
 def test_gpu_arm_fails_loudly_without_gpu():
     import torch
 
@@ -54,12 +64,20 @@ def test_gpu_arm_json_line_and_two_rank_path():
     assert d["n_gpus"] == 1 and d["value"] > 0 and d["gpu_launches"] > 0 and d["valid_outputs"]
     assert d["roofline"]["bound"] == "tensor" and d["roofline"]["frac"] > 0
     env = dict(os.environ, MPS_BENCH_BACKEND="gloo", MPS_BENCH_ONE_GPU="1")
-    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-                          "--master-addr", "127.0.0.1", "--master-port", "29547", str(ROOT / "bench.py"), "--gpus", "2",
-                          "--config", "c2", "--steps", "2", "--warmup", "3", "--no-cpu-baseline"],
+    # the bare driver command: `bench.py --gpus 2` re-executes itself under torchrun (2 ranks)
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--config", "c2", "--steps", "2",
+                          "--warmup", "3", "--no-cpu-baseline"],
                          capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
     assert out.returncode == 0, out.stderr[-3000:]
+    assert "re-executing under torchrun" in out.stderr and "process group up: world=2" in out.stderr
     lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1  # rank 0 only
     d2 = json.loads(lines[0])
     assert d2["n_gpus"] == 2 and d2["scaling"] == "weak" and d2["value"] > 0 and d2["valid_outputs"]
+    assert [r["rank"] for r in d2["config"]["ranks"]] == [0, 1]
+    # torchrun with a world size that contradicts --gpus fails loudly
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", "29547", str(ROOT / "bench.py"), "--gpus", "3",
+                          "--config", "c2", "--steps", "2", "--no-cpu-baseline"],
+                         capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert out.returncode != 0

@@ -32,7 +32,9 @@ def _worker(rank, world, port, mode, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         sites = orc.random_mps(M, CHI, D, seed=1)
-        if mode == "sharded":
+        if mode == "p2p_fallback":
+            pass
+        elif mode == "sharded":
             a, b = shard_range(N, rank, world)
             res = orc.sample_chain(sites, orc.stream_uniforms(SEED, a, b - a, M),
                                    alpha=orc.alpha_stream(SEED, a, b - a, M, SIGMA))
@@ -43,20 +45,28 @@ def _worker(rank, world, port, mode, q):
             n = N // NMICRO
             counts = np.zeros((N, me - mb), dtype=np.int32)
 
-            def stage(t, x):
+            def stage(t, x, out):
                 s0 = t * n
                 u = orc.stream_uniforms(SEED, s0, n, M)[:, mb:me]
                 al = orc.alpha_stream(SEED, s0, n, M, SIGMA)[:, mb:me]
                 res = orc.sample_chain(sites[mb:me], u, alpha=al, state_in=None if x is None else x.numpy(),
                                        return_state=True)
                 counts[s0:s0 + n] = res["counts"]
-                return torch.from_numpy(res["state"])
+                if out is not None:  # the stage writes its hand-off state into the send buffer
+                    out.copy_(torch.from_numpy(res["state"]))
 
             run_pipeline(stage, NMICRO,
                          recv_like=lambda: torch.empty(n, dims[mb], dtype=torch.complex128),
                          send_like=lambda: torch.empty(n, dims[me], dtype=torch.complex128),
                          rank=rank, world=world)
             out = gather_columns(torch.from_numpy(counts), mb, M, rank, world)
+        if mode == "p2p_fallback":
+            # no GPU here: exporting CUDA-IPC buffers fails on every rank, and every rank agrees to fall
+            # back (None) instead of hanging in mismatched collectives
+            from paper_2511_14923_b200.distributed import P2PHandoff
+
+            hp = P2PHandoff.create(rank, world, 1024)
+            out = torch.tensor([hp is None])
         if rank == 0:
             q.put(out.numpy())
     finally:
@@ -109,3 +119,12 @@ def test_sample_sharded_gloo_equals_single_process():
 @pytest.mark.timeout(300)
 def test_mode_pipelined_gloo_equals_single_process():
     assert np.array_equal(_run("pipelined"), _single()["counts"])
+
+
+@pytest.mark.timeout(300)
+def test_p2p_handoff_falls_back_together():
+    """P2PHandoff.create returns None on EVERY rank when any rank cannot export or map the peer
+    buffers (here: no GPU at all), so sample_pipelined / bench fall back to NCCL send/recv."""
+    if torch.cuda.is_available():
+        pytest.skip("exercises the failure path; on a GPU box the peer buffers export fine")
+    assert bool(_run("p2p_fallback")[0])

@@ -61,6 +61,51 @@ def test_counts_roundtrip_and_checks(tmp_path):
         save_counts(p, np.full((2, 2), 10), D=10)
 
 
+def test_counts_v2_provenance(tmp_path):
+    """v2 counts files carry alpha_sigma and each row's sample index (failed samples dropped)."""
+    from paper_2511_14923_b200.formats import load_counts_file
+
+    c = np.random.default_rng(1).integers(0, 4, size=(5, 3))
+    p = tmp_path / "c.gmpc"
+    save_counts(p, c, D=4, seed=9, alpha_sigma=0.5, indices=[0, 1, 3, 4, 7])
+    f = load_counts_file(p)
+    assert f["version"] == 2 and f["alpha_sigma"] == 0.5 and list(f["indices"]) == [0, 1, 3, 4, 7]
+    assert np.array_equal(f["counts"], c) and f["seed"] == 9
+    save_counts(p, c, D=4, seed=9)
+    f = load_counts_file(p)
+    assert f["alpha_sigma"] is None and list(f["indices"]) == [0, 1, 2, 3, 4]
+    with pytest.raises(ValidationError):
+        save_counts(p, c, D=4, indices=[0, 1])
+
+
+def _write_v1_counts(path, counts, D, seed):
+    import struct
+
+    payload = b"GMPC" + struct.pack("<IIQIQ", 1, counts.shape[1], counts.shape[0], D, seed) + \
+        counts.astype(np.uint8).tobytes()
+    path.write_bytes(payload + struct.pack("<Q", int(np.frombuffer(payload, np.uint8).sum(dtype=np.uint64))))
+
+
+def test_evaluate_refuses_unknown_provenance(tmp_path, capsys):
+    """A v1 counts file records neither alpha_sigma nor the row indices: `evaluate` refuses to guess
+    (exit code 2) instead of scoring the rows under the wrong displacement streams."""
+    from paper_2511_14923_b200.cli import main
+    from paper_2511_14923_b200.formats import load_counts_file
+
+    m = tmp_path / "m.gmps"
+    save_mps(MPS.random(3, 4, 2, seed=0), m)
+    p = tmp_path / "old.gmpc"
+    _write_v1_counts(p, np.zeros((4, 3), dtype=np.int32), D=2, seed=1)
+    assert load_counts_file(p)["alpha_sigma"] == "unknown" and load_counts(p)[2] == 1
+    assert main(["evaluate", "--mps", str(m), "--counts", str(p), "--out", str(tmp_path / "l.npy")]) == 2
+    assert main(["evaluate", "--mps", str(m), "--counts", str(p), "--alpha-sigma", "0.5",
+                 "--out", str(tmp_path / "l.npy")]) == 2  # --start still missing
+    save_counts(p, np.zeros((4, 3), dtype=np.int32), D=2, seed=1, alpha_sigma=0.5)
+    assert main(["evaluate", "--mps", str(m), "--counts", str(p), "--alpha-sigma", "0.7",
+                 "--out", str(tmp_path / "l.npy")]) == 2  # contradicts the file
+    assert "contradicts" in capsys.readouterr().err
+
+
 def test_clicks_text_matches_reference_format(tmp_path, golden):
     """counts > 0 written byte-for-byte like gbsemu's save_samples_text (sampler.py:772-778)."""
     bits = golden["text_bits"]

@@ -1,0 +1,114 @@
+"""Parity at the configuration the bench reports (needs a B200), and the CUDA draw pinned to the
+reference's own sampler output.
+
+* C3 = BASELINE.json configs[2]: M=64, chi=1000, D=10, alpha ~ CN(0, 0.5), the bench's own
+  device-generated sites (MPS.random(..., device="cuda"), torch QR), one micro-batch of n=256
+  through all 64 sites.  The oracle runs teacher-forced along the GPU's realised path
+  (sampler.py:394-416 pattern) and free-running on the same uniforms and alpha.
+  Bar (BASELINE.json north_star): normalised marginals within 1e-10 RELATIVE per element
+  (|dp| <= 1e-10 p for p > 1e-12), counts identical except where either engine flagged a draw
+  within 1e-10 of a CDF boundary.  The reference's analog is full-order exactness
+  (pkg/tests/test_sampler.py:84-97).
+* The draw kernel against gbsemu's exact_reference_sampler (sampler.py:686-703): a chi=1, M=1,
+  D=16 site with |Gamma_d|^2 = exact_p reproduces the golden codes for the golden uniforms.
+"""
+
+from collections.abc import Sequence
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from oracle import mps_oracle as orc  # noqa: E402
+from paper_2511_14923_b200 import MPS, MpsSampler, MpsSamplerConfig, alpha_stream, stream_uniforms  # noqa: E402
+from paper_2511_14923_b200 import _native  # noqa: E402
+
+from _parity import P_FLOOR, REL_TOL_C128 as REL_TOL, marginal_errors  # noqa: E402
+
+ABS_TOL = 1e-10
+
+
+class DeviceSites(Sequence):
+    """The oracle's view of device-resident sites: one site copied to the host per access."""
+
+    def __init__(self, mps):
+        self.sites = mps.sites
+
+    def __len__(self):
+        return len(self.sites)
+
+    def __getitem__(self, m):
+        return self.sites[m].cpu().numpy()
+
+
+M3, CHI3, D3, N3, SIG3 = 64, 1000, 10, 256, 0.5 ** 0.5
+
+
+@pytest.fixture(scope="module")
+def c3():
+    mps = MPS.random(M3, CHI3, D3, seed=0, device="cuda")
+    u = stream_uniforms(0, 0, N3, M3)
+    al = alpha_stream(0, 0, N3, M3, SIG3)
+    host = DeviceSites(mps)
+    free = orc.sample_chain(host, u, alpha=al)
+    return mps, host, u, al, free
+
+
+def test_c3_device_sites_row_orthonormal(c3):
+    """The bench's device-generated sites satisfy the oracle's decision 2 (sum_d G_d G_d^+ = I)."""
+    mps = c3[0]
+    worst = 0.0
+    for m in (0, 1, 2, 31, 62, 63):
+        G = mps.sites[m]
+        A = G.reshape(G.shape[0], -1)
+        err = (A @ A.conj().T - torch.eye(A.shape[0], dtype=A.dtype, device=A.device)).abs().max().item()
+        worst = max(worst, err)
+    assert worst < 1e-12, worst
+
+
+@pytest.mark.parametrize("gemm_mode,digits", [(3, 7), (8, 7)])
+def test_c3_headline_chain_vs_oracle(c3, gemm_mode, digits):
+    """All 64 sites of C3 at n=256: 3M DMMA (the headline K1) and the INT8 Ozaki emulation."""
+    mps, host, u, al, free = c3
+    cfg = MpsSamplerConfig(N=N3, seed=0, alpha_sigma=SIG3, batch_size=N3)
+    with MpsSampler(mps) as eng:
+        eng.set_gemm_mode(gemm_mode)
+        eng.set_ozaki_digits(digits)
+        res = eng.sample(cfg, return_marginals=True)
+    assert not (res["status"] & _native.MPS_STATUS_FAILED).any()
+    forced = orc.sample_chain(host, u, alpha=al, forced=res["counts"], return_marginals=True)
+    ab, rel, nbig = marginal_errors(res["marginals"], forced["marginals"])
+    print(f"C3 gemm mode {gemm_mode}: max|dp| {ab:.3e}, max rel {rel:.3e} over {nbig} marginals > {P_FLOOR}")
+    assert ab <= ABS_TOL and rel <= REL_TOL, (ab, rel)
+    flagged = (res["status"] & _native.MPS_STATUS_FLAGGED) != 0
+    mism = (res["counts"] != free["counts"]).any(axis=1)
+    assert not (mism & ~flagged & ~free["flagged"]).any(), int((mism & ~flagged & ~free["flagged"]).sum())
+    # the GPU's log joint probability of its own paths equals the oracle's
+    lp = np.log(np.take_along_axis(res["marginals"], res["counts"][:, :, None].astype(np.int64), 2)[:, :, 0]).sum(1)
+    assert np.allclose(lp, forced["logp"], rtol=1e-10, atol=1e-9)
+
+
+@pytest.mark.parametrize("small_chain", [0, 1])
+def test_draw_matches_reference_exact_sampler(golden, small_chain):
+    """chi=1, M=1, D=16 site with |Gamma_d|^2 = gbsemu's exact distribution: the CUDA draw gives
+    exact_reference_sampler's codes (sampler.py:686-703) for its uniforms, except near-ties."""
+    p, u, codes = golden["exact_p"], golden["exact_u"], golden["exact_codes"]
+    D, N = len(p), len(u)
+    G = np.sqrt(p).astype(np.complex128).reshape(1, 1, D)
+    cfg = MpsSamplerConfig(N=N, seed=3, batch_size=1024)
+    with MpsSampler(MPS([G])) as eng:
+        eng.set_small_chain(small_chain)
+        res = eng.sample(cfg, uniforms=u.reshape(N, 1))
+    cdf = np.cumsum(p)
+    dist = np.abs(cdf[:-1][None, :] - u[:, None]).min(axis=1)
+    near = dist <= 1e-10
+    flagged = (res["status"] & _native.MPS_STATUS_FLAGGED) != 0
+    # the tie flag agrees with the reference cdf away from the band's own edge (rounding of sqrt(p)^2)
+    assert not (flagged & (dist > 1.01e-10)).any() and flagged[dist < 0.99e-10].all()
+    assert np.array_equal(res["counts"][~flagged, 0], codes[~flagged])
+    assert (~flagged).sum() > 0.99 * N
