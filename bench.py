@@ -54,6 +54,9 @@ METRIC = "MPS samples/sec (chi,D,M stated) at 1/2/4/8 B200; % of FP64 tensor-cor
 # on each other inside kernels in the sample-sharded layout; its timings mean nothing).
 BACKEND = os.environ.get("MPS_BENCH_BACKEND", "nccl")
 ONE_GPU = os.environ.get("MPS_BENCH_ONE_GPU") == "1"
+# MPS_BENCH_PROFILE_RANGE=1: bracket the timed steps with cudaProfilerStart/Stop, so
+# `ncu --profile-from-start off --metrics gpu__time_duration.sum` lists exactly their launches
+PROFILE_RANGE = os.environ.get("MPS_BENCH_PROFILE_RANGE") == "1"
 
 
 def dist_barrier(local):
@@ -81,7 +84,7 @@ def dist_max(x, dev):
 def fp64_peak():
     p = ROOT / "profiles" / "fp64_peak.json"
     try:
-        return float(json.loads(p.read_text())["fp64_dmma_tflops"]), "measured (profiles/fp64_peak.json, DMMA loop)"
+        return float(json.loads(p.read_text())["fp64_dmma_tflops"]), ("builder-measured (profiles/fp64_peak.json, register-resident DMMA loop, tools/fp64_peak.cu; MEASURED_PEAKS.json has no FP64 entry; nominal 37.2)")
     except Exception:
         return 37.2, "nominal (148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz)"
 
@@ -96,19 +99,23 @@ def measured_bf16():
 
 
 def ncu_traffic(cfg_name, n):
-    """DRAM bytes per K1 launch from the committed ncu --set full capture of a full-chi mode
-    (profiles/), with the algorithmic bytes of that same launch, or (None, None)."""
+    """DRAM bytes per K1 launch from the committed ncu --set full capture of the CURRENT default K1
+    (site_gemm3m_kernel with sum planes) at a full-chi mode (profiles/), with the algorithmic bytes
+    of that same launch, or (None, None)."""
     if cfg_name != "c3" or n != 1024:
         return None, None
-    p = ROOT / "profiles" / "r01_ncu_k1_site_gemm3m_c3_mode30_n1024.json"
+    p = ROOT / "profiles" / "r02_ncu_k1_site_gemm3m_c3_mode30_n1024.json"
     try:
         rep = json.loads(p.read_text())[0]
     except Exception:
         return None, None
     chi, D = 1000, 10
-    algo = 16.0 * chi * chi * D + 16.0 * n * chi + 16.0 * n * chi * D
-    return rep["dram_bytes_total"], {"source": str(p.relative_to(ROOT)), "launch": "mode 30 (chi_l = chi_r = 1000)",
-                                     "algorithmic_bytes": algo}
+    # Gamma (16 chi^2 D) + its 3M sum plane Gr+Gi (8 chi^2 D) + V (16 n chi) + its sum plane (8 n chi)
+    # + C written (16 n chi D)
+    algo = 24.0 * chi * chi * D + 24.0 * n * chi + 16.0 * n * chi * D
+    return rep["dram_bytes_total"], {"source": str(p.relative_to(ROOT)), "launch": "mode 30 (chi_l = chi_r = 1000), "
+                                     "one lane, the default 3M kernel with sum planes", "kernel": rep["Kernel Name"],
+                                     "algorithmic_bytes": algo, "traffic_over_algorithmic": rep["dram_bytes_total"] / algo}
 
 
 def site_flops(dims, D, n):
@@ -831,11 +838,15 @@ def main():
     l0 = eng.kernel_launches
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
+    if PROFILE_RANGE:  # ncu --profile-from-start off sees exactly the timed steps
+        torch.cuda.profiler.start()
     e0.record(stream)
     for s in range(W, W + K):
         step(s)
     e1.record(stream)
     barrier()
+    if PROFILE_RANGE:
+        torch.cuda.profiler.stop()
     launches = eng.kernel_launches - l0
     ck = clocks.stop()
     # Instrumented repeat of the same K steps: CUDA events around every K1 launch on its

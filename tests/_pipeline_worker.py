@@ -10,14 +10,17 @@ import torch.distributed as dist
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from oracle import mps_oracle as orc  # noqa: E402
 from paper_2511_14923_b200 import MPS, MpsSamplerConfig  # noqa: E402
-from paper_2511_14923_b200.distributed import sample_pipelined  # noqa: E402
+from paper_2511_14923_b200.distributed import sample_pipelined, sample_sharded  # noqa: E402
 
 handoff, out = sys.argv[1], sys.argv[2]
 dist.init_process_group("gloo")
 torch.cuda.set_device(0)
 sites = orc.random_mps(16, 100, 10, seed=0)
-res = sample_pipelined(MpsSamplerConfig(N=350, seed=4, alpha_sigma=0.5, batch_size=100), MPS(sites), device=0,
-                       handoff=handoff)
+cfg = MpsSamplerConfig(N=350, seed=4, alpha_sigma=0.5, batch_size=100)
+if handoff == "sharded":  # sample-sharded layout: contiguous index blocks per rank, counts gathered
+    res = sample_sharded(cfg, MPS(sites), device=0)
+else:
+    res = sample_pipelined(cfg, MPS(sites), device=0, handoff=handoff)
 if dist.get_rank() == 0:
     np.save(out, res.counts)
 dist.destroy_process_group()

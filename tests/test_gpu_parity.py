@@ -793,6 +793,25 @@ def test_distributed_entry_points_single_rank(c2_sites):
     assert np.array_equal(a.counts, ref.counts) and np.array_equal(b.counts, ref.counts)
 
 
+def test_sample_sharded_two_ranks_equals_one(tmp_path, c2_sites):
+    """GPU-count invariance (the analog of the reference's worker-count invariance,
+    pkg/tests/test_sampler.py:272-277): two ranks (both on cuda:0, host plumbing over gloo) each
+    sample their contiguous index block, and rank 0's gathered counts equal single-process sampling."""
+    import os
+    import subprocess
+    import sys
+
+    ref = batch_sample(MpsSamplerConfig(N=350, seed=4, alpha_sigma=0.5, batch_size=100), MPS(c2_sites))
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = tmp_path / "counts.npy"
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29563",
+                        os.path.join(root, "tests", "_pipeline_worker.py"), "sharded", str(out)],
+                       capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    assert np.array_equal(np.load(out), ref.counts)
+
+
 def test_pipelined_p2p_handoff_on_one_gpu(tmp_path, c2_sites):
     """The mode pipeline across two processes (both on cuda:0, host plumbing over gloo) with the
     fused peer-memory hand-off (P2PHandoff: the producer's last draw kernel writes the state into

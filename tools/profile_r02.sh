@@ -5,7 +5,7 @@
 set -x
 P="ncu --clock-control none"
 timeout 600 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/r02_bench_plain.jsonl 2> gpurun_out/r02_bench_plain.err && \
-timeout 900 $P --metrics gpu__time_duration.sum -c 400 --csv --log-file gpurun_out/r02_launches_bench_c3.csv \
+MPS_BENCH_PROFILE_RANGE=1 timeout 900 $P --profile-from-start off --metrics gpu__time_duration.sum --csv --log-file gpurun_out/r02_launches_bench_c3.csv \
   python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 timeout 300 python tools/profile_step.py --lanes 1 > gpurun_out/r02_ps_plain.log 2>&1 && \
 timeout 600 $P --profile-from-start off --set full --import-source on -k regex:site_gemm3m -s 30 -c 1 \
