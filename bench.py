@@ -908,11 +908,14 @@ def main():
 
     ok = bool((counts[W:] >= 0).all().item()) and not bool((status[W:] & 1).any().item()) and e2e_ok
     # parity of this run's own outputs: the first samples of timed step W against the oracle
+    # (rank 0 only: every rank runs the same kernels; the host oracle would contend for the CPU)
     n_chk = min(32, n)
-    parity = parity_spot_check(eng, mps, 0, M, block_index(W), n_chk, stream.cuda_stream, sigma,
-                               uniforms=u_dev[W][:n_chk], alpha=a_dev[W][:n_chk],
-                               ref_counts=counts[W][:n_chk].cpu().numpy(), gemm_mode=args.gemm)
-    ok = ok and parity["ok"]
+    parity = None
+    if rank == 0:
+        parity = parity_spot_check(eng, mps, 0, M, block_index(W), n_chk, stream.cuda_stream, sigma,
+                                   uniforms=u_dev[W][:n_chk], alpha=a_dev[W][:n_chk],
+                                   ref_counts=counts[W][:n_chk].cpu().numpy(), gemm_mode=args.gemm)
+        ok = ok and parity["ok"]
 
     # Same run, same inputs, K1 emulated on the INT8 tensor cores (gemm mode 8, Ozaki, ~1e-13):
     # reported next to the FP64-DMMA headline (the path the north star names) as "alt_gemm".

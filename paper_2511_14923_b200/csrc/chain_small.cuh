@@ -40,7 +40,14 @@ constexpr int SC_FW = SC_FMAX / 8;                // per compute warp (1)
 #endif
 constexpr int SC_KS = SC_KS_DEF;                  // k stages (8 complex k each) per ring slot
 constexpr int SC_STAGES = 12 / SC_KS;             // ring slots (96 KB of Gamma in flight)
-constexpr int SC_COMPUTE = 256;                   // 8 compute warps: 2 per SM sub-partition keep DMMA issuing
+#ifndef SC_KW
+#define SC_KW 8
+#endif
+// compute warps: 8 (each one 8-column fragment x both 8-row fragments) or 16 (one 8 x 8 fragment
+// each: twice the warps to hide the LDS -> DMMA latency of the 16-row K1 slice; every output element
+// still accumulates over k in the same order, so the bits do not change)
+constexpr int SC_COMPUTE = SC_KW * 32;
+constexpr int SC_MFW = SC_KW == 16 ? 1 : SC_MF;   // row fragments per compute warp
 constexpr int SC_THREADS = SC_COMPUTE + 64;       // + ring producer warp + D(alpha) warp
 constexpr int SC_STAGE_BYTES = SC_KS * SC_FMAX * 1024;  // SC_KS x fc blocks of (8 k rows x 8 complex), swizzled
 constexpr int SC_VP = SC_KMAX * 16 + 16;          // V row pitch: == 16 mod 128 -> conflict-free LDS.128
@@ -249,10 +256,11 @@ __global__ void __launch_bounds__(SC_THREADS, 1) small_chain_kernel(const __grid
 
       if (tid == 0) SC_STAMP(0, q, 7);
       // ---- K1: 3M DMMA over this CTA's fragments (site_gemm3m_kernel's inner loop, DADD sums) ----
-      const int fbase = warp * SC_FW;
-      double t1[SC_MF][SC_FW][2], t2[SC_MF][SC_FW][2], t3[SC_MF][SC_FW][2];
+      const int fbase = (warp % 8) * SC_FW;
+      const int mf0 = SC_MFW == SC_MF ? 0 : warp / 8;  // this warp's first row fragment
+      double t1[SC_MFW][SC_FW][2], t2[SC_MFW][SC_FW][2], t3[SC_MFW][SC_FW][2];
 #pragma unroll
-      for (int mf = 0; mf < SC_MF; ++mf)
+      for (int mf = 0; mf < SC_MFW; ++mf)
 #pragma unroll
         for (int j = 0; j < SC_FW; ++j)
 #pragma unroll
@@ -266,13 +274,13 @@ __global__ void __launch_bounds__(SC_THREADS, 1) small_chain_kernel(const __grid
         for (int step = 0; step < 2; ++step) {
           const int i = 2 * t + step;
           const double2 w = *reinterpret_cast<const double2*>(st + fbase * 1024 + i * 128 + ((g ^ i) << 4));
-          double2 v[SC_MF];
+          double2 v[SC_MFW];
 #pragma unroll
-          for (int mf = 0; mf < SC_MF; ++mf)
-            v[mf] = *reinterpret_cast<const double2*>(Vt + (8 * mf + g) * SC_VP + (8 * kt + i) * 16);
+          for (int mf = 0; mf < SC_MFW; ++mf)
+            v[mf] = *reinterpret_cast<const double2*>(Vt + (8 * (mf0 + mf) + g) * SC_VP + (8 * kt + i) * 16);
           const double ws = __dadd_rn(w.x, w.y);
 #pragma unroll
-          for (int mf = 0; mf < SC_MF; ++mf) {
+          for (int mf = 0; mf < SC_MFW; ++mf) {
             dmma_8x8x4(t1[mf][0][0], t1[mf][0][1], v[mf].x, w.x);
             dmma_8x8x4(t2[mf][0][0], t2[mf][0][1], v[mf].y, w.y);
             dmma_8x8x4(t3[mf][0][0], t3[mf][0][1], __dadd_rn(v[mf].x, v[mf].y), ws);
@@ -310,8 +318,8 @@ __global__ void __launch_bounds__(SC_THREADS, 1) small_chain_kernel(const __grid
       SC_STAMP(0, q, 1);
       // epilogue: row 8 mf + g of the group is owned by CTA 8 mf + g — st.async the entries there
 #pragma unroll
-      for (int mf = 0; mf < SC_MF; ++mf) {
-        const uint32_t owner = (uint32_t)(8 * mf + g);
+      for (int mf = 0; mf < SC_MFW; ++mf) {
+        const uint32_t owner = (uint32_t)(8 * (mf0 + mf) + g);
         const uint32_t dst = sc_mapa(c_addr + (uint32_t)((q & 1) * SC_NMAX * 16), owner);
         const uint32_t bar = sc_mapa(cbar_addr + (uint32_t)((q & 1) * 8), owner);
 #pragma unroll
