@@ -164,11 +164,11 @@ def parity_spot_check(eng, mps, m_begin, m_end, first, n_chk, stream, sigma, uni
     ortho = 0.0
     for m in sorted({m_begin, m_begin + 1, (m_begin + m_end) // 2, m_end - 1} & set(range(m_begin, m_end))):
         G = mps.sites[m] if isinstance(mps.sites[m], torch.Tensor) else torch.from_numpy(np.asarray(mps.sites[m])).to(dev)
-        A = G.reshape(G.shape[0], -1)
+        A = G.reshape(G.shape[0], -1)[:256]  # a row subset keeps the check small at chi = 10^4 (16 GB sites)
         eye = torch.eye(A.shape[0], dtype=A.dtype, device=A.device)
         ortho = max(ortho, float((A @ A.conj().T - eye).abs().max().item()))
     same = None if ref_counts is None else bool(np.array_equal(ref_counts[:, cols], cnt_h[:, cols]))
-    site_tol = 1e-12 if tol <= 1e-9 else 1e-5  # complex64 sites are orthonormal to fp32 rounding
+    site_tol = 1e-12 if tol <= 1e-9 else 1e-4  # complex64 sites are orthonormal to fp32 rounding (~sqrt(N) eps)
     ok = bool(d.max() <= tol and rel <= tol and not mism.any() and not (st_h & 1).any() and ortho < site_tol
               and same is not False)
     return {"ok": ok, "n_checked": int(n_chk), "modes": [int(m_begin), int(m_end)], "max_abs_dp": float(d.max()),

@@ -198,6 +198,12 @@ int mps_set_gemm_mode(mps_ctx* ctx, int mode);
 /* Digits per operand of gemm mode 8 (Ozaki): 7 (default, ~1e-13 of the row scales), 6 (25% fewer
  * INT8 products, ~1e-11) or 5. */
 int mps_set_ozaki_digits(mps_ctx* ctx, int S);
+/* Where gemm mode 8 keeps the sites' digit planes (1.75x the site bytes at 7 digits): 0 resident
+ * (built once per site), 1 streamed (sliced per call, column block by column block, into a 2-slot
+ * ring on a copy stream that runs ahead of the GEMMs: for stages whose planes do not fit, e.g. C5),
+ * 2 auto (default: streamed when the planes would not fit in free memory).  block_cols: complex
+ * columns per streamed block (0: ~4 GB of planes per block).  Results are identical in all modes. */
+int mps_set_ozaki_site_mode(mps_ctx* ctx, int mode, int block_cols);
 /* complex128 K1 emulated on the INT8 tensor cores (Ozaki scheme with S = 5..7 digits):
  * C (n x N) = V (n x K) . G (K x N), all complex128.  Test/benchmark entry (slices per call). */
 int mps_site_gemm_ozaki(const void* V, const void* G, void* C, int n, int K, int N, int S, uint64_t stream);

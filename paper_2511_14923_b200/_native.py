@@ -18,7 +18,7 @@ LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
 EXPORTS = (
     "mps_create", "mps_configure", "mps_set_site", "mps_set_streams", "mps_sample", "mps_sample_range",
     "mps_kernel_launches", "mps_profile", "mps_profile_read", "mps_last_error", "mps_destroy",
-    "mps_site_gemm", "mps_site_gemm_cfg", "mps_set_gemm_config", "mps_set_gemm_mode", "mps_set_lanes", "mps_set_micro_batch", "mps_set_small_chain", "mps_set_ozaki_digits", "mps_small_chain_eligible",
+    "mps_site_gemm", "mps_site_gemm_cfg", "mps_set_gemm_config", "mps_set_gemm_mode", "mps_set_lanes", "mps_set_micro_batch", "mps_set_small_chain", "mps_set_ozaki_digits", "mps_set_ozaki_site_mode", "mps_small_chain_eligible",
     "mps_set_sum_planes", "mps_displacement", "mps_stream_uniforms", "mps_site_gemm_c64",
     "mps_c64_state_planes", "mps_c64_site_planes", "mps_c64_gemm_planes", "mps_site_gemm_ozaki",
     "mps_ozaki_state_planes", "mps_ozaki_site_planes", "mps_ozaki_gemm_planes",
@@ -60,6 +60,7 @@ def _declare(L):
     L.mps_set_micro_batch.argtypes = [c_void_p, c_int]
     L.mps_set_small_chain.argtypes = [c_void_p, c_int]
     L.mps_set_ozaki_digits.argtypes = [c_void_p, c_int]
+    L.mps_set_ozaki_site_mode.argtypes = [c_void_p, c_int, c_int]
     L.mps_small_chain_eligible.argtypes = [c_void_p, c_int, c_int, c_int]
     L.mps_set_sum_planes.argtypes = [c_void_p, c_int]
     L.mps_set_forced.argtypes = [c_void_p, c_int]

@@ -210,6 +210,12 @@ struct mps_ctx {
   bool sum_planes = true;                           // feed the 3M GEMM precomputed sums
   int dtype = -1;                                   // MPS_C128 / MPS_C64, fixed by the first site
   int oz_S = 7;                                     // Ozaki digits per operand (gemm mode 8)
+  // gemm mode 8 site digits: 0 resident (built once per site), 1 streamed (sliced per call into a
+  // 2-slot ring of column blocks on the copy stream, for sites whose planes do not fit), 2 auto
+  int oz_site_mode = 2;
+  int oz_block_cols = 0;                            // streamed column block (complex cols; 0 = by budget)
+  DevBuf<int8_t> ozs_planes[2];
+  DevBuf<int> ozs_e[2];
   bool draw_ring = true;                            // stage C rows through a TMA ring in the draw kernel
   bool forced = false;                              // teacher forcing: outcomes read from counts
   // small chains (chi <= 128, chi D <= 1024, 3M): the whole mode loop in one persistent cluster
@@ -575,7 +581,9 @@ static cudaError_t launch_ozaki_cl(const int8_t* a_planes, int n_pad, const int*
 // diagonal-split kernel: clusters of MP CTA pairs, 128 x 128 tiles (ozaki_gemm.cuh)
 template <int S, int MP>
 static cudaError_t launch_ozaki2(const int8_t* a_planes, int n_pad, const int* ea, const int8_t* b_planes, int b_pad,
-                                 const int* eb, int ld, double2* C, int n, int K, int N, cudaStream_t st) {
+                                 const int* eb, int ld, double2* C, int n, int K, int N, cudaStream_t st,
+                                 long long ldc_c = 0) {
+  if (ldc_c == 0) ldc_c = N;  // complex elements per C row (a column block writes into a wider C)
   using Cfg = Oz2Cfg<S, MP>;
   if (cudaError_t e = set_smem_once((const void*)ozaki2_gemm_kernel<Cfg>, Cfg::SMEM_BYTES)) return e;
   const int mtiles = round_up((n + Cfg::BM - 1) / Cfg::BM, MP);
@@ -599,7 +607,7 @@ static cudaError_t launch_ozaki2(const int8_t* a_planes, int n_pad, const int* e
   for (int kb0 = 0; kb0 < KS; kb0 += OZ_SEG_KB) {
     const int KB = std::min(OZ_SEG_KB, KS - kb0);
     cudaError_t e = cudaLaunchKernelEx(&cfg, ozaki2_gemm_kernel<Cfg>, a_planes, b_planes, ea, eb, (double*)C, n, 2 * N,
-                                       KB, 2LL * N, KS, kb0, kb0 > 0 ? 1 : 0);
+                                       KB, 2LL * ldc_c, KS, kb0, kb0 > 0 ? 1 : 0);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
@@ -618,17 +626,21 @@ static bool ozaki_v1() {
 // single-CTA 128 x 64 kernel that keeps all S diagonals (2/3 of the MMA rate, kept for comparison)
 template <int S>
 static cudaError_t launch_ozaki_s(const int8_t* a_planes, int n_pad, const int* ea, const int8_t* b_planes, int b_pad,
-                                  const int* eb, int ld, double2* C, int n, int K, int N, cudaStream_t st) {
-  if (ozaki_v1() && K <= OZ_MAX_K) return launch_ozaki_cl<S, 1, 1>(a_planes, n_pad, ea, b_planes, b_pad, eb, ld, C, n, K, N, st);
-  return launch_ozaki2<S, 1>(a_planes, n_pad, ea, b_planes, b_pad, eb, ld, C, n, K, N, st);
+                                  const int* eb, int ld, double2* C, int n, int K, int N, cudaStream_t st,
+                                  long long ldc_c) {
+  if (ozaki_v1() && K <= OZ_MAX_K && (ldc_c == 0 || ldc_c == N))
+    return launch_ozaki_cl<S, 1, 1>(a_planes, n_pad, ea, b_planes, b_pad, eb, ld, C, n, K, N, st);
+  return launch_ozaki2<S, 1>(a_planes, n_pad, ea, b_planes, b_pad, eb, ld, C, n, K, N, st, ldc_c);
 }
 
+// ldc_c: complex elements per C row (0: N); a site column block passes C + c0 and the full width
 static cudaError_t launch_ozaki(int S, const int8_t* a_planes, int n_pad, const int* ea, const int8_t* b_planes,
-                                int b_pad, const int* eb, int ld, double2* C, int n, int K, int N, cudaStream_t st) {
+                                int b_pad, const int* eb, int ld, double2* C, int n, int K, int N, cudaStream_t st,
+                                long long ldc_c = 0) {
   switch (S) {
-    case 5: return launch_ozaki_s<5>(a_planes, n_pad, ea, b_planes, b_pad, eb, ld, C, n, K, N, st);
-    case 6: return launch_ozaki_s<6>(a_planes, n_pad, ea, b_planes, b_pad, eb, ld, C, n, K, N, st);
-    default: return launch_ozaki_s<7>(a_planes, n_pad, ea, b_planes, b_pad, eb, ld, C, n, K, N, st);
+    case 5: return launch_ozaki_s<5>(a_planes, n_pad, ea, b_planes, b_pad, eb, ld, C, n, K, N, st, ldc_c);
+    case 6: return launch_ozaki_s<6>(a_planes, n_pad, ea, b_planes, b_pad, eb, ld, C, n, K, N, st, ldc_c);
+    default: return launch_ozaki_s<7>(a_planes, n_pad, ea, b_planes, b_pad, eb, ld, C, n, K, N, st, ldc_c);
   }
 }
 
@@ -1118,12 +1130,44 @@ static int run_chain(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
   }
   const bool use_sums = !c64 && c->sum_planes && c->gemm_mode == 3;
   const bool ozaki = !c64 && c->gemm_mode == 8;
+  bool oz_stream = false;  // site digits sliced per call, column block by column block
+  int oz_cols = 0;         // complex columns per streamed block
   if (ozaki) {
     for (int m = m_begin; m < m_end; ++m) {
       if (c->sites[m].host) return fail(c, MPS_ERR_VALIDATION, "host-streamed sites do not support gemm mode 8");
     }
-    for (int m = m_begin; m < m_end; ++m) CU(c, ozaki_prepare_site(c->sites[m], D, c->oz_S), "Ozaki site digits");
+    size_t need = 0, widest = 0;  // plane bytes still to build; widest per-column plane bytes
+    for (int m = m_begin; m < m_end; ++m) {
+      const Site& sm = c->sites[m];
+      const size_t per_col = (size_t)c->oz_S * 2 * oz_ld(sm.chi_l);
+      widest = std::max(widest, per_col);
+      if (!(sm.oz && sm.oz_S == c->oz_S)) need += per_col * (size_t)round_up(2 * sm.chi_r * D, 256) / 2;
+    }
+    oz_stream = c->oz_site_mode == 1;
+    if (c->oz_site_mode == 2 && need > 0) {
+      size_t free_b = 0, total_b = 0;
+      cudaMemGetInfo(&free_b, &total_b);
+      oz_stream = need + ((size_t)4 << 30) > free_b;  // keep 4 GB for the call's workspaces
+    }
+    if (oz_stream) {
+      // two ring slots of column blocks: ~4 GB each by default (C5: 10^5 columns in ~7 blocks per site)
+      oz_cols = c->oz_block_cols > 0 ? round_up(c->oz_block_cols, 64)
+                                     : std::max(64, (int)(((size_t)4 << 30) / widest) / 64 * 64);
+      int ncol_max = 0;
+      for (int m = m_begin; m < m_end; ++m) ncol_max = std::max(ncol_max, c->sites[m].chi_r * D);
+      oz_cols = std::min(oz_cols, round_up(ncol_max, 64));
+      for (int w = 0; w < 2; ++w) {
+        CU(c, c->ozs_planes[w].ensure(widest / 2 * (size_t)round_up(2 * oz_cols, 256)), "alloc Ozaki digit ring");
+        CU(c, c->ozs_e[w].ensure((size_t)2 * oz_cols), "alloc Ozaki digit ring");
+      }
+      CU(c, cudaEventRecord(c->fork_ev, st), "stream fork");
+      CU(c, cudaStreamWaitEvent(c->copy_st, c->fork_ev, 0), "stream fork wait");
+    } else {
+      for (int m = m_begin; m < m_end; ++m) CU(c, ozaki_prepare_site(c->sites[m], D, c->oz_S), "Ozaki site digits");
+    }
   }
+  int oz_block = 0;  // streamed blocks issued in this call (ring slot = oz_block % 2)
+  mps_ctx::Rec oz_rec[mps_ctx::MAX_LANES];
 
 
   if (small_chain_ok(c, m_begin, m_end, n)) {
@@ -1305,7 +1349,7 @@ static int run_chain(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
                                         2LL * N, lst[l]);
         c->launches++;
         if (e != cudaSuccess) return cuda_fail(c, e, "c64 site_gemm launch");
-      } else if (ozaki) {
+      } else if (ozaki && !oz_stream) {
         const int n_pad = round_up(nl, 256);
         CU(c, ozaki_slice_state(v_in[l], nl, s.chi_l, c->oz_S, c->loz[l].p, n_pad, s.oz_ld, c->loz_e[l].p, lst[l]),
            "Ozaki state digits");
@@ -1313,6 +1357,11 @@ static int run_chain(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
                                      c->lcbuf[l].p, nl, s.chi_l, N, lst[l]);
         c->launches += 2;
         if (e != cudaSuccess) return cuda_fail(c, e, "Ozaki site_gemm launch");
+      } else if (ozaki) {  // streamed digits: the state's now, the site's per column block below
+        const int n_pad = round_up(nl, 256);
+        CU(c, ozaki_slice_state(v_in[l], nl, s.chi_l, c->oz_S, c->loz[l].p, n_pad, oz_ld(s.chi_l), c->loz_e[l].p,
+                                lst[l]), "Ozaki state digits");
+        c->launches++;
       } else {
         GemmOps o{v_in[l], vs_in[l], ld_vs_in, &s.tmap, s.gsum ? &s.tmap_gs : nullptr, c->lcbuf[l].p, nl, s.chi_l, N,
                   N};
@@ -1320,8 +1369,45 @@ static int run_chain(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
         if (rc) return rc;
       }
       if (c->profile & 1) {
-        cudaEventRecord(rg.b, lst[l]);
-        c->recs.push_back(rg);
+        if (ozaki && oz_stream) {  // timed around the streamed blocks below instead
+          c->event_pool.insert(c->event_pool.end(), {rg.a, rg.b});
+        } else {
+          cudaEventRecord(rg.b, lst[l]);
+          c->recs.push_back(rg);
+        }
+      }
+    }
+    if (ozaki && oz_stream) {
+      // site digits of this mode, column block by column block, sliced on the copy stream into the
+      // 2-slot ring while the previous block's GEMMs run; every lane's GEMM of a block waits for it
+      const int ld = oz_ld(s.chi_l), nblk = (N + oz_cols - 1) / oz_cols;
+      for (int bk = 0; bk < nblk; ++bk, ++oz_block) {
+        const int w = oz_block % 2, c0 = bk * oz_cols, nb = std::min(oz_cols, N - c0);
+        if (oz_block >= 2)
+          for (int l = 0; l < L; ++l) CU(c, cudaStreamWaitEvent(c->copy_st, c->slot_free[w][l], 0), "digit slot wait");
+        ozaki_slice_site_kernel<<<2 * nb, 128, 0, c->copy_st>>>(s.data + c0, s.chi_l, nb, c->oz_S, c->ozs_planes[w].p, ld,
+                                                                c->ozs_e[w].p, (long long)N);
+        CU(c, cudaGetLastError(), "Ozaki site digits (streamed)");
+        c->launches++;
+        CU(c, cudaEventRecord(c->slot_ready[w], c->copy_st), "digit slot ready");
+        for (int l = 0; l < L; ++l) {
+          const int r0 = lane_r0[l], nl = lane_r0[l + 1] - r0;
+          if ((c->profile & 1) && bk == 0) {  // K1 of this mode on lane l: first block .. last block
+            oz_rec[l] = mps_ctx::Rec{0, c->get_event(), c->get_event(), 8.0 * nl * (double)s.chi_l * N};
+            cudaEventRecord(oz_rec[l].a, lst[l]);
+          }
+          CU(c, cudaStreamWaitEvent(lst[l], c->slot_ready[w], 0), "digit slot ready wait");
+          cudaError_t e = launch_ozaki(c->oz_S, c->loz[l].p, round_up(nl, 256), c->loz_e[l].p, c->ozs_planes[w].p,
+                                       round_up(2 * nb, 256), c->ozs_e[w].p, ld, c->lcbuf[l].p + c0, nl, s.chi_l, nb,
+                                       lst[l], (long long)N);
+          c->launches++;
+          if (e != cudaSuccess) return cuda_fail(c, e, "Ozaki site_gemm launch (streamed)");
+          CU(c, cudaEventRecord(c->slot_free[w][l], lst[l]), "digit slot free");
+          if ((c->profile & 1) && bk == nblk - 1) {
+            cudaEventRecord(oz_rec[l].b, lst[l]);
+            c->recs.push_back(oz_rec[l]);
+          }
+        }
       }
     }
     if (slot >= 0) {  // the GEMMs of this mode are queued: free the slot for streamed site k+2
@@ -1398,7 +1484,7 @@ static int run_chain(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
       CU(c, cudaStreamWaitEvent(st, c->join_ev[l], 0), "join wait");
     }
   }
-  if (!streamed.empty()) {  // the copy stream's work is older than the GEMMs that waited on it
+  if (!streamed.empty() || oz_stream) {  // the copy stream's work is older than the GEMMs that waited on it
     CU(c, cudaEventRecord(c->join_ev[0], c->copy_st), "copy join");
     CU(c, cudaStreamWaitEvent(st, c->join_ev[0], 0), "copy join wait");
   }
@@ -1721,6 +1807,10 @@ void mps_destroy(mps_ctx* c) {
   }
   if (c->pe_out) cudaEventDestroy(c->pe_out);
   c->pipe_d.release();
+  for (int w = 0; w < 2; ++w) {
+    c->ozs_planes[w].release();
+    c->ozs_e[w].release();
+  }
   c->ones.release();
   c->io_d.release();
   if (c->io_h) cudaFreeHost(c->io_h);
@@ -1918,6 +2008,15 @@ int mps_set_gemm_mode(mps_ctx* c, int mode) {
   if (mode != 3 && mode != 4 && mode != 8)
     return fail(c, MPS_ERR_VALIDATION, "gemm mode must be 3 (3M), 4 (4M) or 8 (Ozaki int8), got %d", mode);
   c->gemm_mode = mode;
+  return MPS_OK;
+}
+
+int mps_set_ozaki_site_mode(mps_ctx* c, int mode, int block_cols) {
+  if (!c) return MPS_ERR_VALIDATION;
+  if (mode < 0 || mode > 2) return fail(c, MPS_ERR_VALIDATION, "Ozaki site mode must be 0, 1 or 2, got %d", mode);
+  if (block_cols < 0) return fail(c, MPS_ERR_VALIDATION, "block_cols must be >= 0");
+  c->oz_site_mode = mode;
+  c->oz_block_cols = block_cols;
   return MPS_OK;
 }
 

@@ -578,14 +578,16 @@ __global__ void ozaki_slice_rows_kernel(const double2* __restrict__ V, int K, in
 
 // Digit planes of a site's B_r^T (2N rows x 2K): row 2c = (Gr, -Gi, ...), row 2c+1 = (Gi, Gr, ...)
 // over the site's rows i; one CTA per B_r^T row r; tiled layout with TR = OZ_TR_B.
+// G may be a column block of a wider site: element (i, c) at G[i * ldg + c], c < N (ldg = 0: N).
 __global__ void ozaki_slice_site_kernel(const double2* __restrict__ G, int K, int N, int S, int8_t* __restrict__ planes,
-                                        int ld, int* __restrict__ e_out) {
+                                        int ld, int* __restrict__ e_out, long long ldg = 0) {
+  if (ldg == 0) ldg = N;
   __shared__ double red[32];
   const int r = blockIdx.x;
   const int c = r >> 1, q = r & 1;
   double m = 0.0;
   for (int i = threadIdx.x; i < K; i += blockDim.x) {
-    const double2 g = G[(long long)i * N + c];
+    const double2 g = G[(long long)i * ldg + c];
     m = fmax(m, fmax(fabs(g.x), fabs(g.y)));
   }
   for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -604,7 +606,7 @@ __global__ void ozaki_slice_site_kernel(const double2* __restrict__ G, int K, in
   for (int kk = threadIdx.x; kk < ld; kk += blockDim.x) {
     double x = 0.0;
     if (kk < 2 * K) {
-      const double2 g = G[(long long)(kk >> 1) * N + c];
+      const double2 g = G[(long long)(kk >> 1) * ldg + c];
       const int p = kk & 1;
       x = (p == 0) ? (q == 0 ? g.x : g.y) : (q == 0 ? -g.y : g.x);
     }

@@ -245,6 +245,11 @@ class MpsSampler:
         """Digits per operand of gemm mode 8 (mps_set_ozaki_digits): 7 (default), 6 or 5."""
         _native.check(self.L.mps_set_ozaki_digits(self.ctx, int(S)), self.ctx)
 
+    def set_ozaki_site_mode(self, mode: int, block_cols: int = 0):
+        """gemm mode 8 site digit planes (mps_set_ozaki_site_mode): 0 resident, 1 streamed per call in
+        column blocks of `block_cols` complex columns (0: ~4 GB each) on a copy stream, 2 auto."""
+        _native.check(self.L.mps_set_ozaki_site_mode(self.ctx, int(mode), int(block_cols)), self.ctx)
+
     def set_gemm_mode(self, mode: int):
         """K1 complex product: 3 (3M, default) or 4 (4M)."""
         _native.check(self.L.mps_set_gemm_mode(self.ctx, int(mode)), self.ctx)

@@ -270,6 +270,31 @@ def test_conjugate_view_sites_are_resolved(c1_sites):
     assert not any(G.is_conj() for G in dev.sites)
 
 
+@pytest.mark.parametrize("small_chain", [0, 1])
+def test_zero_probability_outcomes_and_extreme_uniforms(small_chain):
+    """Outcomes of exactly zero probability are never drawn, including for u = 0 and u = 1 - 2^-53
+    at the top of the CDF (oracle decision 4: the draw steps down to the largest k with p(k) > 0;
+    the clamp of sampler.py:694-695), through both kernels; counts equal the oracle's."""
+    D, M, N = 6, 3, 512
+    amp = np.sqrt(np.array([0.3, 0.2, 0.0, 0.5, 0.0, 0.0]))
+    sites = [amp.astype(np.complex128).reshape(1, 1, D) for _ in range(M)]
+    u = stream_uniforms(21, 0, N, M)
+    u[0, :] = 0.0
+    u[1, :] = 1.0 - 2.0 ** -53
+    u[2, :] = 0.5  # exactly the CDF boundary 0.3 + 0.2: flagged, and p = 0 at k = 2 forces k = 3
+    cfg = MpsSamplerConfig(N=N, seed=21, batch_size=N)
+    with MpsSampler(MPS(sites)) as eng:
+        eng.set_small_chain(small_chain)
+        res = eng.sample(cfg, uniforms=u, return_marginals=True)
+    ref = orc.sample_chain(sites, u, return_marginals=True)
+    assert set(np.unique(res["counts"])) <= {0, 1, 3}
+    assert (res["counts"][0] == 0).all() and (res["counts"][1] == 3).all()
+    flagged = (res["status"] & _native.MPS_STATUS_FLAGGED) != 0
+    assert flagged[2] and ref["flagged"][2]
+    assert np.array_equal(res["counts"][~flagged], ref["counts"][~flagged])
+    assert np.abs(res["marginals"] - ref["marginals"]).max() <= MARG_TOL
+
+
 def test_shard_invariance(c2_sites):
     """Contiguous index shards (the sample-sharded multi-GPU layout) reproduce the batch."""
     N = 600
@@ -397,7 +422,7 @@ def test_staged_and_global_draw_agree():
     _check_parity(sites, res, stream_uniforms(2, 0, N, M), alpha=alpha_stream(2, 0, N, M, 0.5))
 
 
-@pytest.mark.parametrize("mode,cfg_id", [(m, c) for m in (3, 4) for c in range(-2, 11 if m == 3 else 6)])
+@pytest.mark.parametrize("mode,cfg_id", [(m, c) for m in (3, 4) for c in range(-2, 12 if m == 3 else 6)])
 def test_gemm_configs_bit_identical(cfg_id, mode):
     """Within a product mode every tile config (and the autotuner's pick) gives the same bits."""
     L = _native.lib()
@@ -753,6 +778,32 @@ def test_ozaki_chi1000_and_invariance(digits):
     for o in outs[1:]:
         assert np.array_equal(o["counts"], outs[0]["counts"])
         assert np.array_equal(o["marginals"], outs[0]["marginals"])
+
+
+@pytest.mark.parametrize("lanes,block", [(1, 128), (2, 320), (1, 0)])
+def test_ozaki_streamed_site_digits_bit_identical(c2_sites, lanes, block):
+    """gemm mode 8 with the sites' digit planes sliced per call, column block by column block, into
+    the 2-slot ring on the copy stream (mps_set_ozaki_site_mode 1; how C5 fits) gives the same bits
+    as resident planes; a chi = 1000 chain checks the blocked K1 against the oracle."""
+    cfg = MpsSamplerConfig(N=300, seed=13, alpha_sigma=0.5, batch_size=150)
+    outs = []
+    for mode in (0, 1):
+        with MpsSampler(MPS(c2_sites)) as eng:
+            eng.set_gemm_mode(8)
+            eng.set_lanes(lanes)
+            eng.set_ozaki_site_mode(mode, block)
+            outs.append(eng.sample(cfg, return_marginals=True))
+    assert np.array_equal(outs[0]["counts"], outs[1]["counts"])
+    assert np.array_equal(outs[0]["marginals"], outs[1]["marginals"])
+    if block == 320:
+        M, chi, D, N = 5, 1000, 10, 64
+        sites = orc.random_mps(M, chi, D, seed=9)
+        c = MpsSamplerConfig(N=N, seed=9, alpha_sigma=0.7, batch_size=N)
+        with MpsSampler(MPS(sites)) as eng:
+            eng.set_gemm_mode(8)
+            eng.set_ozaki_site_mode(1, 2048)
+            res = eng.sample(c, return_marginals=True)
+        _check_parity(sites, res, stream_uniforms(9, 0, N, M), alpha=alpha_stream(9, 0, N, M, 0.7))
 
 
 @pytest.mark.parametrize("lanes,sums", [(1, True), (2, True), (2, False)])
