@@ -39,7 +39,10 @@ constexpr int SC_FW = SC_FMAX / 8;                // per compute warp (1)
 #define SC_KS_DEF 2
 #endif
 constexpr int SC_KS = SC_KS_DEF;                  // k stages (8 complex k each) per ring slot
-constexpr int SC_STAGES = 12 / SC_KS;             // ring slots (96 KB of Gamma in flight)
+#ifndef SC_KSTAGES_DEF  // k stages of Gamma in flight (tuning knob)
+#define SC_KSTAGES_DEF 12
+#endif
+constexpr int SC_STAGES = SC_KSTAGES_DEF / SC_KS; // ring slots (12 k stages = 96 KB of Gamma in flight)
 #ifndef SC_KW
 #define SC_KW 8
 #endif

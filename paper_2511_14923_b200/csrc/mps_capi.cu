@@ -28,6 +28,7 @@
 #include "ozaki_gemm.cuh"
 #include "site_gemm.cuh"
 #include "chain_small.cuh"
+#include "chain_small2.cuh"
 
 using namespace mps;
 
@@ -763,9 +764,22 @@ static cudaError_t launch_c64_gemm(const float* ahi, const float* alo, const flo
 }
 
 // ---- small chains: the whole mode loop in one persistent cluster launch (chain_small.cuh) ----
+// small-chain variant: 2 = halves of each group pipelined (chain_small2.cuh), 1 = lock step
+static int small_chain_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MPS_SMALL_CHAIN_V2");
+    v = (e && e[0] == '0') ? 1 : 2;  // default: the pipelined variant (C2 +13%, C1 +8%, same bits)
+  }
+  return v;
+}
 static void (*small_chain_kernel_for(int D))(ChainArgs) {
+  if (small_chain_variant() == 2)
+    return D == 10 ? small_chain2_kernel<10> : D == 4 ? small_chain2_kernel<4> : small_chain2_kernel<0>;
   return D == 10 ? small_chain_kernel<10> : D == 4 ? small_chain_kernel<4> : small_chain_kernel<0>;
 }
+static int sc_threads() { return small_chain_variant() == 2 ? SC2_THREADS : SC_THREADS; }
+static int sc_smem() { return small_chain_variant() == 2 ? SC2_SMEM : SC_SMEM; }
 
 // co-resident 16-CTA clusters of the instantiation for D on the current device (0: none fit)
 static int small_chain_capacity(int D) {
@@ -780,12 +794,12 @@ static int small_chain_capacity(int D) {
     if (it != cap.end()) return it->second;
   }
   int num = 0;
-  if (set_smem_once((const void*)kern, SC_SMEM) == cudaSuccess &&
+  if (set_smem_once((const void*)kern, sc_smem()) == cudaSuccess &&
       set_attr_once((const void*)kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
     cudaLaunchConfig_t q = {};
     q.gridDim = dim3(SC_CL * 32);
-    q.blockDim = dim3(SC_THREADS);
-    q.dynamicSmemBytes = SC_SMEM;
+    q.blockDim = dim3(sc_threads());
+    q.dynamicSmemBytes = sc_smem();
     cudaLaunchAttribute a[1];
     a[0].id = cudaLaunchAttributeClusterDimension;
     a[0].val.clusterDim.x = SC_CL;
@@ -817,10 +831,16 @@ static bool small_chain_ok(const mps_ctx* c, int m_begin, int m_end, int n) {
   if (c->small_chain == 1) return true;
   const int waves = ((n + SC_CL - 1) / SC_CL + cap - 1) / cap;
   double t_chain = 0.0, t_mode = 0.0;
+  const bool v2 = small_chain_variant() == 2;
   for (int m = m_begin; m < m_end; ++m) {
     const double fl = 8.0 * c->sites[m].chi_l * (double)c->sites[m].chi_r * c->D;  // per sample row
-    t_chain += waves * (3.5e-6 + SC_CL * fl / 2.4e12);
-    t_mode += std::max(13e-6, n * fl / 20e12);
+    if (v2) {  // fitted to the round-2 sweeps (C1: n = 100..600, C2: n = 100..500)
+      t_chain += waves * (3.0e-6 + SC_CL * fl / 3.3e12);
+      t_mode += 10.5e-6 + n * fl / 30e12;
+    } else {
+      t_chain += waves * (3.5e-6 + SC_CL * fl / 2.4e12);
+      t_mode += std::max(13e-6, n * fl / 20e12);
+    }
   }
   return t_chain <= t_mode;
 }
@@ -853,8 +873,8 @@ static cudaError_t launch_small_chain(mps_ctx* c, const ChainArgs& P, cudaStream
   const int groups = (P.n + SC_CL - 1) / SC_CL;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(SC_CL * std::min(groups, mc));
-  cfg.blockDim = dim3(SC_THREADS);
-  cfg.dynamicSmemBytes = SC_SMEM;
+  cfg.blockDim = dim3(sc_threads());
+  cfg.dynamicSmemBytes = sc_smem();
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1978,6 +1998,9 @@ int mps_set_small_chain(mps_ctx* c, int mode) {
 #ifdef SC_TRACE
 int mps_debug_chain_trace(long long* out) {
   return cudaMemcpyFromSymbol(out, sc_trace, sizeof(sc_trace)) == cudaSuccess ? MPS_OK : MPS_ERR_GENERIC;
+}
+int mps_debug_chain2_trace(long long* out) {
+  return cudaMemcpyFromSymbol(out, sc2_trace, sizeof(sc2_trace)) == cudaSuccess ? MPS_OK : MPS_ERR_GENERIC;
 }
 #endif
 
