@@ -154,6 +154,14 @@ __global__ void __launch_bounds__(SC2_THREADS, 1) small_chain2_kernel(const __gr
       const bool first = (m == P.m_begin);
       for (int h = 0; h < 2; ++h) {
         if (first) {  // new group: rows of half h <- state_in (or v = 1), zero elsewhere
+          if (q > 0) {
+            // the previous group's last draws of half h are finished (one 16-byte token from each of
+            // its 8 owners): their C buffers are free and their next C-row expects are armed, so this
+            // half's K1 may send the new group's entries
+            mbar_wait(&v_full[h], vph[h] & 1);
+            ++vph[h];
+          }
+          sc2_bar_k1();  // every K1 warp is done reading these rows for the previous group
           for (int e = tid; e < 8 * SC_KMAX; e += SC2_K1) {
             const int r = 8 * h + e / SC_KMAX, j = e % SC_KMAX;
             double2 v = make_double2(0.0, 0.0);
@@ -168,10 +176,12 @@ __global__ void __launch_bounds__(SC2_THREADS, 1) small_chain2_kernel(const __gr
           ++vph[h];
         }
         if (warp == 0) SC2_STAMP(0, q, 4 * h + 1);
-        // expect half h's next V tile (8 rows x jpad entries) before any of its rows can be drawn: the
-        // draws of mode m need this CTA's K1_h(m) entries, which come after this point
-        if (tid == 0 && q + 1 < nsteps && P.m_begin + (q + 1) % nmodes != P.m_begin)
-          mbar_arrive_expect_tx(&v_full[h], (uint32_t)(8 * ((chi_r + 7) & ~7) * 16));
+        // expect half h's next V tile (8 rows x jpad entries) -- or, before a new group, the 8 owners'
+        // end-of-group tokens -- before any of its rows can be drawn: the draws of mode m need this
+        // CTA's K1_h(m) entries, which come after this point
+        if (tid == 0 && q + 1 < nsteps)
+          mbar_arrive_expect_tx(&v_full[h], P.m_begin + (q + 1) % nmodes != P.m_begin
+                                                ? (uint32_t)(8 * ((chi_r + 7) & ~7) * 16) : 8u * 16u);
         double t1[2] = {0.0, 0.0}, t2[2] = {0.0, 0.0}, t3[2] = {0.0, 0.0};
         auto kstage = [&](const uint8_t* st, int kt) {  // site_gemm3m_kernel's per-accumulator k order
 #pragma unroll
@@ -360,9 +370,15 @@ __global__ void __launch_bounds__(SC2_THREADS, 1) small_chain2_kernel(const __gr
           emit(j, e);
         }
       }
-      sc2_bar_draw();  // every draw thread is done with T, red and k_s / scale_s before reuse
+      sc2_bar_draw();  // every draw thread is done with T, red, C and k_s / scale_s before reuse
       if (dw == 0) SC2_STAMP(2, q, 4);
       if (dt == 0) mbar_arrive(&t_free[q & 1]);
+      if (last && q + 1 < nsteps && dt < SC_CL) {
+        // end of this group: a 16-byte token into row `rank`'s padding slot of every CTA's V tile
+        // releases the next group's K1 of this half (it must not overwrite C buffers still being read)
+        const uint32_t vo = vt_addr + (uint32_t)(rank * SC_VP + SC_KMAX * 16);
+        sc_st_async(sc_mapa(vo, (uint32_t)dt), 0.0, 0.0, sc_mapa(vbar_addr, (uint32_t)dt));
+      }
     }
   }
   sc_cluster_sync();  // no CTA leaves while a peer may still st.async into it
