@@ -57,6 +57,7 @@ ONE_GPU = os.environ.get("MPS_BENCH_ONE_GPU") == "1"
 # MPS_BENCH_PROFILE_RANGE=1: bracket the timed steps with cudaProfilerStart/Stop, so
 # `ncu --profile-from-start off --metrics gpu__time_duration.sum` lists exactly their launches
 PROFILE_RANGE = os.environ.get("MPS_BENCH_PROFILE_RANGE") == "1"
+RANK_INFO: dict = {}  # every rank's device (N > 1), printed next to `config`
 
 
 def dist_barrier(local):
@@ -784,8 +785,7 @@ def main():
               if hasattr(torch.cuda.get_device_properties(local), "pci_bus_id") else None}
         ranks = [None] * world
         dist.all_gather_object(ranks, me)
-        config["ranks"] = ranks
-        config["backend"] = BACKEND
+        RANK_INFO.update(ranks=ranks, backend=BACKEND)  # top-level keys: `config` stays the reference arm's
         if rank == 0:
             print(f"[bench] {BACKEND} process group up: world={world}, devices "
                   + ", ".join(f"r{r['rank']}:cuda:{r['local_rank']}" for r in ranks), file=sys.stderr, flush=True)
@@ -798,7 +798,7 @@ def main():
             return
         line = run_pipelined(args, rank, world, local, W, K, config, dims)
         if rank == 0:
-            print(json.dumps(line), flush=True)
+            print(json.dumps(dict(line, **RANK_INFO)), flush=True)
         if world > 1:
             dist.destroy_process_group()
         return
@@ -1064,7 +1064,7 @@ def main():
         v, cores, sample = CpuBaseline(args.config).run()
         line["cpu_baseline"] = {"value": v, "unit": "samples/s", "cores": cores, "kind": "port", "sample": sample}
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        print(json.dumps(dict(line, **RANK_INFO)), flush=True)
     eng.close()
     if world > 1:
         dist.destroy_process_group()

@@ -74,7 +74,7 @@ def test_gpu_arm_json_line_and_two_rank_path():
     assert len(lines) == 1  # rank 0 only
     d2 = json.loads(lines[0])
     assert d2["n_gpus"] == 2 and d2["scaling"] == "weak" and d2["value"] > 0 and d2["valid_outputs"]
-    assert [r["rank"] for r in d2["config"]["ranks"]] == [0, 1]
+    assert [r["rank"] for r in d2["ranks"]] == [0, 1] and "ranks" not in d2["config"]
     # torchrun with a world size that contradicts --gpus fails loudly
     out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                           "--master-addr", "127.0.0.1", "--master-port", "29547", str(ROOT / "bench.py"), "--gpus", "3",
