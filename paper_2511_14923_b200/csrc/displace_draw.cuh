@@ -349,7 +349,10 @@ __global__ void __launch_bounds__(DRAW_THREADS, C64 ? 8 : 4)
     const uint32_t bytes = (uint32_t)(nj * D * (int)sizeof(ElemT));
     uint64_t* bar = &ring_bar[u % NS];
     mbar_arrive_expect_tx(bar, bytes);
-    bulk_load_1d(ring_smem + (size_t)(u % NS) * chunk_elems * sizeof(ElemT), Crow + (long long)j0 * D, bytes, bar);
+    // pass 1 (u < nchunks) keeps the row's lines in L2 for pass 2's re-read, pass 2 lets them go:
+    // DRAM reads drop from 1.16x to 1.00x the row bytes at C3 (profiles/r02_ncu_k23_draw_l2hints.txt)
+    bulk_load_1d_hint(ring_smem + (size_t)(u % NS) * chunk_elems * sizeof(ElemT), Crow + (long long)j0 * D, bytes, bar,
+                      u < nchunks);
   };
   auto ring_slot = [&](int u) -> const ElemT* {
     mbar_wait(&ring_bar[u % NS], (u / NS) & 1);
