@@ -71,7 +71,7 @@ def cmd_sample(args) -> int:
     mps = load_mps(args.mps, device="cuda" if args.device_sites else None)
     config = MpsSamplerConfig(N=args.samples, seed=args.seed, alpha_sigma=args.alpha_sigma,
                               batch_size=args.batch_size, device=args.device)
-    batch = batch_sample(config, mps)
+    batch = batch_sample(config, mps, start=args.start)  # indices start..start+N-1: runs resume by range
     # the rows' sample indices and the displacement law travel with the counts, so `evaluate`
     # scores each row under its own streams (failed samples are dropped from batch.counts)
     save_counts(args.out, batch.counts, mps.D, seed=args.seed, alpha_sigma=args.alpha_sigma, indices=batch.indices)
@@ -165,6 +165,8 @@ def build_parser() -> argparse.ArgumentParser:
     s = sub.add_parser("sample", help="draw photon-count samples on the GPU")
     s.add_argument("--mps", required=True)
     s.add_argument("--samples", type=int, required=True)
+    s.add_argument("--start", type=int, default=0,
+                   help="first sample index (counter streams): a run resumes or shards by index range")
     s.add_argument("--seed", type=int, default=0)
     s.add_argument("--alpha-sigma", type=float, default=None, help="alpha ~ CN(0, sigma^2) per sample and mode")
     s.add_argument("--batch-size", type=int, default=None)

@@ -317,12 +317,16 @@ class MpsSampler:
 
 
 def batch_sample(config: MpsSamplerConfig, mps: MPS, disp=None, alpha=None, uniforms=None,
-                 sampler: MpsSampler | None = None) -> MpsSampleBatch:
-    """Generate N samples with the B200 engine (gbsemu batch_sample, sampler.py:706-761).
+                 sampler: MpsSampler | None = None, start: int = 0) -> MpsSampleBatch:
+    """Generate N samples with the B200 engine (gbsemu batch_sample, sampler.py:706-761): sample
+    indices start..start+N-1 of the counter streams, so a long run resumes (or shards) by index
+    range with identical output.
 
     Failed samples (non-finite or zero step norm) are dropped and counted;
     flagged samples (a draw within 1e-10 of a CDF boundary) are kept and counted.
     """
+    if start < 0:
+        raise ValidationError("start must be >= 0")
     if config.method not in METHODS:
         raise ValidationError(f"unknown method {config.method!r}")
     if not isinstance(mps, MPS):
@@ -337,7 +341,7 @@ def batch_sample(config: MpsSamplerConfig, mps: MPS, disp=None, alpha=None, unif
     own = sampler is None
     eng = sampler or MpsSampler(mps, device=config.device)
     try:
-        res = eng.sample(config, disp=disp, alpha=alpha, uniforms=uniforms)
+        res = eng.sample(config, start=start, stop=start + config.N, disp=disp, alpha=alpha, uniforms=uniforms)
     finally:
         if own:
             eng.close()
@@ -351,7 +355,7 @@ def batch_sample(config: MpsSamplerConfig, mps: MPS, disp=None, alpha=None, unif
         M=mps.M, N=n_ok, counts=counts, method="mps", seed=config.seed, D=mps.D, chi=mps.chi,
         wall_time=wall, per_sample_mean=wall / max(n_ok, 1), n_failed=int(config.N - n_ok),
         n_flagged=int(((st & _native.MPS_STATUS_FLAGGED) != 0)[keep].sum()),
-        indices=np.nonzero(keep)[0],
+        indices=start + np.nonzero(keep)[0],
     )
 
 

@@ -305,6 +305,16 @@ def test_shard_invariance(c2_sites):
     assert np.array_equal(np.concatenate(parts), full)
 
 
+def test_batch_sample_resumes_by_index_range(c1_sites):
+    """batch_sample(start=s): samples s..s+N-1 of the streams, so a run split into index ranges (a
+    resumed or sharded run) reproduces the single run, indices included."""
+    full = batch_sample(MpsSamplerConfig(N=500, seed=8, alpha_sigma=0.5, batch_size=128), MPS(c1_sites))
+    a = batch_sample(MpsSamplerConfig(N=230, seed=8, alpha_sigma=0.5, batch_size=64), MPS(c1_sites))
+    b = batch_sample(MpsSamplerConfig(N=270, seed=8, alpha_sigma=0.5, batch_size=100), MPS(c1_sites), start=230)
+    assert np.array_equal(np.concatenate([a.counts, b.counts]), full.counts)
+    assert np.array_equal(np.concatenate([a.indices, b.indices]), full.indices)
+
+
 def test_sample_one_matches_batch(c1_sites):
     cfg = MpsSamplerConfig(N=6, seed=9, alpha_sigma=0.5)
     mps = MPS(c1_sites)
