@@ -240,7 +240,7 @@ struct mps_ctx {
   // micro-batches' compute; device slots are double-buffered, one host synchronisation per call
   int micro = 0;
   cudaStream_t cs_in = nullptr, cs_out = nullptr;
-  cudaEvent_t pe_in[2] = {}, pe_comp[2] = {}, pe_out = nullptr;
+  cudaEvent_t pe_in[2] = {}, pe_comp[2] = {}, pe_d2h[2] = {}, pe_out = nullptr;
   DevBuf<uint8_t> pipe_d;
   // workspaces
   DevBuf<double2> ones;
@@ -920,7 +920,8 @@ int mps_create(int n_dev, const int* dev_ids, int layout, mps_ctx** out) {
        cudaEventCreateWithFlags(&c->pe_out, cudaEventDisableTiming) == cudaSuccess;
   for (int w = 0; ok && w < 2; ++w)
     ok = cudaEventCreateWithFlags(&c->pe_in[w], cudaEventDisableTiming) == cudaSuccess &&
-         cudaEventCreateWithFlags(&c->pe_comp[w], cudaEventDisableTiming) == cudaSuccess;
+         cudaEventCreateWithFlags(&c->pe_comp[w], cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&c->pe_d2h[w], cudaEventDisableTiming) == cudaSuccess;
   for (int w = 0; ok && w < 2; ++w) {
     ok = cudaEventCreateWithFlags(&c->slot_ready[w], cudaEventDisableTiming) == cudaSuccess;
     for (int l = 0; ok && l < mps_ctx::MAX_LANES; ++l)
@@ -1590,7 +1591,10 @@ static int sample_pipelined(mps_ctx* c, int m_begin, int m_end, int64_t first_in
     const size_t r0 = (size_t)t * nb;
     const int nt = std::min(nb, n - (int)r0);
     uint8_t* slot = c->pipe_d.p + (size_t)w * slot_bytes;
-    if (t >= 2) CU(c, cudaStreamWaitEvent(c->cs_in, c->pe_comp[w], 0), "slot free");
+    if (t >= 2) {  // slot w: micro-batch t-2's kernels AND the D2H of its in-out fields are done
+      CU(c, cudaStreamWaitEvent(c->cs_in, c->pe_comp[w], 0), "slot free");
+      CU(c, cudaStreamWaitEvent(c->cs_in, c->pe_d2h[w], 0), "slot read back");
+    }
     for (int i = 0; i < 6; ++i)
       if (f[i].in)
         CU(c, cudaMemcpyAsync(slot + f[i].slot_off, hsrc(i, r0), (size_t)nt * f[i].row, cudaMemcpyHostToDevice,
@@ -1621,6 +1625,7 @@ static int sample_pipelined(mps_ctx* c, int m_begin, int m_end, int64_t first_in
       if (f[i].out)
         CU(c, cudaMemcpyAsync(hdst(i, r0), slot + f[i].slot_off, (size_t)nt * f[i].row, cudaMemcpyDeviceToHost,
                               c->cs_out), "D2H micro-batch");
+    CU(c, cudaEventRecord(c->pe_d2h[w], c->cs_out), "outputs read");
   }
   CU(c, cudaEventRecord(c->pe_out, c->cs_out), "outputs done");
   CU(c, cudaStreamWaitEvent(st, c->pe_out, 0), "join");
@@ -1824,6 +1829,7 @@ void mps_destroy(mps_ctx* c) {
   for (int w = 0; w < 2; ++w) {
     if (c->pe_in[w]) cudaEventDestroy(c->pe_in[w]);
     if (c->pe_comp[w]) cudaEventDestroy(c->pe_comp[w]);
+    if (c->pe_d2h[w]) cudaEventDestroy(c->pe_d2h[w]);
   }
   if (c->pe_out) cudaEventDestroy(c->pe_out);
   c->pipe_d.release();

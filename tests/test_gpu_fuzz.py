@@ -69,3 +69,46 @@ def test_random_chain_vs_oracle(case):
     flagged = (status & _native.MPS_STATUS_FLAGGED) != 0
     mism = (counts != free["counts"]).any(axis=1) & ~flagged & ~free["flagged"]
     assert not mism.any(), int(mism.sum())
+
+
+def _split_cases(n_cases=24, seed=77):
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(n_cases):
+        M = int(rng.integers(2, 9))
+        out.append(dict(M=M, mid=int(rng.integers(1, M)), chi=int(rng.choice([3, 16, 40, 100])),
+                        D=int(rng.choice([2, 4, 10])), N=int(rng.integers(1, 260)),
+                        dtype=str(rng.choice(["complex128", "complex128", "complex64"])),
+                        micro=int(rng.choice([0, 32])), small_chain=int(rng.integers(0, 3)),
+                        lanes=int(rng.integers(1, 3)), seed=int(rng.integers(0, 2**31))))
+    return out
+
+
+@pytest.mark.parametrize("case", _split_cases(), ids=lambda c: "M{M}-mid{mid}-chi{chi}-D{D}-N{N}-{dtype}".format(**c))
+def test_random_stage_split_equals_full_chain(case):
+    """A chain run as two stages (modes [0, mid) then [mid, M), the n x chi state handed over on the
+    device) gives the same bits as the one-stage run, for both dtypes, micro-batched host outputs,
+    lanes and small-chain selection -- the mode-pipelined layout's invariant."""
+    c = case
+    sites = [s.astype(c["dtype"]) for s in orc.random_mps(c["M"], c["chi"], c["D"], seed=c["seed"] % 1000)]
+    mps = MPS(sites)
+    N, M, D, mid = c["N"], c["M"], c["D"], c["mid"]
+    cdt = torch.complex64 if c["dtype"] == "complex64" else torch.complex128
+    chi_mid = mps.bond_dims[mid]
+    with MpsSampler(mps) as eng:
+        eng.set_lanes(c["lanes"])
+        eng.set_small_chain(c["small_chain"])
+        eng.set_micro_batch(c["micro"])
+        eng.set_streams(c["seed"], 0.5)
+        full_c = np.zeros((N, M), dtype=np.int32)
+        full_m = np.zeros((N, M, D))
+        eng.run(0, N, full_c, marginals=full_m, status=np.zeros(N, dtype=np.uint8))
+        st = np.zeros(N, dtype=np.uint8)
+        c2, m2 = np.zeros((N, M), dtype=np.int32), np.zeros((N, M, D))
+        mid_state = torch.zeros((N, chi_mid), dtype=cdt, device="cuda")
+        eng.run(0, N, c2, m_begin=0, m_end=mid, state_out=mid_state, marginals=m2, status=st)
+        eng.run(0, N, c2, m_begin=mid, m_end=M, state_in=mid_state, marginals=m2, status=st)
+    dm = np.abs(full_m - m2).max(axis=(0, 2))
+    assert np.array_equal(full_c, c2) and np.array_equal(full_m, m2), (
+        c, "modes with marginal differences", np.nonzero(dm)[0].tolist(), float(dm.max()),
+        "rows", np.nonzero(np.abs(full_m - m2).max(axis=(1, 2)))[0][:10].tolist())
