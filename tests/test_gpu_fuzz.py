@@ -112,3 +112,60 @@ def test_random_stage_split_equals_full_chain(case):
     assert np.array_equal(full_c, c2) and np.array_equal(full_m, m2), (
         c, "modes with marginal differences", np.nonzero(dm)[0].tolist(), float(dm.max()),
         "rows", np.nonzero(np.abs(full_m - m2).max(axis=(1, 2)))[0][:10].tolist())
+
+
+def _knob_cases(n_cases=32, seed=5150):
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(n_cases):
+        out.append(dict(M=int(rng.integers(1, 7)), chi=int(rng.choice([2, 16, 60, 130])), D=int(rng.choice([3, 4, 10])),
+                        N=int(rng.integers(1, 400)), gemm=int(rng.choice([3, 8])), seed=int(rng.integers(0, 2**31)),
+                        knobs=dict(lanes=int(rng.integers(1, 5)), micro=int(rng.choice([0, 40, 100])),
+                                   small_chain=int(rng.integers(0, 3)), sum_planes=bool(rng.integers(0, 2)),
+                                   stream_sites=bool(rng.integers(0, 2)), borrow=bool(rng.integers(0, 2)),
+                                   oz_site_mode=int(rng.integers(0, 3)), batch=int(rng.choice([1, 33, 128, 1000])),
+                                   forced=bool(rng.integers(0, 2)))))
+    return out
+
+
+def _run_knobs(sites, c, k):
+    """One sampling (or, with k["forced"], teacher-forced evaluation) pass under the given knobs."""
+    N, M, D = c["N"], c["M"], c["D"]
+    stream = k.get("stream_sites", False) and c["gemm"] == 3
+    if stream:
+        mps = MPS(sites)
+    elif k.get("borrow", False):
+        mps = MPS([torch.from_numpy(G).cuda() for G in sites])
+    else:
+        mps = MPS(sites)
+    with MpsSampler(mps, sum_planes=k.get("sum_planes", True), stream_sites=stream) as eng:
+        eng.set_gemm_mode(c["gemm"])
+        eng.set_lanes(k.get("lanes", 1))
+        eng.set_micro_batch(k.get("micro", 0))
+        eng.set_small_chain(k.get("small_chain", 2))
+        eng.set_ozaki_site_mode(k.get("oz_site_mode", 0), 64)
+        eng.set_streams(c["seed"], 0.5)
+        counts = np.zeros((N, M), dtype=np.int32)
+        if k.get("forced", False):
+            counts[:] = np.random.default_rng(c["seed"]).integers(0, min(D, 3), size=(N, M))
+            eng.set_forced(True)
+        marg = np.zeros((N, M, D))
+        status = np.zeros(N, dtype=np.uint8)
+        B = k.get("batch", N)
+        for s0 in range(0, N, B):
+            b = min(B, N - s0)
+            eng.run(s0, b, counts[s0:s0 + b], marginals=marg[s0:s0 + b], status=status[s0:s0 + b])
+    return counts, marg, status
+
+
+@pytest.mark.parametrize("case", _knob_cases(), ids=lambda c: "M{M}-chi{chi}-D{D}-N{N}-g{gemm}".format(**c))
+def test_random_knobs_bit_identical(case):
+    """Every engine knob that promises identical results (lanes, micro-batching, small-chain selection,
+    sum planes, host-streamed / borrowed / copied sites, streamed INT8 digit planes, call batch size)
+    gives the same bits as the plain configuration, sampling or teacher-forced."""
+    c = case
+    sites = orc.random_mps(c["M"], c["chi"], c["D"], seed=c["seed"] % 997)
+    plain = _run_knobs(sites, c, dict(forced=c["knobs"]["forced"]))
+    other = _run_knobs(sites, c, c["knobs"])
+    for a, b, name in zip(plain, other, ("counts", "marginals", "status")):
+        assert np.array_equal(a, b), (name, c)
