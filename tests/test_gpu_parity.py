@@ -108,6 +108,9 @@ def test_displacement_kernel_vs_oracle():
         assert np.abs(out.cpu().numpy() - orc.displacement_matrix(a, D)).max() < 1e-11
 
 
+# numpy routes key lists holding ints >= 2^63 through float64 (2^64 - 1 casts with a RuntimeWarning);
+# the device stream reproduces that key derivation, so the warning is the oracle's expected path.
+@pytest.mark.filterwarnings("ignore:invalid value encountered in cast:RuntimeWarning")
 @pytest.mark.parametrize("seed,first,count,M", [(0, 0, 200, 8), (7, 100, 300, 16), (123456789, 63, 3, 64),
                                                  (2**63 + 5, 1000, 130, 5), (2**64 - 1, 7, 9, 3),
                                                  (1, 10**9, 70, 144)])
