@@ -1618,7 +1618,14 @@ static int sample_pipelined(mps_ctx* c, int m_begin, int m_end, int64_t first_in
       sin = state_in ? (const void*)((const float2*)state_in + r0 * chi0) : nullptr;
       sout = state_out ? (void*)((float2*)state_out + r0 * chiM) : nullptr;
     }
-    if (int rc = run_chain(c, m_begin, m_end, first_index + (int64_t)r0, nt, io, sin, sout, st)) return rc;
+    if (int rc = run_chain(c, m_begin, m_end, first_index + (int64_t)r0, nt, io, sin, sout, st)) {
+      // copies already queued still read / write the caller's pinned arrays and the staging buffer:
+      // drain them before handing the buffers back
+      cudaStreamSynchronize(c->cs_in);
+      cudaStreamSynchronize(c->cs_out);
+      cudaStreamSynchronize(st);
+      return rc;
+    }
     CU(c, cudaEventRecord(c->pe_comp[w], st), "compute done");
     CU(c, cudaStreamWaitEvent(c->cs_out, c->pe_comp[w], 0), "outputs wait");
     for (int i = 3; i < 6; ++i)
