@@ -132,8 +132,23 @@ def parity_tol(args):
     return 1e-10
 
 
+def parity_rel_tol(args):
+    """Relative bar on the marginals above parity_rel_floor: the absolute bar, except complex64, whose
+    fp32 state drifts to ~1e-3 relative over the 64 C3 modes (1e-2 relative above p = 1e-3,
+    tests/test_gpu_headline.py)."""
+    return 1e-2 if args.dtype == "c64" else parity_tol(args)
+
+
+def parity_rel_floor(args):
+    """Marginals above this floor are held to the relative bar (tests/_parity.py P_FLOOR; complex64:
+    tests/test_gpu_parity.py C64_REL_FLOOR -- fp32 state rounding gives ~1e-7 / p where the einsum
+    cancels); smaller ones to the absolute bar."""
+    return 1e-3 if args.dtype == "c64" else 1e-12
+
+
 def parity_spot_check(eng, mps, m_begin, m_end, first, n_chk, stream, sigma, uniforms=None, alpha=None,
-                      state_in=None, ref_counts=None, gemm_mode=None, tol=1e-10):
+                      state_in=None, ref_counts=None, gemm_mode=None, tol=1e-10, rel_floor=1e-12,
+                      rel_tol=None):
     """Parity of the bench's own run against the oracle (the checker, never the thing timed):
     n_chk samples starting at global index `first` through sites [m_begin, m_end) of the bench's
     device-resident sites, with marginals; the oracle follows the GPU's realised path
@@ -167,7 +182,7 @@ def parity_spot_check(eng, mps, m_begin, m_end, first, n_chk, stream, sigma, uni
     free = orc.sample_chain(sites, u_all[:, cols], alpha=a_all[:, cols], state_in=v0)
     pg, pc = marg_h[:, cols], forced["marginals"]
     d = np.abs(pg - pc)
-    big = pc > 1e-12
+    big = pc > rel_floor
     rel = float((d[big] / pc[big]).max()) if big.any() else 0.0
     flagged = (st_h & 2) != 0
     mism = (cnt_h[:, cols] != free["counts"]).any(axis=1) & ~flagged & ~free["flagged"]
@@ -179,10 +194,11 @@ def parity_spot_check(eng, mps, m_begin, m_end, first, n_chk, stream, sigma, uni
         ortho = max(ortho, float((A @ A.conj().T - eye).abs().max().item()))
     same = None if ref_counts is None else bool(np.array_equal(ref_counts[:, cols], cnt_h[:, cols]))
     site_tol = 1e-12 if tol <= 1e-9 else 1e-4  # complex64 sites are orthonormal to fp32 rounding (~sqrt(N) eps)
-    ok = bool(d.max() <= tol and rel <= tol and not mism.any() and not (st_h & 1).any() and ortho < site_tol
+    rel_tol = tol if rel_tol is None else rel_tol
+    ok = bool(d.max() <= tol and rel <= rel_tol and not mism.any() and not (st_h & 1).any() and ortho < site_tol
               and same is not False)
     return {"ok": ok, "n_checked": int(n_chk), "modes": [int(m_begin), int(m_end)], "max_abs_dp": float(d.max()),
-            "max_rel_dp": rel, "tolerance": tol, "rel_floor": 1e-12, "n_marginals_above_floor": int(big.sum()),
+            "max_rel_dp": rel, "tolerance": tol, "rel_tolerance": rel_tol, "rel_floor": rel_floor, "n_marginals_above_floor": int(big.sum()),
             "counts_mismatch_unflagged": int(mism.sum()), "n_flagged": int(flagged.sum()),
             "same_as_timed_run": same, "site_orthonormality_max": ortho,
             "gemm_mode": gemm_mode, "oracle": "oracle.sample_chain teacher-forced along the GPU path + free run",
@@ -627,7 +643,8 @@ def run_stage(args, local, W, K, config, dims):
     parity = parity_spot_check(eng, mps, mb, min(mb + 2, me), W * n, n_chk, stream.cuda_stream, sigma,
                                state_in=x[W][:n_chk].contiguous() if mb > 0 else None,
                                ref_counts=counts[W][:n_chk].cpu().numpy(), gemm_mode=args.gemm,
-                               tol=parity_tol(args))
+                               tol=parity_tol(args), rel_floor=parity_rel_floor(args),
+                               rel_tol=parity_rel_tol(args))
     ok = ok and parity["ok"]
     cfg = dict(config, layout=f"one stage of a {G}-stage mode pipeline, measured alone on one B200",
                l2="inputs larger than L2 (stage sites %.1f GB streamed per step)" % (block_bytes / 1e9),
@@ -924,7 +941,8 @@ def main():
         parity = parity_spot_check(eng, mps, 0, M, block_index(W), n_chk, stream.cuda_stream, sigma,
                                    uniforms=u_dev[W][:n_chk], alpha=a_dev[W][:n_chk],
                                    ref_counts=counts[W][:n_chk].cpu().numpy(), gemm_mode=args.gemm,
-                                   tol=parity_tol(args))
+                                   tol=parity_tol(args), rel_floor=parity_rel_floor(args),
+                                   rel_tol=parity_rel_tol(args))
         ok = ok and parity["ok"]
 
     # Same run, same inputs, K1 emulated on the INT8 tensor cores (gemm mode 8, Ozaki, ~1e-13):
