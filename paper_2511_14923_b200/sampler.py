@@ -293,11 +293,13 @@ class MpsSampler:
         uniforms (N x M) host arrays are indexed by global sample index - start."""
         torch = self._torch
         stop = config.N if stop is None else stop
+        if start < 0 or stop < start:
+            raise ValidationError(f"sample range [{start}, {stop}) invalid")
         n_all = stop - start
         M, D = self.M, self.D
         dev = torch.device("cuda", self.device)
-        counts = torch.empty((max(n_all, 0), M), dtype=torch.int32, device=dev)
-        status = torch.zeros(max(n_all, 0), dtype=torch.uint8, device=dev)
+        counts = torch.empty((n_all, M), dtype=torch.int32, device=dev)
+        status = torch.zeros(n_all, dtype=torch.uint8, device=dev)
         marg = torch.empty((n_all, M, D), dtype=torch.float64, device=dev) if return_marginals else None
         self.set_streams(config.seed, config.alpha_sigma)
         B = config.batch_size or DEFAULT_BATCH
