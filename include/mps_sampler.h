@@ -44,8 +44,9 @@
  *     results are on the host.
  *   * The caller owns every buffer; the library borrows pointers for the
  *     call only (sites: see MPS_SITE_*).
- *   * Calls on one context are serialised by the caller; distinct contexts
- *     are independent.  ctypes releases the GIL around every call.
+ *   * Calls on one context are serialised by the library (a per-context lock
+ *     held while a call validates, stages and enqueues its work); distinct
+ *     contexts are independent.  ctypes releases the GIL around every call.
  */
 #ifndef MPS_SAMPLER_H
 #define MPS_SAMPLER_H

@@ -188,6 +188,7 @@ struct DevBuf {
 }  // namespace
 
 struct mps_ctx {
+  std::recursive_mutex mu;  // calls on one context are serialised (SURVEY.md §8b threading contract)
   int device = 0;
   int layout = 0;
   int M = 0, D = 0;
@@ -944,6 +945,7 @@ int mps_create(int n_dev, const int* dev_ids, int layout, mps_ctx** out) {
 
 int mps_configure(mps_ctx* c, int M, int D) {
   if (!c) return MPS_ERR_VALIDATION;
+  std::lock_guard<std::recursive_mutex> lk_(c->mu);
   if (M < 1) return fail(c, MPS_ERR_VALIDATION, "M must be >= 1, got %d", M);
   if (D < 1 || D > DMAX) return fail(c, MPS_ERR_VALIDATION, "D must lie in [1, %d], got %d", DMAX, D);
   cudaSetDevice(c->device);
@@ -958,6 +960,7 @@ int mps_configure(mps_ctx* c, int M, int D) {
 
 int mps_set_site(mps_ctx* c, int m, int chi_l, int chi_r, int D, const void* gamma, int flags, int dtype) {
   if (!c) return MPS_ERR_VALIDATION;
+  std::lock_guard<std::recursive_mutex> lk_(c->mu);
   if (c->M == 0) return fail(c, MPS_ERR_VALIDATION, "mps_configure must precede mps_set_site");
   if (m < 0 || m >= c->M) return fail(c, MPS_ERR_VALIDATION, "site index %d outside [0, %d)", m, c->M);
   if (D != c->D) return fail(c, MPS_ERR_VALIDATION, "site %d: D=%d but the chain has D=%d", m, D, c->D);
@@ -1083,6 +1086,7 @@ int mps_set_site(mps_ctx* c, int m, int chi_l, int chi_r, int D, const void* gam
 
 int mps_set_streams(mps_ctx* c, uint64_t seed, double alpha_sigma) {
   if (!c) return MPS_ERR_VALIDATION;
+  std::lock_guard<std::recursive_mutex> lk_(c->mu);
   if (!(alpha_sigma == alpha_sigma)) return fail(c, MPS_ERR_VALIDATION, "alpha_sigma is NaN");
   // numpy routes a key list holding an int >= 2^63 through float64: the uniform stream keeps that
   // quirk (numpy_key0) but the alpha stream's [seed, 2^62 + i/64] keys would collapse, so refuse
@@ -1646,6 +1650,7 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
                      int64_t ld_u, const void* disp, const void* alpha, const void* state_in, void* state_out,
                      int32_t* counts, int64_t ld_c, double* marginals, uint8_t* status, uint64_t stream) {
   if (!c) return MPS_ERR_VALIDATION;
+  std::lock_guard<std::recursive_mutex> lk_(c->mu);
   c->err.clear();
   if (c->M == 0) return fail(c, MPS_ERR_VALIDATION, "context not configured");
   if (m_begin < 0 || m_end > c->M || m_begin >= m_end)
@@ -1752,6 +1757,7 @@ int mps_sample_range(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
 int mps_sample(mps_ctx* c, int64_t first_index, int n, const double* uniforms, const void* disp, const void* alpha,
                int32_t* counts, double* marginals, uint64_t* n_flagged) {
   if (!c) return MPS_ERR_VALIDATION;
+  std::lock_guard<std::recursive_mutex> lk_(c->mu);
   if (c->M == 0) return fail(c, MPS_ERR_VALIDATION, "context not configured");
   if (n < 0) return fail(c, MPS_ERR_VALIDATION, "n must be >= 0");
   std::vector<uint8_t> st(n > 0 ? n : 1, 0);
@@ -1768,12 +1774,14 @@ uint64_t mps_kernel_launches(const mps_ctx* c) { return c ? c->launches : 0; }
 
 int mps_profile(mps_ctx* c, int enable) {
   if (!c) return MPS_ERR_VALIDATION;
+  std::lock_guard<std::recursive_mutex> lk_(c->mu);
   c->profile = enable & 3;
   return MPS_OK;
 }
 
 int mps_profile_read(mps_ctx* c, double* out6) {
   if (!c || !out6) return MPS_ERR_VALIDATION;
+  std::lock_guard<std::recursive_mutex> lk_(c->mu);
   double acc[6] = {0, 0, 0, 0, 0, 0};  // gemm: ms, launches, flops; draw: ms, launches, bytes
   for (auto& r : c->recs) {
     cudaEventSynchronize(r.b);
@@ -1984,12 +1992,14 @@ int mps_site_gemm_c64(const void* V, const void* G, void* C, int n, int K, int N
 
 int mps_set_forced(mps_ctx* c, int enable) {
   if (!c) return MPS_ERR_VALIDATION;
+  std::lock_guard<std::recursive_mutex> lk_(c->mu);
   c->forced = enable != 0;
   return MPS_OK;
 }
 
 int mps_set_sum_planes(mps_ctx* c, int enable) {
   if (!c) return MPS_ERR_VALIDATION;
+  std::lock_guard<std::recursive_mutex> lk_(c->mu);
   c->sum_planes = enable != 0;
   c->chain_dirty = true;
   if (!c->sum_planes)
@@ -2003,6 +2013,7 @@ int mps_set_sum_planes(mps_ctx* c, int enable) {
 
 int mps_set_small_chain(mps_ctx* c, int mode) {
   if (!c) return MPS_ERR_VALIDATION;
+  std::lock_guard<std::recursive_mutex> lk_(c->mu);
   if (mode < 0 || mode > 2) return fail(c, MPS_ERR_VALIDATION, "small-chain mode must be 0, 1 or 2, got %d", mode);
   c->small_chain = mode;
   return MPS_OK;
@@ -2026,6 +2037,7 @@ int mps_small_chain_eligible(const mps_ctx* c, int m_begin, int m_end, int n) {
 
 int mps_set_micro_batch(mps_ctx* c, int micro) {
   if (!c) return MPS_ERR_VALIDATION;
+  std::lock_guard<std::recursive_mutex> lk_(c->mu);
   if (micro < 0) return fail(c, MPS_ERR_VALIDATION, "micro-batch size must be >= 0, got %d", micro);
   c->micro = micro;
   return MPS_OK;
@@ -2033,6 +2045,7 @@ int mps_set_micro_batch(mps_ctx* c, int micro) {
 
 int mps_set_lanes(mps_ctx* c, int lanes) {
   if (!c) return MPS_ERR_VALIDATION;
+  std::lock_guard<std::recursive_mutex> lk_(c->mu);
   if (lanes < 1 || lanes > mps_ctx::MAX_LANES)
     return fail(c, MPS_ERR_VALIDATION, "lanes must lie in [1, %d], got %d", mps_ctx::MAX_LANES, lanes);
   c->lanes = lanes;
@@ -2041,6 +2054,7 @@ int mps_set_lanes(mps_ctx* c, int lanes) {
 
 int mps_set_gemm_mode(mps_ctx* c, int mode) {
   if (!c) return MPS_ERR_VALIDATION;
+  std::lock_guard<std::recursive_mutex> lk_(c->mu);
   if (mode != 3 && mode != 4 && mode != 8)
     return fail(c, MPS_ERR_VALIDATION, "gemm mode must be 3 (3M), 4 (4M) or 8 (Ozaki int8), got %d", mode);
   c->gemm_mode = mode;
@@ -2049,6 +2063,7 @@ int mps_set_gemm_mode(mps_ctx* c, int mode) {
 
 int mps_set_ozaki_site_mode(mps_ctx* c, int mode, int block_cols) {
   if (!c) return MPS_ERR_VALIDATION;
+  std::lock_guard<std::recursive_mutex> lk_(c->mu);
   if (mode < 0 || mode > 2) return fail(c, MPS_ERR_VALIDATION, "Ozaki site mode must be 0, 1 or 2, got %d", mode);
   if (block_cols < 0) return fail(c, MPS_ERR_VALIDATION, "block_cols must be >= 0");
   c->oz_site_mode = mode;
@@ -2058,6 +2073,7 @@ int mps_set_ozaki_site_mode(mps_ctx* c, int mode, int block_cols) {
 
 int mps_set_ozaki_digits(mps_ctx* c, int S) {
   if (!c) return MPS_ERR_VALIDATION;
+  std::lock_guard<std::recursive_mutex> lk_(c->mu);
   if (S < 5 || S > OZ_MAX_S) return fail(c, MPS_ERR_VALIDATION, "Ozaki digits must lie in [5, %d], got %d", OZ_MAX_S, S);
   c->oz_S = S;  // the sites' digit planes are re-sliced on the next gemm-mode-8 call
   return MPS_OK;
@@ -2065,6 +2081,7 @@ int mps_set_ozaki_digits(mps_ctx* c, int S) {
 
 int mps_set_gemm_config(mps_ctx* c, int cfg) {
   if (!c) return MPS_ERR_VALIDATION;
+  std::lock_guard<std::recursive_mutex> lk_(c->mu);
   if (cfg < -2 || cfg >= N_GEMM_CFGS) return fail(c, MPS_ERR_VALIDATION, "gemm config %d outside [-2, %d)", cfg,
                                                   N_GEMM_CFGS);
   c->gemm_cfg = cfg;

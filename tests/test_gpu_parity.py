@@ -948,3 +948,39 @@ def test_stage_split_into_host_arrays(c2_sites, chain):
     assert np.array_equal(counts, full["counts"])
     assert np.array_equal(marg, full["marginals"])
     assert np.array_equal(status, full["status"])
+
+
+def test_concurrent_calls_on_one_context(c2_sites):
+    """Threads calling one context at once (ctypes releases the GIL) are serialised by the library's
+    per-context lock: every thread's index window gives the bits of the sequential calls."""
+    import threading
+
+    N, M, D, T = 300, 16, 10, 6
+    with MpsSampler(MPS(c2_sites)) as eng:
+        eng.set_streams(21, 0.5)
+        seq = []
+        for w in range(T):
+            c, mg = np.zeros((N, M), dtype=np.int32), np.zeros((N, M, D))
+            eng.run(w * N, N, c, marginals=mg, status=np.zeros(N, dtype=np.uint8))
+            seq.append((c, mg))
+        par = [(np.zeros((N, M), dtype=np.int32), np.zeros((N, M, D))) for _ in range(T)]
+        errs = []
+
+        def work(w):
+            try:
+                for _ in range(8):
+                    eng.run(w * N, N, par[w][0], marginals=par[w][1], status=np.zeros(N, dtype=np.uint8))
+                    for a, b in zip(seq[w], par[w]):
+                        if not np.array_equal(a, b):
+                            errs.append(f"window {w} differs")
+            except Exception as e:  # pragma: no cover
+                errs.append(e)
+
+        th = [threading.Thread(target=work, args=(w,)) for w in range(T)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+    assert not errs, errs
+    for (c0, m0), (c1, m1) in zip(seq, par):
+        assert np.array_equal(c0, c1) and np.array_equal(m0, m1)
