@@ -831,8 +831,10 @@ def main():
     eng.set_lanes(args.lanes)
     eng.set_gemm_mode({"3m": 3, "4m": 4, "ozaki": 8}[args.gemm])
     eng.set_ozaki_digits(args.oz_digits)
-    small_chain = eng.small_chain_active(n)  # whole chain in one persistent launch (chi <= 128, small n)
-    path = "small_chain_kernel (one launch per step)" if small_chain else "per-mode K1 + K2/K3 kernels"
+    sc_kind = eng.small_chain_kind(n)  # whole chain in one launch: 1 cluster kernel (chi <= 128), 2 tiny (chi <= 32)
+    small_chain = sc_kind != 0
+    path = {0: "per-mode K1 + K2/K3 kernels", 1: "small_chain_kernel (one launch per step)",
+            2: "tiny_chain_kernel (one launch per step)"}[sc_kind]
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t_setup
     stream = torch.cuda.Stream(dev)  # explicit stream: events and kernels share it
@@ -1021,9 +1023,11 @@ def main():
                       "6 on the DMMA pipe, so the executed rate is 0.75 x achieved and frac can exceed 1")
     if small_chain:
         kernel_name = ("small_chain_kernel (whole mode chain in one persistent launch: K1 3M FP64 DMMA + K2/K3 "
-                       "draw, 16-CTA clusters, st.async exchange)")
+                       "draw, 16-CTA clusters, st.async exchange)") if sc_kind == 1 else (
+                       "tiny_chain_kernel (whole mode chain in one launch: one CTA per 8-row group, every site in "
+                       "shared memory, K1 3M FP64 DMMA + K2/K3 draw)")
         bound_note = ("achieved = K1 algorithmic flops over the fused kernel's whole duration (the draw and the "
-                      "cluster exchanges included); " + bound_note)
+                      "exchanges included); " + bound_note)
     if args.dtype == "c64":
         # tcgen05 kind::tf32 executes 3 passes (hi.hi, hi.lo, lo.hi) of the real-doubled
         # product = 24 tensor flops per complex MAC; the roofline is the dense TF32 rate,

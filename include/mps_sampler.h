@@ -175,9 +175,14 @@ int mps_set_micro_batch(mps_ctx* ctx, int micro);
  * return to the host between modes (the two-kernels-per-mode chain is latency-bound there).
  * Results are bit-identical to the per-mode kernels.  mode 0: off; 1: whenever eligible;
  * 2 (default): when its latency model beats the per-mode kernels' for the call's n (one to a few
- * waves of 16-row groups).  MPS_SMALL_CHAIN=0 / =1 set modes 0 / 1 at context creation. */
+ * waves of 16-row groups); 3: as 1 but never the tiny-chain kernel (mps_small_chain_eligible).
+ * MPS_SMALL_CHAIN=0 / =1 / =3 set modes 0 / 1 / 3 at context creation. */
 int mps_set_small_chain(mps_ctx* ctx, int mode);
-/* 1 when mps_sample_range over [m_begin, m_end) with n samples would take the small-chain kernel. */
+/* Which whole-chain kernel mps_sample_range over [m_begin, m_end) with n samples would take:
+ * 0 the per-mode kernels, 1 the 16-CTA cluster kernel, 2 the tiny-chain kernel (one CTA per 8-row
+ * group, every site in shared memory: chi_l, chi_r <= 32, chi_r D <= 256; taken in modes 1 and 2
+ * whenever eligible -- faster than both other paths at any n).  Mode 3 of mps_set_small_chain is
+ * mode 1 without the tiny kernel (A/B and tests).  All paths give the same bits. */
 int mps_small_chain_eligible(const mps_ctx* ctx, int m_begin, int m_end, int n);
 /* Teacher forcing (the oracle's forced=, the pattern of gbsemu's forced path, sampler.py:394-416):
  * when enabled, mps_sample / mps_sample_range read sample b's outcome at mode m from counts

@@ -29,6 +29,7 @@
 #include "site_gemm.cuh"
 #include "chain_small.cuh"
 #include "chain_small2.cuh"
+#include "chain_tiny.cuh"
 
 using namespace mps;
 
@@ -222,7 +223,7 @@ struct mps_ctx {
   bool forced = false;                              // teacher forcing: outcomes read from counts
   // small chains (chi <= 128, chi D <= 1024, 3M): the whole mode loop in one persistent cluster
   // kernel (chain_small.cuh); its per-site tensor maps + bond dims live in chain_meta
-  int small_chain = 2;  // 0 off, 1 always when eligible, 2 auto (when the cost model prefers it)
+  int small_chain = 2;  // 0 off, 1 always when eligible, 2 auto (when the cost model prefers it), 3 = 1 without the tiny kernel
   bool chain_dirty = true;
   DevBuf<uint8_t> chain_meta;
   // host->HBM site streaming: 2-slot ring filled on a copy stream ahead of the GEMMs
@@ -816,6 +817,55 @@ static int small_chain_capacity(int D) {
   return num;
 }
 
+// ---- tiny chains: one CTA per 8-row group, every site in shared memory (chain_tiny.cuh) ----
+static void (*tiny_chain_kernel_for(int D))(ChainArgs) {
+  return D == 4 ? tiny_chain_kernel<4> : D == 10 ? tiny_chain_kernel<10> : tiny_chain_kernel<0>;
+}
+static int tiny_smem(const mps_ctx* c, int m_begin, int m_end) {
+  long long b = TC_OFF_SITES;
+  for (int m = m_begin; m < m_end; ++m) b += tc_site_bytes(c->sites[m].chi_l, c->sites[m].chi_r, c->D);
+  return b + 1024 <= TC_SMEM_MAX ? (int)(b + 1024) : -1;  // + the 1 KB alignment slack
+}
+// Whether the call takes the tiny-chain kernel: small-chain modes 1 / 2 (not 0, not 3), complex128 3M,
+// chi_l <= 32, chi_r <= 32, chi_r D <= 256 at every site, and the range's sites fit in shared memory.
+// It replaces both the cluster kernel and the per-mode kernels for such chains at any n (its CTAs
+// persist over 8-row groups), with the same bits.
+static bool tiny_chain_ok(const mps_ctx* c, int m_begin, int m_end, int n) {
+  if ((c->small_chain != 1 && c->small_chain != 2) || c->dtype != MPS_C128 || c->gemm_mode != 3 || n < 1)
+    return false;
+  if (m_end - m_begin > TC_MMAX || c->D > DMAX) return false;
+  for (int m = m_begin; m < m_end; ++m) {
+    const Site& s = c->sites[m];
+    if (s.host || !s.chain || s.chi_l > TC_KMAX || s.chi_r > TC_RMAX || s.chi_r * c->D > TC_NMAX) return false;
+  }
+  return tiny_smem(c, m_begin, m_end) > 0;
+}
+static cudaError_t launch_tiny_chain(mps_ctx* c, const ChainArgs& P, cudaStream_t st) {
+  void (*kern)(ChainArgs) = tiny_chain_kernel_for(c->D);
+  const int smem = tiny_smem(c, P.m_begin, P.m_end);
+  if (smem < 0) return cudaErrorNotSupported;
+  cudaError_t e = set_smem_once((const void*)kern, TC_SMEM_MAX);
+  if (e != cudaSuccess) return e;
+  static std::map<std::tuple<void*, int, int>, int> occ;  // (kernel, device, smem) -> CTAs per SM
+  static std::mutex mu;
+  int dev = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = occ.find({(void*)kern, dev, smem});
+    if (it != occ.end()) per_sm = it->second;
+  }
+  if (per_sm == 0) {
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TC_THREADS, smem);
+    if (e != cudaSuccess || per_sm < 1) return e != cudaSuccess ? e : cudaErrorNotSupported;
+    std::lock_guard<std::mutex> lk(mu);
+    occ[{(void*)kern, dev, smem}] = per_sm;
+  }
+  const int groups = (P.n + TC_ROWS - 1) / TC_ROWS;
+  kern<<<std::min(groups, per_sm * g_num_sms), TC_THREADS, smem, st>>>(P);
+  return cudaGetLastError();
+}
+
 // Whether a call of n samples over [m_begin, m_end) takes the small-chain kernel.  Auto mode
 // compares two latency models fitted to the C1/C2 sweeps (profiles/r01_small_chain_crossover.txt):
 // the fused kernel costs ~3.5 us + its 16-row K1 slice (~2.4 TFLOP/s per cluster) per mode and per
@@ -823,13 +873,14 @@ static int small_chain_capacity(int D) {
 // Both paths give the same bits, so the choice only moves time.
 static bool small_chain_ok(const mps_ctx* c, int m_begin, int m_end, int n) {
   if (!c->small_chain || c->dtype != MPS_C128 || c->gemm_mode != 3 || n < 1) return false;
+  if (tiny_chain_ok(c, m_begin, m_end, n)) return true;
   for (int m = m_begin; m < m_end; ++m) {
     const Site& s = c->sites[m];
     if (s.host || !s.chain || s.chi_l > SC_KMAX || s.chi_r * c->D > SC_NMAX) return false;
   }
   const int cap = small_chain_capacity(c->D);
   if (cap < 1) return false;
-  if (c->small_chain == 1) return true;
+  if (c->small_chain == 1 || c->small_chain == 3) return true;
   const int waves = ((n + SC_CL - 1) / SC_CL + cap - 1) / cap;
   double t_chain = 0.0, t_mode = 0.0;
   const bool v2 = small_chain_variant() == 2;
@@ -937,7 +988,7 @@ int mps_create(int n_dev, const int* dev_ids, int layout, mps_ctx** out) {
     const char* e = getenv("MPS_DRAW_RING");
     if (e && e[0] == '0') c->draw_ring = false;
     e = getenv("MPS_SMALL_CHAIN");
-    if (e && (e[0] == '0' || e[0] == '1')) c->small_chain = e[0] - '0';
+    if (e && (e[0] == '0' || e[0] == '1' || e[0] == '3')) c->small_chain = e[0] - '0';
   }
   *out = c;
   return MPS_OK;
@@ -1230,7 +1281,7 @@ static int run_chain(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
       rg.b = c->get_event();
       cudaEventRecord(rg.a, st);
     }
-    const cudaError_t le = launch_small_chain(c, P, st);
+    const cudaError_t le = tiny_chain_ok(c, m_begin, m_end, n) ? launch_tiny_chain(c, P, st) : launch_small_chain(c, P, st);
     if (le != cudaSuccess) {
       // the launch did not happen (no co-resident 16-CTA cluster fits right now: other kernels or
       // MPS clients hold the SMs, cudaErrorClusterOutOfResources / NotSupported ...): the per-mode
@@ -2014,11 +2065,16 @@ int mps_set_sum_planes(mps_ctx* c, int enable) {
 int mps_set_small_chain(mps_ctx* c, int mode) {
   if (!c) return MPS_ERR_VALIDATION;
   std::lock_guard<std::recursive_mutex> lk_(c->mu);
-  if (mode < 0 || mode > 2) return fail(c, MPS_ERR_VALIDATION, "small-chain mode must be 0, 1 or 2, got %d", mode);
+  if (mode < 0 || mode > 3) return fail(c, MPS_ERR_VALIDATION, "small-chain mode must be 0, 1, 2 or 3, got %d", mode);
   c->small_chain = mode;
   return MPS_OK;
 }
 
+#ifdef TC_TRACE
+int mps_debug_tiny_trace(long long* out) {
+  return cudaMemcpyFromSymbol(out, tc_trace, sizeof(tc_trace)) == cudaSuccess ? MPS_OK : MPS_ERR_GENERIC;
+}
+#endif
 #ifdef SC_TRACE
 int mps_debug_chain_trace(long long* out) {
   return cudaMemcpyFromSymbol(out, sc_trace, sizeof(sc_trace)) == cudaSuccess ? MPS_OK : MPS_ERR_GENERIC;
@@ -2032,7 +2088,7 @@ int mps_small_chain_eligible(const mps_ctx* c, int m_begin, int m_end, int n) {
   if (!c || m_begin < 0 || m_end > c->M || m_begin >= m_end) return 0;
   for (int m = m_begin; m < m_end; ++m)
     if (!c->sites[m].loaded) return 0;
-  return small_chain_ok(c, m_begin, m_end, n) ? 1 : 0;
+  return !small_chain_ok(c, m_begin, m_end, n) ? 0 : tiny_chain_ok(c, m_begin, m_end, n) ? 2 : 1;
 }
 
 int mps_set_micro_batch(mps_ctx* c, int micro) {

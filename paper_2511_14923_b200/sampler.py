@@ -233,13 +233,17 @@ class MpsSampler:
         _native.check(self.L.mps_set_lanes(self.ctx, int(lanes)), self.ctx)
 
     def set_small_chain(self, mode):
-        """Whole-chain persistent cluster kernel for small chains (mps_set_small_chain): False / 0
-        off, True / 1 whenever eligible, 2 automatic (default).  Results are bit-identical."""
+        """Whole-chain kernels for small chains (mps_set_small_chain): False / 0 off, True / 1 whenever
+        eligible, 2 automatic (default), 3 as 1 without the tiny-chain kernel.  Results are bit-identical."""
         _native.check(self.L.mps_set_small_chain(self.ctx, int(mode)), self.ctx)
 
     def small_chain_active(self, n: int) -> bool:
-        """Whether a call of n samples over this context's sites runs the small-chain kernel."""
-        return bool(self.L.mps_small_chain_eligible(self.ctx, *self.sites_range, int(n)))
+        """Whether a call of n samples over this context's sites runs a whole-chain kernel."""
+        return self.small_chain_kind(n) != 0
+
+    def small_chain_kind(self, n: int) -> int:
+        """0 per-mode kernels, 1 the 16-CTA cluster kernel, 2 the tiny-chain kernel (mps_small_chain_eligible)."""
+        return int(self.L.mps_small_chain_eligible(self.ctx, *self.sites_range, int(n)))
 
     def set_ozaki_digits(self, S: int):
         """Digits per operand of gemm mode 8 (mps_set_ozaki_digits): 7 (default), 6 or 5."""

@@ -153,8 +153,9 @@ def test_small_chain_state_out_stays_in_bounds(c2_sites, n):
 
 
 def test_small_chain_auto_choice(c2_sites, c1_sites):
-    """Automatic mode takes the fused kernel for one wave of 16-row groups and the per-mode kernels
-    once the batch is large enough for them to win (both give the same bits)."""
+    """Automatic mode takes the cluster kernel for one wave of 16-row groups and the per-mode kernels
+    once the batch is large enough for them to win, and the tiny-chain kernel for chi <= 32 at any n
+    (all give the same bits)."""
     with MpsSampler(MPS(c2_sites)) as eng:
         assert eng.small_chain_active(100)
         assert not eng.small_chain_active(1024)
@@ -162,5 +163,9 @@ def test_small_chain_auto_choice(c2_sites, c1_sites):
         assert eng.small_chain_active(1024)
         eng.set_small_chain(False)
         assert not eng.small_chain_active(100)
-    with MpsSampler(MPS(c1_sites)) as eng:
-        assert eng.small_chain_active(300) and not eng.small_chain_active(4096)
+    with MpsSampler(MPS(c1_sites)) as eng:  # chi <= 32: the tiny-chain kernel, at any n
+        assert eng.small_chain_kind(300) == 2 and eng.small_chain_kind(100_000) == 2
+        eng.set_small_chain(3)  # without it: the cluster kernel whenever eligible
+        assert eng.small_chain_kind(300) == 1 and eng.small_chain_kind(4096) == 1
+        eng.set_small_chain(False)
+        assert eng.small_chain_kind(300) == 0
