@@ -72,6 +72,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tiny_chain_kernel(const __grid_
   double2* Tw = reinterpret_cast<double2*>(smem + TC_OFF_T) + warp * DMAX * DMAX;  // Q modes' D(alpha)
   const int Q = min(32, (DMAX * DMAX) / (D * D));  // modes per chunk of this warp's D(alpha) buffer
 
+  // PDL: the next call's kernel may launch onto free SMs and stage its sites while this one runs
+  griddep_launch_dependents();
   if (tid == 0) {
     int off = 0;
     for (int q = 0; q < nmodes; ++q) {
@@ -88,6 +90,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tiny_chain_kernel(const __grid_
       bulk_load_1d(smem + TC_OFF_SITES + soff[q], P.sites[m], bytes, &sbar[q]);
     }
   }
+  // the sites and their metadata were written by synchronous uploads (mps_set_site); everything else
+  // (inputs, status, state_in, outputs) may belong to the previous kernel in the stream
+  griddep_wait();
   __syncthreads();
 
   for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {

@@ -862,8 +862,7 @@ static cudaError_t launch_tiny_chain(mps_ctx* c, const ChainArgs& P, cudaStream_
     occ[{(void*)kern, dev, smem}] = per_sm;
   }
   const int groups = (P.n + TC_ROWS - 1) / TC_ROWS;
-  kern<<<std::min(groups, per_sm * g_num_sms), TC_THREADS, smem, st>>>(P);
-  return cudaGetLastError();
+  return launch_pdl(kern, dim3(std::min(groups, per_sm * g_num_sms)), dim3(TC_THREADS), (size_t)smem, st, P);
 }
 
 // Whether a call of n samples over [m_begin, m_end) takes the small-chain kernel.  Auto mode
@@ -1568,12 +1567,17 @@ static int run_chain(mps_ctx* c, int m_begin, int m_end, int64_t first_index, in
   return MPS_OK;
 }
 
-// One call over n samples with host arrays, as micro-batches of c->micro rows: micro-batch t's inputs
-// go up on cs_in while t-1 computes on st, its outputs come down on cs_out while t+1 computes.  Host
+// One call over n samples with host arrays, as micro-batches of c->micro rows.  Micro-batches are
+// grouped into chunks of G (about 2 MB of inputs, at most 64 micro-batches): chunk k's inputs go up on
+// cs_in in one copy per field while chunk k-1 computes on st, its outputs come down on cs_out while
+// chunk k+1 computes.  Inside a chunk the micro-batches' kernels follow each other on st with nothing
+// in between, so programmatic dependent launch overlaps each kernel's prologue with its
+// predecessor's tail (an event wait or a copy between two kernels would serialise them).  Host
 // arrays that are pinned are copied directly; pageable ones are packed into (inputs) / unpacked from
-// (outputs) the context's pinned staging for the whole call.  Device input/output slots are
-// double-buffered: the H2D of t waits for the compute of t-2.  One host synchronisation per call.
-// Results are bit-identical to the single-shot path (per-sample results do not depend on the split).
+// (outputs) the context's pinned staging for the whole call.  Device slots are double-buffered per
+// chunk: the H2D of chunk k waits for the compute and the D2H of chunk k-2.  One host
+// synchronisation per call.  Results are bit-identical to the single-shot path (per-sample results
+// do not depend on the split).
 static bool is_pinned_host(const void* p) {
   cudaPointerAttributes at;
   if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
@@ -1606,6 +1610,12 @@ static int sample_pipelined(mps_ctx* c, int m_begin, int m_end, int64_t first_in
                           (size_t)ld_c * D * 8, 1};
   bool host[6];
   for (int i = 0; i < 6; ++i) host[i] = dptr[i] && !is_device_ptr(dptr[i]);
+  size_t in_row = 0;  // host input bytes per sample row
+  for (int i = 0; i < 6; ++i) in_row += host[i] ? rows[i] : 0;
+  const int T = (n + nb - 1) / nb;
+  const int G = (int)std::max<size_t>(1, std::min<size_t>({(size_t)64, (size_t)T,
+                                                              ((size_t)2 << 20) / std::max<size_t>(1, (size_t)nb * in_row)}));
+  const size_t slot_rows = (size_t)G * nb;
   size_t stage_bytes = 0, slot_bytes = 0;
   for (int i = 0; i < 6; ++i) {
     Field& x = f[i];
@@ -1618,7 +1628,7 @@ static int sample_pipelined(mps_ctx* c, int m_begin, int m_end, int64_t first_in
     x.stage_off = stage_bytes;
     if (host[i] && !x.pinned) stage_bytes += ((size_t)n * x.row + 255) & ~(size_t)255;
     x.slot_off = slot_bytes;
-    if (host[i] || (i == 5 && !status)) slot_bytes += ((size_t)nb * x.row + 255) & ~(size_t)255;
+    if (host[i] || (i == 5 && !status)) slot_bytes += (slot_rows * x.row + 255) & ~(size_t)255;
   }
   CU(c, c->pipe_d.ensure(2 * slot_bytes), "alloc micro-batch slots");
   if (stage_bytes > c->io_h_cap) {
@@ -1636,57 +1646,64 @@ static int sample_pipelined(mps_ctx* c, int m_begin, int m_end, int64_t first_in
   auto hdst = [&](int i, size_t r0) -> uint8_t* {
     return (f[i].pinned ? f[i].hout : c->io_h + f[i].stage_off) + r0 * f[i].row;
   };
+  auto drain = [&]() {  // queued copies still use the caller's arrays and the staging buffer
+    cudaStreamSynchronize(c->cs_in);
+    cudaStreamSynchronize(c->cs_out);
+    cudaStreamSynchronize(st);
+  };
   // the copy streams start after everything already queued on st (the caller's prior work)
   CU(c, cudaEventRecord(c->fork_ev, st), "fork");
   CU(c, cudaStreamWaitEvent(c->cs_in, c->fork_ev, 0), "fork wait");
   CU(c, cudaStreamWaitEvent(c->cs_out, c->fork_ev, 0), "fork wait");
-  const int T = (n + nb - 1) / nb;
-  for (int t = 0; t < T; ++t) {
-    const int w = t & 1;
-    const size_t r0 = (size_t)t * nb;
-    const int nt = std::min(nb, n - (int)r0);
+  const int NC = (T + G - 1) / G;
+  for (int k = 0; k < NC; ++k) {
+    const int w = k & 1;
+    const size_t r0 = (size_t)k * slot_rows;
+    const int nr = (int)std::min<size_t>(slot_rows, (size_t)n - r0);  // rows of this chunk
     uint8_t* slot = c->pipe_d.p + (size_t)w * slot_bytes;
-    if (t >= 2) {  // slot w: micro-batch t-2's kernels AND the D2H of its in-out fields are done
+    if (k >= 2) {  // slot w: chunk k-2's kernels AND the D2H of its in-out fields are done
       CU(c, cudaStreamWaitEvent(c->cs_in, c->pe_comp[w], 0), "slot free");
       CU(c, cudaStreamWaitEvent(c->cs_in, c->pe_d2h[w], 0), "slot read back");
     }
     for (int i = 0; i < 6; ++i)
       if (f[i].in)
-        CU(c, cudaMemcpyAsync(slot + f[i].slot_off, hsrc(i, r0), (size_t)nt * f[i].row, cudaMemcpyHostToDevice,
-                              c->cs_in), "H2D micro-batch");
+        CU(c, cudaMemcpyAsync(slot + f[i].slot_off, hsrc(i, r0), (size_t)nr * f[i].row, cudaMemcpyHostToDevice,
+                              c->cs_in), "H2D chunk");
     CU(c, cudaEventRecord(c->pe_in[w], c->cs_in), "inputs ready");
     CU(c, cudaStreamWaitEvent(st, c->pe_in[w], 0), "inputs wait");
-    ChainIO io;
-    io.u = !uniforms ? nullptr : host[0] ? (const double*)(slot + f[0].slot_off) : uniforms + r0 * ld_u;
-    io.ld_u = ld_u;
-    io.alpha = !alpha ? nullptr : host[1] ? (const double2*)(slot + f[1].slot_off) : (const double2*)alpha + r0 * M;
-    io.disp = !disp ? nullptr : host[2] ? (const double2*)(slot + f[2].slot_off)
-                                         : (const double2*)disp + r0 * M * D * D;
-    io.counts = host[3] ? (int32_t*)(slot + f[3].slot_off) : counts + r0 * ld_c;
-    io.ld_c = ld_c;
-    io.marg = !marginals ? nullptr : host[4] ? (double*)(slot + f[4].slot_off) : marginals + r0 * ld_c * D;
-    io.status = (!status || host[5]) ? slot + f[5].slot_off : status + r0;
-    if (!status) CU(c, cudaMemsetAsync(io.status, 0, nt, st), "zero status");
-    const void* sin = state_in ? (const double2*)state_in + r0 * chi0 : nullptr;
-    void* sout = state_out ? (void*)((double2*)state_out + r0 * chiM) : nullptr;
-    if (c->dtype == MPS_C64) {
-      sin = state_in ? (const void*)((const float2*)state_in + r0 * chi0) : nullptr;
-      sout = state_out ? (void*)((float2*)state_out + r0 * chiM) : nullptr;
-    }
-    if (int rc = run_chain(c, m_begin, m_end, first_index + (int64_t)r0, nt, io, sin, sout, st)) {
-      // copies already queued still read / write the caller's pinned arrays and the staging buffer:
-      // drain them before handing the buffers back
-      cudaStreamSynchronize(c->cs_in);
-      cudaStreamSynchronize(c->cs_out);
-      cudaStreamSynchronize(st);
-      return rc;
+    if (!status) CU(c, cudaMemsetAsync(slot + f[5].slot_off, 0, nr, st), "zero status");
+    for (int r = 0; r < nr; r += nb) {  // the chunk's micro-batches, back to back on st
+      const int nt = std::min(nb, nr - r);
+      const size_t g0 = r0 + r;  // global row of this micro-batch
+      ChainIO io;
+      io.u = !uniforms ? nullptr : host[0] ? (const double*)(slot + f[0].slot_off) + (size_t)r * ld_u : uniforms + g0 * ld_u;
+      io.ld_u = ld_u;
+      io.alpha = !alpha ? nullptr : host[1] ? (const double2*)(slot + f[1].slot_off) + (size_t)r * M
+                                            : (const double2*)alpha + g0 * M;
+      io.disp = !disp ? nullptr : host[2] ? (const double2*)(slot + f[2].slot_off) + (size_t)r * M * D * D
+                                          : (const double2*)disp + g0 * M * D * D;
+      io.counts = host[3] ? (int32_t*)(slot + f[3].slot_off) + (size_t)r * ld_c : counts + g0 * ld_c;
+      io.ld_c = ld_c;
+      io.marg = !marginals ? nullptr : host[4] ? (double*)(slot + f[4].slot_off) + (size_t)r * ld_c * D
+                                               : marginals + g0 * ld_c * D;
+      io.status = (!status || host[5]) ? slot + f[5].slot_off + r : status + g0;
+      const void* sin = state_in ? (const void*)((const double2*)state_in + g0 * chi0) : nullptr;
+      void* sout = state_out ? (void*)((double2*)state_out + g0 * chiM) : nullptr;
+      if (c->dtype == MPS_C64) {
+        sin = state_in ? (const void*)((const float2*)state_in + g0 * chi0) : nullptr;
+        sout = state_out ? (void*)((float2*)state_out + g0 * chiM) : nullptr;
+      }
+      if (int rc = run_chain(c, m_begin, m_end, first_index + (int64_t)g0, nt, io, sin, sout, st)) {
+        drain();
+        return rc;
+      }
     }
     CU(c, cudaEventRecord(c->pe_comp[w], st), "compute done");
     CU(c, cudaStreamWaitEvent(c->cs_out, c->pe_comp[w], 0), "outputs wait");
     for (int i = 3; i < 6; ++i)
       if (f[i].out)
-        CU(c, cudaMemcpyAsync(hdst(i, r0), slot + f[i].slot_off, (size_t)nt * f[i].row, cudaMemcpyDeviceToHost,
-                              c->cs_out), "D2H micro-batch");
+        CU(c, cudaMemcpyAsync(hdst(i, r0), slot + f[i].slot_off, (size_t)nr * f[i].row, cudaMemcpyDeviceToHost,
+                              c->cs_out), "D2H chunk");
     CU(c, cudaEventRecord(c->pe_d2h[w], c->cs_out), "outputs read");
   }
   CU(c, cudaEventRecord(c->pe_out, c->cs_out), "outputs done");
