@@ -156,6 +156,10 @@ __global__ void __launch_bounds__(SC_THREADS, 1) small_chain_kernel(const __grid
   }
   __syncthreads();
   sc_cluster_sync();  // peers' barriers initialised (and step 0 expected) before any st.async lands
+  // PDL: the Gamma ring (sites uploaded synchronously) may run ahead; every other warp reads inputs or
+  // writes outputs that may belong to the previous kernel in the stream
+  griddep_launch_dependents();
+  if (warp != SC_COMPUTE / 32) griddep_wait();
 
   if (warp == SC_COMPUTE / 32) {
     // ===================== ring producer: Gamma stages of every step, in order =====================

@@ -89,6 +89,10 @@ __global__ void __launch_bounds__(SC2_THREADS, 1) small_chain2_kernel(const __gr
   }
   __syncthreads();
   sc_cluster_sync();  // peers' barriers initialised (and step 0 expected) before any st.async lands
+  // PDL: the Gamma ring (sites uploaded synchronously) may run ahead; every other warp reads inputs or
+  // writes outputs that may belong to the previous kernel in the stream
+  griddep_launch_dependents();
+  if (warp != SC2_W_PROD) griddep_wait();
 
   if (warp == SC2_W_PROD) {
     // ============ ring producer: Gamma stages of every step, once per half, in order ============

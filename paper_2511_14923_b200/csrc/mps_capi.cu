@@ -927,13 +927,15 @@ static cudaError_t launch_small_chain(mps_ctx* c, const ChainArgs& P, cudaStream
   cfg.blockDim = dim3(sc_threads());
   cfg.dynamicSmemBytes = sc_smem();
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = SC_CL;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // the kernels call griddepcontrol.wait
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = (pdl_enabled() && !t_no_pdl) ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, kern, P);
 }
 
