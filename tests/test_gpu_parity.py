@@ -234,13 +234,14 @@ def test_every_gemm_config_first_call_equals_repeat(c2_sites):
 def test_micro_batched_call_bit_identical(c2_sites, pinned):
     """mps_set_micro_batch: one call over N samples with host arrays runs as overlapped micro-batches;
     counts, status and marginals equal the single-shot call's bit for bit (pinned and pageable host
-    arrays, a ragged last micro-batch)."""
+    arrays, a ragged last micro-batch; micro-batches of 3 and 7 make several chunks of <= 64
+    micro-batches with a ragged last chunk)."""
     N, M, D = 1037, 16, 10
     u, al = stream_uniforms(3, 40, N, M), alpha_stream(3, 40, N, M, 0.5)
     mk = (lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()) if pinned else np.ascontiguousarray
     outs = []
     with MpsSampler(MPS(c2_sites)) as eng:
-        for micro in (0, 100, 256):
+        for micro in (0, 3, 7, 100, 256):
             eng.set_micro_batch(micro)
             c = mk(np.zeros((N, M), dtype=np.int32))
             st = mk(np.zeros(N, dtype=np.uint8))

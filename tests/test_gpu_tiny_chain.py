@@ -153,3 +153,26 @@ def test_tiny_chain_not_taken_past_its_bounds():
     with MpsSampler(MPS(orc.random_mps(6, 16, 4, seed=1))) as eng:
         eng.set_gemm_mode(4)
         assert eng.small_chain_kind(100) == 0
+
+
+def test_tiny_chain_micro_batched_chunks(c1_sites):
+    """C1 through one micro-batched call (chunks of micro-batches run back to back under PDL):
+    the same bits as one call per micro-batch."""
+    N, M, D, nb = 2003, 8, 4, 100
+    u, al = stream_uniforms(6, 0, N, M), alpha_stream(6, 0, N, M, 0.25)
+    outs = []
+    with MpsSampler(MPS(c1_sites)) as eng:
+        for micro in (0, nb):
+            eng.set_micro_batch(micro)
+            c = np.zeros((N, M), dtype=np.int32)
+            st = np.zeros(N, dtype=np.uint8)
+            mg = np.zeros((N, M, D))
+            if micro == 0:
+                for s0 in range(0, N, nb):
+                    b = min(nb, N - s0)
+                    eng.run(s0, b, c[s0:s0 + b], uniforms=u[s0:s0 + b], alpha=al[s0:s0 + b], status=st[s0:s0 + b],
+                            marginals=mg[s0:s0 + b])
+            else:
+                eng.run(0, N, c, uniforms=u, alpha=al, status=st, marginals=mg)
+            outs.append((c, st, mg))
+    assert all(np.array_equal(a, b) for a, b in zip(*outs))
