@@ -521,6 +521,7 @@ def run_pipelined(args, rank, world, local, W, K, config, dims):
         "e2e": {"value": K * n / (ms_e2e / 1e3), "unit": "samples/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": n * M * 4},
         "gpu_launches": int(launches),
+        "value_l2_warm": None if ms_warm is None else world * K * n / (ms_warm / 1e3),
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak if peak else None, "traffic": None,
                      "kernel": "site_gemm3m_kernel (K1, FP64 DMMA, 3M), rank 0's stage", "peak_source": peak_src,
@@ -685,6 +686,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--lanes", type=int, default=0,
                     help="concurrent row-block chains per micro-batch (default: 2 for the DMMA K1, 1 for INT8)")
+    ap.add_argument("--l2", default="auto", choices=["auto", "replicas", "flush", "warm"],
+                    help="keeping the timed steps honest about L2 (126 MB): 'auto' = the sites already exceed "
+                         "L2 (C3-C5), else R replicas of the sites cycled per step when R <= 16 suffice (C2), "
+                         "else an L2 flush between steps timed out with per-step events (C1); 'warm' = "
+                         "back-to-back steps with the sites L2-resident (reported as value_l2_warm anyway)")
     ap.add_argument("--stream-sites", action="store_true",
                     help="keep the sites in pinned host memory and stream them into HBM every step")
     ap.add_argument("--gemm", default="3m", choices=["3m", "4m", "ozaki"],
@@ -739,6 +745,25 @@ def main():
               "layout": "sample-sharded" if world > 1 else "single GPU",
               "l2": "inputs larger than L2 (sites %.2f GB streamed per step)" % (
                   sum(a * b for a, b in zip(dims[:-1], dims[1:])) * D * 16 / 1e9)}
+    L2_BYTES = 126e6
+    site_bytes = sum(a * b for a, b in zip(dims[:-1], dims[1:])) * D * (8 if args.dtype == "c64" else 16)
+    l2_mode, n_rep = args.l2, 1
+    if l2_mode == "auto":
+        if site_bytes >= L2_BYTES or args.stream_sites:
+            l2_mode = "large"
+        else:
+            n_rep = int(np.ceil(1.25 * L2_BYTES / site_bytes))
+            l2_mode = "replicas" if n_rep <= 16 else "flush"
+    if l2_mode == "replicas":
+        n_rep = max(2, int(np.ceil(1.25 * L2_BYTES / site_bytes)))
+    if l2_mode == "replicas":
+        config["l2"] = ("inputs larger than L2: %d device copies of the sites (%.1f MB each, %.0f MB in all) used in "
+                        "turn, one per step" % (n_rep, site_bytes / 1e6, n_rep * site_bytes / 1e6))
+    elif l2_mode == "flush":
+        config["l2"] = ("L2 flushed between timed steps (a 512 MB write on the stream); each step timed by its own "
+                        "CUDA events, the flushes excluded (sites %.2f MB)" % (site_bytes / 1e6))
+    elif l2_mode == "warm":
+        config["l2"] = "sites L2-resident across back-to-back steps (%.2f MB; --l2 warm)" % (site_bytes / 1e6)
 
     if args.impl == "reference":
         # The reference ships no MPS sampler; its arm is the CPU oracle restating
@@ -850,33 +875,68 @@ def main():
     counts = torch.empty((nsteps, n, M), dtype=torch.int32, device=dev)
     status = torch.zeros((nsteps, n), dtype=torch.uint8, device=dev)
 
-    def step(s):
-        eng.run(block_index(s), n, counts[s], uniforms=u_dev[s], alpha=a_dev[s], status=status[s],
-                stream=stream.cuda_stream)
+    def step(s, e=None):
+        (e or eng).run(block_index(s), n, counts[s], uniforms=u_dev[s], alpha=a_dev[s], status=status[s],
+                       stream=stream.cuda_stream)
 
     def barrier():
         dist_barrier(local)
         torch.cuda.synchronize()
 
+    # L2 policy of the timed region (--l2): replicas = extra contexts, each with its own device copy
+    # of the sites (and of their chain / sum-plane layouts), used in turn, one per step
+    engs = [eng]
+    if l2_mode == "replicas":
+        for _ in range(n_rep - 1):
+            e = MpsSampler(mps, device=local, borrow=False)
+            e.set_lanes(args.lanes)
+            e.set_gemm_mode({"3m": 3, "4m": 4, "ozaki": 8}[args.gemm])
+            e.set_ozaki_digits(args.oz_digits)
+            engs.append(e)
+    flush_buf = torch.empty(512 << 20, dtype=torch.uint8, device=dev) if l2_mode == "flush" else None
+
     for s in range(W):
-        step(s)
+        for e in engs:
+            step(s, e)
     barrier()
     clocks = Clocks(local)
     clocks.start()
-    l0 = eng.kernel_launches
+    l0 = sum(e.kernel_launches for e in engs)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     if PROFILE_RANGE:  # ncu --profile-from-start off sees exactly the timed steps
         torch.cuda.profiler.start()
-    e0.record(stream)
-    for s in range(W, W + K):
-        step(s)
-    e1.record(stream)
+    if l2_mode == "flush":
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        for i, s in enumerate(range(W, W + K)):
+            flush_buf.fill_(i & 0xFF)
+            evs[i][0].record(stream)
+            step(s)
+            evs[i][1].record(stream)
+    else:
+        e0.record(stream)
+        for s in range(W, W + K):
+            step(s, engs[s % len(engs)])
+        e1.record(stream)
     barrier()
     if PROFILE_RANGE:
         torch.cuda.profiler.stop()
-    launches = eng.kernel_launches - l0
+    launches = sum(e.kernel_launches for e in engs) - l0
     ck = clocks.stop()
+    ms_main = sum(a.elapsed_time(b) for a, b in evs) if l2_mode == "flush" else e0.elapsed_time(e1)
+    ms_warm = None
+    if l2_mode in ("replicas", "flush"):  # the same K steps back to back on one context, sites L2-resident
+        w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        w0.record(stream)
+        for s in range(W, W + K):
+            step(s)
+        w1.record(stream)
+        barrier()
+        ms_warm = dist_max(w0.elapsed_time(w1), dev)
+    for e in engs[1:]:
+        e.close()
+    del flush_buf
     # Instrumented repeat of the same K steps: CUDA events around every K1 launch on its
     # stream (the roofline kernel), then around every K2+K3 launch.  Kept out of the
     # clean timed region because events between launches defeat programmatic
@@ -902,7 +962,7 @@ def main():
     prof.update({k: v for k, v in prof_draw.items() if k.startswith("draw")})
     eng.profile(0)
     eng.set_lanes(args.lanes)
-    ms = dist_max(e0.elapsed_time(e1), dev)
+    ms = dist_max(ms_main, dev)
     value = world * K * n / (ms / 1e3)
 
     # e2e: host (pinned) uniforms + alpha in, counts + status out, through the same C ABI call, every
@@ -1057,8 +1117,11 @@ def main():
                 "d2h_bytes_per_step": n * M * 4 + n,
                 "how": "one C-ABI call over the K steps' K n samples from pinned host arrays, micro-batch n: "
                        "per step an H2D of its uniforms + alpha + status and a D2H of its counts + status, "
-                       "overlapping the neighbouring steps' kernels; one host synchronisation"},
+                       "overlapping the neighbouring steps' kernels; one host synchronisation"
+                       + ("" if l2_mode == "large" else "; one context, so the sites stay L2-resident across "
+                          "the call's micro-batches as in any production call")},
         "gpu_launches": int(launches),
+        "value_l2_warm": None if ms_warm is None else world * K * n / (ms_warm / 1e3),
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_note": traffic_note,
                      "kernel": kernel_name, "note": bound_note,
