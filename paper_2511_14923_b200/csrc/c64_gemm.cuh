@@ -381,6 +381,172 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// CTA-pair variant (tcgen05.mma.cta_group::2): a 2-CTA cluster along M owns a 256 x BN tile.  CTA r
+// loads its 128 A rows and its BN/2 B rows (hi / lo planes) into its own shared memory, both TMA
+// loads completing on the LEADER's stage barrier; the leader's single MMA thread issues
+// M = 256 MMAs that read A and B from both CTAs (each CTA's TMEM receives its 128 rows x BN); the
+// commits multicast "slot free" / "accumulator ready" to both CTAs.  Per SM, a K = 8 step reads
+// 4 KB of A and BN/2 x 32 B of B for 128 x BN x 8 MACs: half the B shared-memory traffic of the
+// single-CTA kernel at the same tile width.  Same k order (stage, k-step, pass) as the other
+// variants.
+// ---------------------------------------------------------------------------------------------
+template <int BN_, int STAGES_>
+struct C64Cg2Cfg {
+  static constexpr int BM = 128, BN = BN_, BK = 32, STAGES = STAGES_;
+  static constexpr int A_BYTES = BM * BK * 4;             // per plane, this CTA's rows
+  static constexpr int B_BYTES = (BN / 2) * BK * 4;       // per plane, this CTA's half of the B rows
+  static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 2 * STAGES * 8 + 5 * 8 + 16;
+  static constexpr int TMEM_COLS = BN;
+  static constexpr int THREADS = 192;
+};
+
+__device__ __forceinline__ void umma_tf32_cg2(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit_cg2(uint64_t* bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::
+                   "r"(smem_u32(bar)),
+               "h"(mask)
+               : "memory");
+}
+// 2-D TMA load into this CTA's shared memory whose completion is signalled on the pair leader's
+// mbarrier (bar_cluster: a shared::cluster address from mapa)
+__device__ __forceinline__ void tma_load_2d_cg2(void* smem_dst, const CUtensorMap* map, int x, int y,
+                                                uint32_t bar_cluster) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar_cluster)
+      : "memory");
+}
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, 1)
+    c64_gemm_cg2_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
+                        const __grid_constant__ CUtensorMap tm_bhi, const __grid_constant__ CUtensorMap tm_blo,
+                        float* __restrict__ C, int n, int N2, int KB, long long ldc) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint64_t* empty = full + Cfg::STAGES;
+  uint64_t* tmem_full = empty + Cfg::STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * Cfg::BM, n0 = blockIdx.y * Cfg::BN;
+  const uint32_t crank = cluster_ctarank();
+
+  griddep_launch_dependents();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < Cfg::STAGES; ++s) {
+      mbar_init(&full[s], 1);   // used on the leader: its arrive.expect_tx + both CTAs' TMA bytes
+      mbar_init(&empty[s], 1);  // the leader's MMA commit, multicast to both CTAs
+    }
+    mbar_init(tmem_full, 1);
+    fence_barrier_init();
+    prefetch_tmap(&tm_ahi);
+    prefetch_tmap(&tm_alo);
+    prefetch_tmap(&tm_bhi);
+    prefetch_tmap(&tm_blo);
+  }
+  if (warp == 1) {  // TMEM allocation for the pair: one warp in each CTA
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"((uint32_t)Cfg::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // both CTAs' barriers and TMEM ready before any cross-CTA signal
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer (both CTAs): my A rows and my half of the B rows ----
+      griddep_wait();
+      uint32_t lead_full;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(lead_full) : "r"(smem_u32(full)));
+      for (int kb = 0; kb < KB; ++kb) {
+        const int s = kb % Cfg::STAGES;
+        mbar_wait(&empty[s], ((kb / Cfg::STAGES) & 1) ^ 1);
+        uint8_t* st = smem + s * Cfg::STAGE_BYTES;
+        if (crank == 0) mbar_arrive_expect_tx(&full[s], 2 * Cfg::STAGE_BYTES);  // both CTAs' bytes
+        const uint32_t fb = lead_full + (uint32_t)(s * 8);
+        const int nb = n0 + (int)crank * (Cfg::BN / 2);
+        tma_load_2d_cg2(st, &tm_ahi, kb * Cfg::BK, m0, fb);
+        tma_load_2d_cg2(st + Cfg::A_BYTES, &tm_alo, kb * Cfg::BK, m0, fb);
+        tma_load_2d_cg2(st + 2 * Cfg::A_BYTES, &tm_bhi, kb * Cfg::BK, nb, fb);
+        tma_load_2d_cg2(st + 2 * Cfg::A_BYTES + Cfg::B_BYTES, &tm_blo, kb * Cfg::BK, nb, fb);
+      }
+    }
+  } else if (warp == 1) {
+    if (crank == 0 && lane == 0) {  // ---- MMA issuer: the leader only, M = 256 over the pair ----
+      constexpr uint32_t idesc = idesc_tf32(2 * Cfg::BM, Cfg::BN);
+      for (int kb = 0; kb < KB; ++kb) {
+        const int s = kb % Cfg::STAGES;
+        mbar_wait(&full[s], (kb / Cfg::STAGES) & 1);
+        tc_fence_after();
+        const uint32_t st = smem_u32(smem + s * Cfg::STAGE_BYTES);
+        const uint32_t ahi = st, alo = st + Cfg::A_BYTES, bhi = st + 2 * Cfg::A_BYTES, blo = bhi + Cfg::B_BYTES;
+#pragma unroll
+        for (int k = 0; k < Cfg::BK / 8; ++k) {
+          const uint32_t off = k * 32;
+          const uint64_t dah = umma_desc_k_sw128(ahi + off), dal = umma_desc_k_sw128(alo + off);
+          const uint64_t dbh = umma_desc_k_sw128(bhi + off), dbl = umma_desc_k_sw128(blo + off);
+          umma_tf32_cg2(tmem, dah, dbh, idesc, (kb | k) != 0);
+          umma_tf32_cg2(tmem, dah, dbl, idesc, 1u);
+          umma_tf32_cg2(tmem, dal, dbh, idesc, 1u);
+        }
+        umma_commit_cg2(&empty[s], 0x3);  // both CTAs' slots are free once these MMAs read them
+      }
+      umma_commit_cg2(tmem_full, 0x3);  // both CTAs' accumulators complete
+    }
+  } else {
+    // ---- epilogue (both CTAs): warps 2..5 drain TMEM lanes 32*(warp%4) .. +31 of this CTA's rows ----
+    mbar_wait(tmem_full, 0);
+    tc_fence_after();
+    const int q = warp & 3;
+    const int row = m0 + 32 * q + lane;
+    float* crow = C + (long long)row * ldc;
+#pragma unroll 1
+    for (int c0 = 0; c0 < Cfg::BN; c0 += 32) {
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(tmem + ((uint32_t)(32 * q) << 16) + c0, r);
+      const int col = n0 + c0;
+      if (row < n) {
+        if (col + 32 <= N2 && (ldc & 3) == 0) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            *reinterpret_cast<float4*>(crow + col + j) = make_float4(
+                __uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+        } else if (col + 32 <= N2) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 2)
+            *reinterpret_cast<float2*>(crow + col + j) = make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1]));
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (col + j < N2) crow[col + j] = __uint_as_float(r[j]);
+        }
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  cluster_sync_all();  // no CTA releases TMEM while the pair's MMAs or its peer's epilogue may run
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)Cfg::TMEM_COLS));
+  }
+}
+
 // Site planes: Gamma (K x N complex64) -> B_r^T hi / lo (2N rows x ld fp32, K-major, zero pad)
 //   row 2c   : (Gr[i][c], -Gi[i][c]) at columns (2i, 2i+1)
 //   row 2c+1 : (Gi[i][c],  Gr[i][c])

@@ -713,20 +713,57 @@ static int c64_kernel_choice() {
   if (v < 0) {
     // default (auto): persistent 128-column tiles when the grid is a few waves (C3: +10%, finer
     // tiles quantise better and the double-buffered accumulator hides the epilogue), 256-column
-    // multicast pairs when it is many (C4: +11% over p128)
+    // multicast pairs when it is many (C4: +11% over p128); cg2 = the cta_group::2 pair kernel (the
+    // default for two or more waves of 256-wide tiles, below)
     const char* e = getenv("MPS_C64_KERNEL");
-    v = !e ? 3 : (strcmp(e, "p256") == 0 ? 1 : strcmp(e, "mc256") == 0 ? 0 : strcmp(e, "p128") == 0 ? 2 : 3);
+    v = !e ? 3
+           : (strcmp(e, "p256") == 0 ? 1 : strcmp(e, "mc256") == 0 ? 0 : strcmp(e, "p128") == 0 ? 2
+              : strcmp(e, "cg2") == 0 ? 4 : 3);
   }
   return v;
+}
+
+// cta_group::2 pairs: 256 x 256 tiles (each CTA 128 rows x 256 columns of TMEM), 3-stage ring
+using C64Cg2 = C64Cg2Cfg<256, 3>;
+static cudaError_t launch_c64_cg2(const float* ahi, const float* alo, const float* bhi, const float* blo, int ld,
+                                  float* C, int n, int K, int N, long long ldc_f, cudaStream_t st) {
+  using Cfg = C64Cg2;
+  if (cudaError_t e = set_smem_once((const void*)c64_gemm_cg2_kernel<Cfg>, Cfg::SMEM_BYTES)) return e;
+  CUtensorMap tah, tal, tbh, tbl;
+  const uint64_t cols = 2 * (uint64_t)K, pitch = 4 * (uint64_t)ld;
+  if (!make_tmap(&tah, ahi, n, cols, pitch, Cfg::BM, 32, true) || !make_tmap(&tal, alo, n, cols, pitch, Cfg::BM, 32, true) ||
+      !make_tmap(&tbh, bhi, 2 * (uint64_t)N, cols, pitch, Cfg::BN / 2, 32, true) ||
+      !make_tmap(&tbl, blo, 2 * (uint64_t)N, cols, pitch, Cfg::BN / 2, 32, true))
+    return cudaErrorInvalidValue;
+  const int KB = (int)((cols + Cfg::BK - 1) / Cfg::BK);
+  const int mtiles = (n + Cfg::BM - 1) / Cfg::BM;
+  dim3 grid((mtiles + 1) & ~1, (2 * N + Cfg::BN - 1) / Cfg::BN);  // pairs along M (a padding CTA stores nothing)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(Cfg::THREADS);
+  cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, c64_gemm_cg2_kernel<Cfg>, tah, tal, tbh, tbl, C, n, 2 * N, KB, ldc_f);
 }
 
 static cudaError_t launch_c64_gemm(const float* ahi, const float* alo, const float* bhi, const float* blo, int ld,
                                    float* C, int n, int K, int N, long long ldc_f, cudaStream_t st) {
   int choice = c64_kernel_choice();
-  if (choice == 3) {  // auto: many 256-wide tiles -> multicast pairs; a few waves -> persistent 128-wide
+  if (choice == 3) {  // auto: two or more waves of 256-wide tiles -> cta_group::2 pairs (C3 -4%, C4 -4%
+                      // vs the next best); fewer -> persistent 128-wide tiles.  All variants give the same bits.
     const long long tiles256 = (long long)((n + 127) / 128) * ((2 * N + 255) / 256);
-    choice = tiles256 >= 8LL * g_num_sms ? 0 : 2;
+    choice = tiles256 >= 2LL * g_num_sms ? 4 : 2;
   }
+  if (choice == 4) return launch_c64_cg2(ahi, alo, bhi, blo, ld, C, n, K, N, ldc_f, st);
   if (choice == 1) return launch_c64_persistent<C64P256>(ahi, alo, bhi, blo, ld, C, n, K, N, ldc_f, st);
   if (choice == 2) return launch_c64_persistent<C64P128>(ahi, alo, bhi, blo, ld, C, n, K, N, ldc_f, st);
   using Cfg = C64Big;
