@@ -608,6 +608,42 @@ def test_site_gemm_c64_tcgen05_vs_fp64(n, K, N):
     assert err <= 2e-5 * scale, (err, scale)
 
 
+_C64_VARIANT_SCRIPT = r"""
+import hashlib, sys, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2511_14923_b200 import _native
+L = _native.lib()
+out = []
+for n, K, N in ((1024, 300, 3000), (300, 64, 700)):
+    g = torch.Generator(device="cuda").manual_seed(n + K)
+    V = torch.randn(n, K, dtype=torch.complex64, device="cuda", generator=g)
+    G = torch.randn(K, N, dtype=torch.complex64, device="cuda", generator=g)
+    C = torch.empty(n, N, dtype=torch.complex64, device="cuda")
+    assert L.mps_site_gemm_c64(V.data_ptr(), G.data_ptr(), C.data_ptr(), n, K, N, 0) == 0
+    torch.cuda.synchronize()
+    out.append(hashlib.sha1(C.cpu().numpy().tobytes()).hexdigest())
+print(" ".join(out))
+"""
+
+
+def test_c64_kernel_variants_bit_identical():
+    """Every complex64 K1 variant (single-CTA persistent 128 / 256, multicast pairs, cta_group::2
+    pairs; MPS_C64_KERNEL is read once per process) gives the same bits: the (stage, k-step, pass)
+    order is shared, so the automatic choice by tile count never makes results depend on n."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sums = {}
+    for v in ("p128", "p256", "mc256", "cg2"):
+        r = subprocess.run([sys.executable, "-c", _C64_VARIANT_SCRIPT, root], capture_output=True, text=True,
+                           timeout=300, env=dict(os.environ, MPS_C64_KERNEL=v))
+        assert r.returncode == 0, r.stderr[-2000:]
+        sums[v] = r.stdout.split()
+    assert len({tuple(x) for x in sums.values()}) == 1, sums
+
+
 C64_TOL = 1e-4  # north star: marginals within 1e-4 in complex64
 # complex64 keeps the state and C in fp32 (24-bit mantissa): where the displacement einsum cancels,
 # a small marginal p carries ~1e-7 / p relative error whatever the arithmetic after the GEMM, so the
