@@ -166,8 +166,10 @@ int mps_set_gemm_config(mps_ctx* ctx, int cfg);
 int mps_set_lanes(mps_ctx* ctx, int lanes);
 /* Micro-batch size for calls with host arrays (0, the default: a call is one micro-batch).  With
  * micro > 0, a mps_sample / mps_sample_range call of n > micro samples runs as micro-batches of
- * `micro` rows whose host<->device copies (copy-engine streams) overlap the neighbouring
- * micro-batches' kernels, with one host synchronisation per call; results are identical. */
+ * `micro` rows, grouped into chunks of about 2 MB of inputs (at most 64 micro-batches): a chunk's
+ * inputs go up in one copy per array on a copy-engine stream while the previous chunk computes,
+ * its kernels run back to back (programmatic dependent launch), its outputs come down while the
+ * next chunk computes; one host synchronisation per call; results are identical. */
 int mps_set_micro_batch(mps_ctx* ctx, int micro);
 /* Small chains (complex128, 3M product mode, every site chi_l <= 128 and chi_r * D <= 1024):
  * run the whole mode range of a call as ONE persistent kernel -- clusters of 16 CTAs each own
