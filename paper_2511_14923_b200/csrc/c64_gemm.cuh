@@ -547,6 +547,163 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   }
 }
 
+// Persistent CTA-pair variant: each 2-CTA cluster walks pair tiles t = pair, pair + npairs, ... (m
+// fastest).  Two TMEM accumulators per CTA (2 x BN = 512 columns): the leader's MMA fills one while
+// both CTAs' epilogue warps drain the other, so a tile's epilogue overlaps the next tile's
+// mainloop; the leader waits for all 8 epilogue warps of the pair (4 local arrivals + 4 remote)
+// before reusing an accumulator.  Same k order, same bits as every other variant.
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, 1)
+    c64_gemm_cg2p_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
+                         const __grid_constant__ CUtensorMap tm_bhi, const __grid_constant__ CUtensorMap tm_blo,
+                         float* __restrict__ C, int n, int N2, int KB, long long ldc) {
+  static_assert(2 * Cfg::BN <= 512, "two accumulators must fit TMEM");
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint64_t* empty = full + Cfg::STAGES;
+  uint64_t* acc_full = empty + Cfg::STAGES;  // [2] both CTAs: the leader's commit, multicast
+  uint64_t* acc_empty = acc_full + 2;        // [2] leader: the pair's 8 epilogue warps
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  constexpr uint32_t TMEM_COLS = 2 * Cfg::BN <= 256 ? 256 : 512;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_ctarank();
+  const int MT2 = (n + 2 * Cfg::BM - 1) / (2 * Cfg::BM);  // pair tiles along M (256 rows each)
+  const int ntiles = MT2 * ((N2 + Cfg::BN - 1) / Cfg::BN);
+  const int pair = (int)blockIdx.x / 2, npairs = (int)gridDim.x / 2;
+  const int my_tiles = pair < ntiles ? (ntiles - pair + npairs - 1) / npairs : 0;
+
+  griddep_launch_dependents();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < Cfg::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&acc_full[a], 1);
+      mbar_init(&acc_empty[a], 8);  // 4 epilogue warps per CTA of the pair
+    }
+    fence_barrier_init();
+    prefetch_tmap(&tm_ahi);
+    prefetch_tmap(&tm_alo);
+    prefetch_tmap(&tm_bhi);
+    prefetch_tmap(&tm_blo);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer (both CTAs) over all (tile, k-block) pairs ----
+      griddep_wait();
+      uint32_t lead_full;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(lead_full) : "r"(smem_u32(full)));
+      int g = 0;
+      for (int q = 0; q < my_tiles; ++q) {
+        const int tile = pair + q * npairs;
+        const int m0 = (tile % MT2) * 2 * Cfg::BM + (int)crank * Cfg::BM, n0 = (tile / MT2) * Cfg::BN;
+        const int nb = n0 + (int)crank * (Cfg::BN / 2);
+        for (int kb = 0; kb < KB; ++kb, ++g) {
+          const int s = g % Cfg::STAGES;
+          mbar_wait(&empty[s], ((g / Cfg::STAGES) & 1) ^ 1);
+          uint8_t* st = smem + s * Cfg::STAGE_BYTES;
+          if (crank == 0) mbar_arrive_expect_tx(&full[s], 2 * Cfg::STAGE_BYTES);
+          const uint32_t fb = lead_full + (uint32_t)(s * 8);
+          tma_load_2d_cg2(st, &tm_ahi, kb * Cfg::BK, m0, fb);
+          tma_load_2d_cg2(st + Cfg::A_BYTES, &tm_alo, kb * Cfg::BK, m0, fb);
+          tma_load_2d_cg2(st + 2 * Cfg::A_BYTES, &tm_bhi, kb * Cfg::BK, nb, fb);
+          tma_load_2d_cg2(st + 2 * Cfg::A_BYTES + Cfg::B_BYTES, &tm_blo, kb * Cfg::BK, nb, fb);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (crank == 0 && lane == 0) {  // ---- MMA issuer: the leader ----
+      constexpr uint32_t idesc = idesc_tf32(2 * Cfg::BM, Cfg::BN);
+      int g = 0;
+      for (int q = 0; q < my_tiles; ++q) {
+        const int a = q & 1;
+        mbar_wait(&acc_empty[a], ((q >> 1) & 1) ^ 1);  // both CTAs have drained this accumulator
+        tc_fence_after();
+        const uint32_t acc = tmem + a * Cfg::BN;
+        for (int kb = 0; kb < KB; ++kb, ++g) {
+          const int s = g % Cfg::STAGES;
+          mbar_wait(&full[s], (g / Cfg::STAGES) & 1);
+          tc_fence_after();
+          const uint32_t st = smem_u32(smem + s * Cfg::STAGE_BYTES);
+          const uint32_t ahi = st, alo = st + Cfg::A_BYTES, bhi = st + 2 * Cfg::A_BYTES, blo = bhi + Cfg::B_BYTES;
+#pragma unroll
+          for (int k = 0; k < Cfg::BK / 8; ++k) {
+            const uint32_t off = k * 32;
+            const uint64_t dah = umma_desc_k_sw128(ahi + off), dal = umma_desc_k_sw128(alo + off);
+            const uint64_t dbh = umma_desc_k_sw128(bhi + off), dbl = umma_desc_k_sw128(blo + off);
+            umma_tf32_cg2(acc, dah, dbh, idesc, (kb | k) != 0);
+            umma_tf32_cg2(acc, dah, dbl, idesc, 1u);
+            umma_tf32_cg2(acc, dal, dbh, idesc, 1u);
+          }
+          umma_commit_cg2(&empty[s], 0x3);
+        }
+        umma_commit_cg2(&acc_full[a], 0x3);
+      }
+    }
+  } else {
+    // ---- epilogue warps 2..5 of both CTAs: drain accumulator q & 1 of this CTA's 128 rows ----
+    const int qw = warp & 3;
+    uint32_t lead_empty;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(lead_empty) : "r"(smem_u32(acc_empty)));
+    for (int q = 0; q < my_tiles; ++q) {
+      const int a = q & 1;
+      const int tile = pair + q * npairs;
+      const int m0 = (tile % MT2) * 2 * Cfg::BM + (int)crank * Cfg::BM, n0 = (tile / MT2) * Cfg::BN;
+      mbar_wait(&acc_full[a], (q >> 1) & 1);
+      tc_fence_after();
+      const int row = m0 + 32 * qw + lane;
+      float* crow = C + (long long)row * ldc;
+#pragma unroll 1
+      for (int c0 = 0; c0 < Cfg::BN; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem + a * Cfg::BN + ((uint32_t)(32 * qw) << 16) + c0, r);
+        const int col = n0 + c0;
+        if (row < n) {
+          if (col + 32 <= N2 && (ldc & 3) == 0) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4)
+              *reinterpret_cast<float4*>(crow + col + j) =
+                  make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                              __uint_as_float(r[j + 3]));
+          } else if (col + 32 <= N2) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 2)
+              *reinterpret_cast<float2*>(crow + col + j) = make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1]));
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (col + j < N2) crow[col + j] = __uint_as_float(r[j]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0)  // this warp is done with accumulator a: tell the leader (local or remote arrive)
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(lead_empty + (uint32_t)(a * 8))
+                     : "memory");
+    }
+  }
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
 // Site planes: Gamma (K x N complex64) -> B_r^T hi / lo (2N rows x ld fp32, K-major, zero pad)
 //   row 2c   : (Gr[i][c], -Gi[i][c]) at columns (2i, 2i+1)
 //   row 2c+1 : (Gi[i][c],  Gr[i][c])

@@ -718,7 +718,7 @@ static int c64_kernel_choice() {
     const char* e = getenv("MPS_C64_KERNEL");
     v = !e ? 3
            : (strcmp(e, "p256") == 0 ? 1 : strcmp(e, "mc256") == 0 ? 0 : strcmp(e, "p128") == 0 ? 2
-              : strcmp(e, "cg2") == 0 ? 4 : 3);
+              : strcmp(e, "cg2") == 0 ? 4 : strcmp(e, "cg2p") == 0 ? 5 : 3);
   }
   return v;
 }
@@ -726,9 +726,11 @@ static int c64_kernel_choice() {
 // cta_group::2 pairs: 256 x 256 tiles (each CTA 128 rows x 256 columns of TMEM), 3-stage ring
 using C64Cg2 = C64Cg2Cfg<256, 3>;
 static cudaError_t launch_c64_cg2(const float* ahi, const float* alo, const float* bhi, const float* blo, int ld,
-                                  float* C, int n, int K, int N, long long ldc_f, cudaStream_t st) {
+                                  float* C, int n, int K, int N, long long ldc_f, cudaStream_t st, bool persistent) {
   using Cfg = C64Cg2;
-  if (cudaError_t e = set_smem_once((const void*)c64_gemm_cg2_kernel<Cfg>, Cfg::SMEM_BYTES)) return e;
+  void (*kern)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, float*, int, int, int, long long) =
+      persistent ? c64_gemm_cg2p_kernel<Cfg> : c64_gemm_cg2_kernel<Cfg>;
+  if (cudaError_t e = set_smem_once((const void*)kern, Cfg::SMEM_BYTES)) return e;
   CUtensorMap tah, tal, tbh, tbl;
   const uint64_t cols = 2 * (uint64_t)K, pitch = 4 * (uint64_t)ld;
   if (!make_tmap(&tah, ahi, n, cols, pitch, Cfg::BM, 32, true) || !make_tmap(&tal, alo, n, cols, pitch, Cfg::BM, 32, true) ||
@@ -737,7 +739,12 @@ static cudaError_t launch_c64_cg2(const float* ahi, const float* alo, const floa
     return cudaErrorInvalidValue;
   const int KB = (int)((cols + Cfg::BK - 1) / Cfg::BK);
   const int mtiles = (n + Cfg::BM - 1) / Cfg::BM;
-  dim3 grid((mtiles + 1) & ~1, (2 * N + Cfg::BN - 1) / Cfg::BN);  // pairs along M (a padding CTA stores nothing)
+  const int ntile = (2 * N + Cfg::BN - 1) / Cfg::BN;
+  dim3 grid((mtiles + 1) & ~1, ntile);  // pairs along M (a padding CTA stores nothing)
+  if (persistent) {  // one pair per two SMs, walking the pair tiles
+    const long long ptiles = (long long)((mtiles + 1) / 2) * ntile;
+    grid = dim3((unsigned)(2 * std::min<long long>(ptiles, g_num_sms / 2)), 1);
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(Cfg::THREADS);
@@ -752,18 +759,20 @@ static cudaError_t launch_c64_cg2(const float* ahi, const float* alo, const floa
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  return cudaLaunchKernelEx(&cfg, c64_gemm_cg2_kernel<Cfg>, tah, tal, tbh, tbl, C, n, 2 * N, KB, ldc_f);
+  return cudaLaunchKernelEx(&cfg, kern, tah, tal, tbh, tbl, C, n, 2 * N, KB, ldc_f);
 }
 
 static cudaError_t launch_c64_gemm(const float* ahi, const float* alo, const float* bhi, const float* blo, int ld,
                                    float* C, int n, int K, int N, long long ldc_f, cudaStream_t st) {
   int choice = c64_kernel_choice();
-  if (choice == 3) {  // auto: two or more waves of 256-wide tiles -> cta_group::2 pairs (C3 -4%, C4 -4%
-                      // vs the next best); fewer -> persistent 128-wide tiles.  All variants give the same bits.
+  if (choice == 3) {  // auto: two to 16 waves of 256-wide tiles -> persistent cta_group::2 pairs (C3 site:
+                      // 0.503 ms vs 0.525 one tile per pair, 0.548 p128); more -> one tile per pair (C4 site:
+                      // 12.4 ms vs 12.6 persistent, 13.0 multicast); fewer -> persistent 128-wide tiles.
+                      // All variants give the same bits.
     const long long tiles256 = (long long)((n + 127) / 128) * ((2 * N + 255) / 256);
-    choice = tiles256 >= 2LL * g_num_sms ? 4 : 2;
+    choice = tiles256 >= 16LL * g_num_sms ? 4 : tiles256 >= 2LL * g_num_sms ? 5 : 2;
   }
-  if (choice == 4) return launch_c64_cg2(ahi, alo, bhi, blo, ld, C, n, K, N, ldc_f, st);
+  if (choice == 4 || choice == 5) return launch_c64_cg2(ahi, alo, bhi, blo, ld, C, n, K, N, ldc_f, st, choice == 5);
   if (choice == 1) return launch_c64_persistent<C64P256>(ahi, alo, bhi, blo, ld, C, n, K, N, ldc_f, st);
   if (choice == 2) return launch_c64_persistent<C64P128>(ahi, alo, bhi, blo, ld, C, n, K, N, ldc_f, st);
   using Cfg = C64Big;

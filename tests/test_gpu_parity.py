@@ -628,7 +628,7 @@ print(" ".join(out))
 
 def test_c64_kernel_variants_bit_identical():
     """Every complex64 K1 variant (single-CTA persistent 128 / 256, multicast pairs, cta_group::2
-    pairs; MPS_C64_KERNEL is read once per process) gives the same bits: the (stage, k-step, pass)
+    pairs one tile each and persistent; MPS_C64_KERNEL is read once per process) gives the same bits: the (stage, k-step, pass)
     order is shared, so the automatic choice by tile count never makes results depend on n."""
     import os
     import subprocess
@@ -636,7 +636,7 @@ def test_c64_kernel_variants_bit_identical():
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sums = {}
-    for v in ("p128", "p256", "mc256", "cg2"):
+    for v in ("p128", "p256", "mc256", "cg2", "cg2p"):
         r = subprocess.run([sys.executable, "-c", _C64_VARIANT_SCRIPT, root], capture_output=True, text=True,
                            timeout=300, env=dict(os.environ, MPS_C64_KERNEL=v))
         assert r.returncode == 0, r.stderr[-2000:]
