@@ -748,6 +748,8 @@ def main():
     L2_BYTES = 126e6
     site_bytes = sum(a * b for a, b in zip(dims[:-1], dims[1:])) * D * (8 if args.dtype == "c64" else 16)
     l2_mode, n_rep = args.l2, 1
+    if ONE_GPU and l2_mode == "auto":  # plumbing check with every rank on cuda:0: its timing means nothing
+        l2_mode = "warm"
     if l2_mode == "auto":
         if site_bytes >= L2_BYTES or args.stream_sites:
             l2_mode = "large"

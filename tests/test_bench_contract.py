@@ -2,18 +2,18 @@
 its N>1 sample-sharded code path on a B200 (pytest -m gpu)."""
 
 import json
-import subprocess
 import sys
 from pathlib import Path
 
 import pytest
+from _proc import run_group
 
 ROOT = Path(__file__).resolve().parents[1]
 
 
 def test_reference_arm_json_line():
-    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--config", "c1",
-                          "--steps", "1", "--warmup", "3"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    out = run_group([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--config", "c1",
+                          "--steps", "1", "--warmup", "3"], timeout=600, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1
@@ -32,8 +32,8 @@ def test_gpus_flag_must_match_world_size():
     import os
 
     env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
-    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--config", "c1", "--steps", "1"],
-                         capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    out = run_group([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--config", "c1", "--steps", "1"],
+                         timeout=600, cwd=ROOT, env=env)
     assert out.returncode != 0 and "WORLD_SIZE=1" in out.stderr
 
 
@@ -42,20 +42,21 @@ def test_gpu_arm_fails_loudly_without_gpu():
 
     if torch.cuda.is_available():
         return
-    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--config", "c1", "--steps", "1"],
-                         capture_output=True, text=True, timeout=600, cwd=ROOT)
+    out = run_group([sys.executable, str(ROOT / "bench.py"), "--config", "c1", "--steps", "1"],
+                         timeout=600, cwd=ROOT)
     assert out.returncode != 0  # no CPU fallback for the product path
 
 
 @pytest.mark.gpu
+@pytest.mark.timeout(1500)  # above the sum of the subprocess timeouts, so a stuck child is killed by them
 def test_gpu_arm_json_line_and_two_rank_path():
     """One GPU arm line at N=1 (c2), then the N>1 sample-sharded code path under torchrun with
     two ranks sharing cuda:0 over gloo (MPS_BENCH_ONE_GPU plumbing mode: keys, max-over-ranks,
     whole-job value; the timing of that run means nothing)."""
     import os
 
-    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--config", "c2", "--steps", "2", "--warmup", "3",
-                          "--no-cpu-baseline"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    out = run_group([sys.executable, str(ROOT / "bench.py"), "--config", "c2", "--steps", "2", "--warmup", "3",
+                          "--no-cpu-baseline"], timeout=420, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-2000:]
     d = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
@@ -65,9 +66,9 @@ def test_gpu_arm_json_line_and_two_rank_path():
     assert d["roofline"]["bound"] == "tensor" and d["roofline"]["frac"] > 0
     env = dict(os.environ, MPS_BENCH_BACKEND="gloo", MPS_BENCH_ONE_GPU="1")
     # the bare driver command: `bench.py --gpus 2` re-executes itself under torchrun (2 ranks)
-    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--config", "c2", "--steps", "2",
+    out = run_group([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--config", "c2", "--steps", "2",
                           "--warmup", "3", "--no-cpu-baseline"],
-                         capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+                         timeout=600, cwd=ROOT, env=env)
     assert out.returncode == 0, out.stderr[-3000:]
     assert "re-executing under torchrun" in out.stderr and "process group up: world=2" in out.stderr
     lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
@@ -76,8 +77,8 @@ def test_gpu_arm_json_line_and_two_rank_path():
     assert d2["n_gpus"] == 2 and d2["scaling"] == "weak" and d2["value"] > 0 and d2["valid_outputs"]
     assert [r["rank"] for r in d2["ranks"]] == [0, 1] and "ranks" not in d2["config"]
     # torchrun with a world size that contradicts --gpus fails loudly
-    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+    out = run_group([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                           "--master-addr", "127.0.0.1", "--master-port", "29547", str(ROOT / "bench.py"), "--gpus", "3",
                           "--config", "c2", "--steps", "2", "--no-cpu-baseline"],
-                         capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+                         timeout=300, cwd=ROOT, env=env)
     assert out.returncode != 0

@@ -35,6 +35,7 @@ from paper_2511_14923_b200 import (  # noqa: E402
 from paper_2511_14923_b200 import _native  # noqa: E402
 
 from _parity import P_FLOOR, REL_TOL_C64, REL_TOL_C128, marginal_errors  # noqa: E402
+from _proc import run_group  # noqa: E402
 
 MARG_TOL = 1e-10
 
@@ -631,14 +632,13 @@ def test_c64_kernel_variants_bit_identical():
     pairs one tile each and persistent; MPS_C64_KERNEL is read once per process) gives the same bits: the (stage, k-step, pass)
     order is shared, so the automatic choice by tile count never makes results depend on n."""
     import os
-    import subprocess
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sums = {}
     for v in ("p128", "p256", "mc256", "cg2", "cg2p"):
-        r = subprocess.run([sys.executable, "-c", _C64_VARIANT_SCRIPT, root], capture_output=True, text=True,
-                           timeout=300, env=dict(os.environ, MPS_C64_KERNEL=v))
+        r = run_group([sys.executable, "-c", _C64_VARIANT_SCRIPT, root], timeout=300,
+                      env=dict(os.environ, MPS_C64_KERNEL=v))
         assert r.returncode == 0, r.stderr[-2000:]
         sums[v] = r.stdout.split()
     assert len({tuple(x) for x in sums.values()}) == 1, sums
@@ -899,16 +899,15 @@ def test_sample_sharded_two_ranks_equals_one(tmp_path, c2_sites):
     pkg/tests/test_sampler.py:272-277): two ranks (both on cuda:0, host plumbing over gloo) each
     sample their contiguous index block, and rank 0's gathered counts equal single-process sampling."""
     import os
-    import subprocess
     import sys
 
     ref = batch_sample(MpsSamplerConfig(N=350, seed=4, alpha_sigma=0.5, batch_size=100), MPS(c2_sites))
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = tmp_path / "counts.npy"
-    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+    r = run_group([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                         "--master-addr", "127.0.0.1", "--master-port", "29563",
                         os.path.join(root, "tests", "_pipeline_worker.py"), "sharded", str(out)],
-                       capture_output=True, text=True, timeout=600, cwd=root)
+                       timeout=600, cwd=root)
     assert r.returncode == 0, r.stderr[-3000:]
     assert np.array_equal(np.load(out), ref.counts)
 
@@ -919,16 +918,15 @@ def test_pipelined_p2p_handoff_on_one_gpu(tmp_path, c2_sites):
     the consumer's CUDA-IPC buffer; interprocess events order the two) reproduces single-process
     batch_sample.  (The send/recv schedule is covered over gloo on the CPU in test_distributed.)"""
     import os
-    import subprocess
     import sys
 
     ref = batch_sample(MpsSamplerConfig(N=350, seed=4, alpha_sigma=0.5, batch_size=100), MPS(c2_sites))
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = tmp_path / "counts.npy"
-    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+    r = run_group([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                         "--master-addr", "127.0.0.1", "--master-port", "29561",
                         os.path.join(root, "tests", "_pipeline_worker.py"), "p2p", str(out)],
-                       capture_output=True, text=True, timeout=600, cwd=root)
+                       timeout=600, cwd=root)
     assert r.returncode == 0, r.stderr[-3000:]
     assert np.array_equal(np.load(out), ref.counts)
 
