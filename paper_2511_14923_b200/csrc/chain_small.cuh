@@ -425,19 +425,24 @@ __global__ void __launch_bounds__(SC_THREADS, 1) small_chain_kernel(const __grid
         sc_bar_compute();  // red[][] complete
         if (tid == 0) SC_STAMP(0, q, 5);
         if (warp == 0) {  // the draw (draw_row_warp, as displace_draw_kernel; u / forced k prefetched)
-          const RowDraw r = draw_row_warp(red, DRAW_THREADS / 32, p_s, D, st_s, A.forced != 0,
-                                          __shfl_sync(0xffffffffu, k_pref, 0), __shfl_sync(0xffffffffu, u_pref, 0),
-                                          A.tie_eps);
-          if (A.marg && lane < D) A.marg[crow * D + lane] = (r.k >= 0) ? p_s[lane] / r.Ptot : 0.0;
+          const RowDraw r = draw_row_warp<DT>(red, DRAW_THREADS / 32, p_s, D, st_s, A.forced != 0,
+                                              __shfl_sync(0xffffffffu, k_pref, 0), __shfl_sync(0xffffffffu, u_pref, 0),
+                                              A.tie_eps);
           if (lane == 0) {
             st_s = r.status;
+            k_s = r.k;
+            scale_s = r.scale;
+          }
+          __syncwarp();
+          named_bar_arrive(1, SC_COMPUTE);  // release pass 2; the bookkeeping stores are off its path
+          if (A.marg && lane < D) A.marg[crow * D + lane] = (r.k >= 0) ? r.p / r.Ptot : 0.0;
+          if (lane == 0) {
             A.status[b] = r.status;
             if (!A.forced) A.counts[crow] = r.k;
-            k_s = r.k;
-            scale_s = (r.k >= 0 && p_s[r.k] > 0.0) ? 1.0 / sqrt(p_s[r.k]) : 0.0;
           }
+        } else {
+          sc_bar_compute();
         }
-        sc_bar_compute();
         if (tid == 0) SC_STAMP(0, q, 6);
         const int ks = k_s;
         const double scale = scale_s;

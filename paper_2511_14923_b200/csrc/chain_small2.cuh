@@ -336,18 +336,23 @@ __global__ void __launch_bounds__(SC2_THREADS, 1) small_chain2_kernel(const __gr
         sc2_bar_draw();  // red[][] complete
         if (dw == 0) SC2_STAMP(2, q, 2);
         if (dw == 0) {  // the draw (draw_row_warp, as displace_draw_kernel)
-          const RowDraw r = draw_row_warp(red, DRAW_THREADS / 32, p_s, D, st_s, A.forced != 0,
-                                          __shfl_sync(0xffffffffu, kf, 0), __shfl_sync(0xffffffffu, u, 0), A.tie_eps);
-          if (A.marg && lane < D) A.marg[crow * D + lane] = (r.k >= 0) ? p_s[lane] / r.Ptot : 0.0;
+          const RowDraw r = draw_row_warp<DT>(red, DRAW_THREADS / 32, p_s, D, st_s, A.forced != 0,
+                                              __shfl_sync(0xffffffffu, kf, 0), __shfl_sync(0xffffffffu, u, 0), A.tie_eps);
+          if (lane == 0) {
+            k_s = r.k;
+            scale_s = r.scale;
+            st_s = r.status;
+          }
+          __syncwarp();
+          named_bar_arrive(3, SC2_DRAW);  // release pass 2; the bookkeeping stores are off its path
+          if (A.marg && lane < D) A.marg[crow * D + lane] = (r.k >= 0) ? r.p / r.Ptot : 0.0;
           if (lane == 0) {
             A.status[b] = r.status;
             if (!A.forced) A.counts[crow] = r.k;
-            k_s = r.k;
-            scale_s = (r.k >= 0 && p_s[r.k] > 0.0) ? 1.0 / sqrt(p_s[r.k]) : 0.0;
-            st_s = r.status;
           }
+        } else {
+          sc2_bar_draw();
         }
-        sc2_bar_draw();
         if (dw == 0) SC2_STAMP(2, q, 3);
         const int ks = k_s;
         const double scale = scale_s;

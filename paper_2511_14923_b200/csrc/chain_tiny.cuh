@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tiny_chain_kernel(const __grid_
       }
       __syncwarp();
       TC_STAMP(q, 5);
-      const RowDraw r = draw_row_warp(red + warp, 1, p_s[warp], D, st, A.forced != 0, kf, u, A.tie_eps);
+      const RowDraw r = draw_row_warp<DT>(red + warp, 1, p_s[warp], D, st, A.forced != 0, kf, u, A.tie_eps);
       if (lane == 0) {
         A.status[b] = r.status;
         if (!A.forced) A.counts[crow] = r.k;
@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tiny_chain_kernel(const __grid_
       st = r.status;
       TC_STAMP(q, 6);
       const int ks = r.k;
-      const double scale = (ks >= 0 && p_s[warp][ks] > 0.0) ? 1.0 / sqrt(p_s[warp][ks]) : 0.0;
+      const double scale = r.scale;
       for (int j = lane; j < jpad; j += 32) {  // pass 2: gather + renormalise
         double2 e = make_double2(0.0, 0.0);
         if (j < chi_r && ks >= 0) {
@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tiny_chain_kernel(const __grid_
         emit(j, e);
       }
       // the normalised marginals leave after v' (p_s is rewritten only by this warp's next draw)
-      if (A.marg && lane < D) A.marg[crow * D + lane] = (ks >= 0) ? p_s[warp][lane] / r.Ptot : 0.0;
+      if (A.marg && lane < D) A.marg[crow * D + lane] = (ks >= 0) ? r.p / r.Ptot : 0.0;
       TC_STAMP(q, 7);
     }
     __syncthreads();  // the group's last V / T reads are done before the next group overwrites them

@@ -256,29 +256,53 @@ __device__ __forceinline__ float2 disp_row_f(const float2* T, int D, int k, cons
 // and its own prefix run_k with the serial loop's sequence of adds and divides once; the count,
 // the min distance to a CDF boundary (fmin is exact) and the zero-probability walk-back
 // (while (k > 0 && !(p[k] > 0)) --k) become ballots.  Writes p_s[0..D); returns the outcome
-// (-1: failed), the updated status bits and Ptot in every lane.
+// (-1: failed), the updated status bits, Ptot and the renormalisation 1/sqrt(p(k)) in every lane,
+// and in lane k < D its own p(k).
+//
+// Latency (it sits on every chain's serial path, ~860 cycles at C1 in the round-2 form): the D-long
+// prefix loop is unrolled (DT) with its loads hoisted; the tie flag is one ballot (the minimum of
+// |cdf - u| over lanes < D - 1, or 1e300, is <= eps exactly when one of those terms is, or 1e300 is:
+// fmin is exact and drops NaNs like the ballot does) instead of five shuffle rounds; and every lane
+// k < D forms the candidate 1/sqrt(p(k)) while the CDF divides run, so the chosen one is a shuffle.
+// Same operations on the same operands: every result bit is unchanged.
 struct RowDraw {
   int k;
   uint8_t status;
   double Ptot;
+  double scale;  // (k >= 0 && p(k) > 0) ? 1 / sqrt(p(k)) : 0
+  double p;      // lane < D: p(lane)
 };
+template <int DT>
 __device__ inline RowDraw draw_row_warp(const double (*red)[DMAX], int nwarps, double* p_s, int D, uint8_t st0,
                                         bool forced, int k_forced, double u, double tie_eps) {
   const int lane = threadIdx.x & 31;
+  double sacc = 0.0;
   if (lane < D) {
-    double sacc = 0.0;
     for (int w = 0; w < nwarps; ++w) sacc += red[w][lane];
     p_s[lane] = sacc;
   }
+  // candidate renormalisation of outcome `lane` (independent of the CDF chain below)
+  const double sc = (lane < D && sacc > 0.0) ? 1.0 / sqrt(sacc) : 0.0;
   __syncwarp();
   double Ptot = 0.0, run = 0.0;
-  for (int k = 0; k < D; ++k) {
-    const double pv = p_s[k];
-    Ptot += pv;
-    if (k <= lane) run += pv;
+  if constexpr (DT > 0) {
+    double pv[DT];
+#pragma unroll
+    for (int k = 0; k < DT; ++k) pv[k] = p_s[k];
+#pragma unroll
+    for (int k = 0; k < DT; ++k) {
+      Ptot += pv[k];
+      if (k <= lane) run += pv[k];
+    }
+  } else {
+    for (int k = 0; k < D; ++k) {
+      const double pv = p_s[k];
+      Ptot += pv;
+      if (k <= lane) run += pv;
+    }
   }
-  RowDraw r{-1, st0, Ptot};
-  const unsigned pos = __ballot_sync(0xffffffffu, lane < D && p_s[lane] > 0.0);
+  RowDraw r{-1, st0, Ptot, 0.0, sacc};
+  const unsigned pos = __ballot_sync(0xffffffffu, lane < D && sacc > 0.0);
   if (!(Ptot > 0.0) || !isfinite(Ptot)) {
     r.status |= ST_FAILED;
   } else if (forced) {
@@ -290,14 +314,14 @@ __device__ inline RowDraw draw_row_warp(const double (*red)[DMAX], int nwarps, d
   } else {
     const double cdf = (lane == D - 1) ? 1.0 : run / Ptot;
     const int cnt = __popc(__ballot_sync(0xffffffffu, lane < D && cdf <= u));
-    double mind = (lane < D - 1) ? fabs(cdf - u) : 1e300;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mind = fmin(mind, __shfl_xor_sync(0xffffffffu, mind, o));
+    const bool near = __any_sync(0xffffffffu, lane < D - 1 && fabs(cdf - u) <= tie_eps) || 1e300 <= tie_eps;
     const int kc = cnt < D - 1 ? cnt : D - 1;
     const unsigned below = pos & ((2u << kc) - 1u);
     r.k = below ? 31 - __clz(below) : 0;
-    if (mind <= tie_eps) r.status |= ST_FLAGGED;
+    if (near) r.status |= ST_FLAGGED;
   }
+  r.scale = __shfl_sync(0xffffffffu, sc, r.k >= 0 ? r.k : 0);
+  if (r.k < 0) r.scale = 0.0;
   return r;
 }
 
@@ -476,17 +500,22 @@ __global__ void __launch_bounds__(DRAW_THREADS, C64 ? 8 : 4)
     const double u = A.forced ? 0.0
                      : A.u   ? A.u[ui]
                              : philox_double(numpy_key0(A.seed), gi / 64, (gi % 64) * (uint64_t)A.M + A.m);
-    const RowDraw r = draw_row_warp(red, DRAW_THREADS / 32, p_s, D, A.status[b], A.forced != 0,
-                                    A.forced ? A.counts[crow] : 0, u, A.tie_eps);
-    if (A.marg && lane < D) A.marg[crow * D + lane] = (r.k >= 0) ? p_s[lane] / r.Ptot : 0.0;
+    const RowDraw r = draw_row_warp<DT>(red, DRAW_THREADS / 32, p_s, D, A.status[b], A.forced != 0,
+                                        A.forced ? A.counts[crow] : 0, u, A.tie_eps);
+    if (lane == 0) {
+      k_s = r.k;
+      scale_s = r.scale;
+    }
+    __syncwarp();
+    named_bar_arrive(1, DRAW_THREADS);  // release pass 2; the bookkeeping stores below are off its path
+    if (A.marg && lane < D) A.marg[crow * D + lane] = (r.k >= 0) ? r.p / r.Ptot : 0.0;
     if (lane == 0) {
       A.status[b] = r.status;
       if (!A.forced) A.counts[crow] = r.k;
-      k_s = r.k;
-      scale_s = (r.k >= 0 && p_s[r.k] > 0.0) ? 1.0 / sqrt(p_s[r.k]) : 0.0;
     }
+  } else {
+    named_bar_sync(1, DRAW_THREADS);
   }
-  __syncthreads();
   const int ks = k_s;
   const double scale = scale_s;
 

@@ -112,6 +112,14 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
 // Programmatic dependent launch (sm_90+): a kernel launched with the programmatic-
 // serialization attribute may start while its predecessor drains; it must call
 // griddep_wait() before touching anything the predecessor writes or reads-then-we-write.
+// named CTA barrier: producers arrive (no wait), consumers sync; prior memory accesses of the
+// arriving threads are visible to the syncing ones once the barrier completes
+__device__ __forceinline__ void named_bar_arrive(int id, int nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch_dependents() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
