@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(SC_THREADS, 1) small_chain_kernel(const __grid
   __shared__ double red[DRAW_THREADS / 32][DMAX];
   __shared__ double p_s[DMAX];
   __shared__ int k_s;
-  __shared__ double scale_s;
+  __shared__ double pk_s;
   __shared__ uint8_t st_s;
 
   const DrawArgs& A = P.d;
@@ -413,14 +413,13 @@ __global__ void __launch_bounds__(SC_THREADS, 1) small_chain_kernel(const __grid
             }
           }
           if (tid == 0) SC_STAMP(0, q, 4);
+          warp_tree_sum(acc);
+          if (lane == 0)
 #pragma unroll
-          for (int k = 0; k < DR; ++k) {
-            if (!DT && k >= D) break;
-            double v = acc[k];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            if (lane == 0) red[warp][k] = v;
-          }
+            for (int k = 0; k < DR; ++k) {
+              if (!DT && k >= D) break;
+              red[warp][k] = acc[k];
+            }
         }
         sc_bar_compute();  // red[][] complete
         if (tid == 0) SC_STAMP(0, q, 5);
@@ -431,7 +430,7 @@ __global__ void __launch_bounds__(SC_THREADS, 1) small_chain_kernel(const __grid
           if (lane == 0) {
             st_s = r.status;
             k_s = r.k;
-            scale_s = r.scale;
+            pk_s = r.pk;
           }
           __syncwarp();
           named_bar_arrive(1, SC_COMPUTE);  // release pass 2; the bookkeeping stores are off its path
@@ -445,7 +444,7 @@ __global__ void __launch_bounds__(SC_THREADS, 1) small_chain_kernel(const __grid
         }
         if (tid == 0) SC_STAMP(0, q, 6);
         const int ks = k_s;
-        const double scale = scale_s;
+        const double pk = pk_s;
         for (int j = tid; j < jpad; j += SC_COMPUTE) {
           double2 e = make_double2(0.0, 0.0);
           if (j < chi_r && ks >= 0) {
@@ -464,6 +463,7 @@ __global__ void __launch_bounds__(SC_THREADS, 1) small_chain_kernel(const __grid
                 e.y = fma(tk.y, c.x, e.y);
               }
             }
+            const double scale = row_scale(ks, pk);
             e = make_double2(e.x * scale, e.y * scale);
           }
           emit(j, e);

@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(SC2_THREADS, 1) small_chain2_kernel(const __gr
   __shared__ double red[DRAW_THREADS / 32][DMAX];
   __shared__ double p_s[DMAX];
   __shared__ int k_s;
-  __shared__ double scale_s;
+  __shared__ double pk_s;
   __shared__ uint8_t st_s;  // status of this CTA's row (the draw warps')
 
   const DrawArgs& A = P.d;
@@ -325,14 +325,13 @@ __global__ void __launch_bounds__(SC2_THREADS, 1) small_chain2_kernel(const __gr
             }
           }
         }
+        warp_tree_sum(acc);
+        if (lane == 0)
 #pragma unroll
-        for (int k = 0; k < DR; ++k) {
-          if (!DT && k >= D) break;
-          double v = acc[k];
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-          if (lane == 0) red[dw][k] = v;
-        }
+          for (int k = 0; k < DR; ++k) {
+            if (!DT && k >= D) break;
+            red[dw][k] = acc[k];
+          }
         sc2_bar_draw();  // red[][] complete
         if (dw == 0) SC2_STAMP(2, q, 2);
         if (dw == 0) {  // the draw (draw_row_warp, as displace_draw_kernel)
@@ -340,7 +339,7 @@ __global__ void __launch_bounds__(SC2_THREADS, 1) small_chain2_kernel(const __gr
                                               __shfl_sync(0xffffffffu, kf, 0), __shfl_sync(0xffffffffu, u, 0), A.tie_eps);
           if (lane == 0) {
             k_s = r.k;
-            scale_s = r.scale;
+            pk_s = r.pk;
             st_s = r.status;
           }
           __syncwarp();
@@ -355,7 +354,7 @@ __global__ void __launch_bounds__(SC2_THREADS, 1) small_chain2_kernel(const __gr
         }
         if (dw == 0) SC2_STAMP(2, q, 3);
         const int ks = k_s;
-        const double scale = scale_s;
+        const double pk = pk_s;
         for (int j = dt; j < jpad; j += SC2_DRAW) {
           double2 e = make_double2(0.0, 0.0);
           if (j < chi_r && ks >= 0) {
@@ -374,12 +373,13 @@ __global__ void __launch_bounds__(SC2_THREADS, 1) small_chain2_kernel(const __gr
                 e.y = fma(tk.y, c.x, e.y);
               }
             }
+            const double scale = row_scale(ks, pk);
             e = make_double2(e.x * scale, e.y * scale);
           }
           emit(j, e);
         }
       }
-      sc2_bar_draw();  // every draw thread is done with T, red, C and k_s / scale_s before reuse
+      sc2_bar_draw();  // every draw thread is done with T, red, C and k_s / pk_s before reuse
       if (dw == 0) SC2_STAMP(2, q, 4);
       if (dt == 0) mbar_arrive(&t_free[q & 1]);
       if (last && q + 1 < nsteps && dt < SC_CL) {

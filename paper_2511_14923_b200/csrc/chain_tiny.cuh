@@ -254,14 +254,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tiny_chain_kernel(const __grid_
           }
         }
       }
+      warp_tree_sum(acc);
+      if (lane == 0)
 #pragma unroll
-      for (int k = 0; k < DR; ++k) {
-        if (!DT && k >= D) break;
-        double v = acc[k];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) red[warp][k] = v;
-      }
+        for (int k = 0; k < DR; ++k) {
+          if (!DT && k >= D) break;
+          red[warp][k] = acc[k];
+        }
       __syncwarp();
       TC_STAMP(q, 5);
       const RowDraw r = draw_row_warp<DT>(red + warp, 1, p_s[warp], D, st, A.forced != 0, kf, u, A.tie_eps);
@@ -272,7 +271,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tiny_chain_kernel(const __grid_
       st = r.status;
       TC_STAMP(q, 6);
       const int ks = r.k;
-      const double scale = r.scale;
+
       for (int j = lane; j < jpad; j += 32) {  // pass 2: gather + renormalise
         double2 e = make_double2(0.0, 0.0);
         if (j < chi_r && ks >= 0) {
@@ -291,6 +290,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tiny_chain_kernel(const __grid_
               e.y = fma(tk.y, c.x, e.y);
             }
           }
+          const double scale = row_scale(ks, r.pk);
           e = make_double2(e.x * scale, e.y * scale);
         }
         emit(j, e);

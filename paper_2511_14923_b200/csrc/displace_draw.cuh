@@ -257,21 +257,37 @@ __device__ __forceinline__ float2 disp_row_f(const float2* T, int D, int k, cons
 // the min distance to a CDF boundary (fmin is exact) and the zero-probability walk-back
 // (while (k > 0 && !(p[k] > 0)) --k) become ballots.  Writes p_s[0..D); returns the outcome
 // (-1: failed), the updated status bits, Ptot and the renormalisation 1/sqrt(p(k)) in every lane,
-// and in lane k < D its own p(k).
+// p(k) in every lane, and in lane k < D its own p(k).
 //
 // Latency (it sits on every chain's serial path, ~860 cycles at C1 in the round-2 form): the D-long
 // prefix loop is unrolled (DT) with its loads hoisted; the tie flag is one ballot (the minimum of
 // |cdf - u| over lanes < D - 1, or 1e300, is <= eps exactly when one of those terms is, or 1e300 is:
-// fmin is exact and drops NaNs like the ballot does) instead of five shuffle rounds; and every lane
-// k < D forms the candidate 1/sqrt(p(k)) while the CDF divides run, so the chosen one is a shuffle.
-// Same operations on the same operands: every result bit is unchanged.
+// fmin is exact and drops NaNs like the ballot does) instead of five shuffle rounds; and the
+// renormalisation 1/sqrt(p(k)) is left to the caller's pass 2 (row_scale).  Same operations on the
+// same operands: every result bit is unchanged.
 struct RowDraw {
   int k;
   uint8_t status;
   double Ptot;
-  double scale;  // (k >= 0 && p(k) > 0) ? 1 / sqrt(p(k)) : 0
-  double p;      // lane < D: p(lane)
+  double pk;  // p(k) in every lane (0 when k < 0): the renormalisation is row_scale(k, pk)
+  double p;   // lane < D: p(lane)
 };
+// v' = E[:, k] / sqrt(p(k)) is formed as E * (1 / sqrt(p(k))) on every path.  Callers evaluate it
+// where it is used (after their pass-2 FMAs are issued), so its ~300-cycle sqrt + reciprocal chain
+// overlaps the gather instead of sitting between the draw and pass 2.
+__device__ __forceinline__ double row_scale(int k, double pk) { return (k >= 0 && pk > 0.0) ? 1.0 / sqrt(pk) : 0.0; }
+
+// The xor-shuffle tree sum of the draw's partial marginals over the 32 lanes, in place over the N
+// partials of one lane (rounds outermost: the N shuffle chains of a round are independent).  All
+// five rounds always run: skipping the rounds that only add the exact zeros of lanes past chi_r
+// (same bits) measured slower, the runtime branch between rounds costs more than the shuffles.
+template <int N, typename T>
+__device__ __forceinline__ void warp_tree_sum(T (&v)[N]) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int k = 0; k < N; ++k) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+}
 template <int DT>
 __device__ inline RowDraw draw_row_warp(const double (*red)[DMAX], int nwarps, double* p_s, int D, uint8_t st0,
                                         bool forced, int k_forced, double u, double tie_eps) {
@@ -281,8 +297,6 @@ __device__ inline RowDraw draw_row_warp(const double (*red)[DMAX], int nwarps, d
     for (int w = 0; w < nwarps; ++w) sacc += red[w][lane];
     p_s[lane] = sacc;
   }
-  // candidate renormalisation of outcome `lane` (independent of the CDF chain below)
-  const double sc = (lane < D && sacc > 0.0) ? 1.0 / sqrt(sacc) : 0.0;
   __syncwarp();
   double Ptot = 0.0, run = 0.0;
   if constexpr (DT > 0) {
@@ -320,8 +334,8 @@ __device__ inline RowDraw draw_row_warp(const double (*red)[DMAX], int nwarps, d
     r.k = below ? 31 - __clz(below) : 0;
     if (near) r.status |= ST_FLAGGED;
   }
-  r.scale = __shfl_sync(0xffffffffu, sc, r.k >= 0 ? r.k : 0);
-  if (r.k < 0) r.scale = 0.0;
+  r.pk = __shfl_sync(0xffffffffu, sacc, r.k >= 0 ? r.k : 0);
+  if (r.k < 0) r.pk = 0.0;
   return r;
 }
 
@@ -352,7 +366,7 @@ __global__ void __launch_bounds__(DRAW_THREADS, C64 ? 8 : 4)
   __shared__ double red[DRAW_THREADS / 32][DMAX];
   __shared__ double p_s[DMAX];
   __shared__ int k_s;
-  __shared__ double scale_s;
+  __shared__ double pk_s;
 
   const int b = blockIdx.x;
   const int tid = threadIdx.x;
@@ -486,14 +500,13 @@ __global__ void __launch_bounds__(DRAW_THREADS, C64 ? 8 : 4)
       }
     }
   }
+  warp_tree_sum(acc);
+  if (lane == 0)
 #pragma unroll
-  for (int k = 0; k < DR; ++k) {
-    if (!DT && k >= D) break;
-    AccT v = acc[k];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) red[warp][k] = (double)v;
-  }
+    for (int k = 0; k < DR; ++k) {
+      if (!DT && k >= D) break;
+      red[warp][k] = (double)acc[k];
+    }
   __syncthreads();
   if (warp == 0) {  // the draw, on warp 0 (draw_row_warp: the serial rule's exact operations)
     const long long ui = (long long)b * A.ld_u + A.m;
@@ -504,7 +517,7 @@ __global__ void __launch_bounds__(DRAW_THREADS, C64 ? 8 : 4)
                                         A.forced ? A.counts[crow] : 0, u, A.tie_eps);
     if (lane == 0) {
       k_s = r.k;
-      scale_s = r.scale;
+      pk_s = r.pk;
     }
     __syncwarp();
     named_bar_arrive(1, DRAW_THREADS);  // release pass 2; the bookkeeping stores below are off its path
@@ -517,7 +530,7 @@ __global__ void __launch_bounds__(DRAW_THREADS, C64 ? 8 : 4)
     named_bar_sync(1, DRAW_THREADS);
   }
   const int ks = k_s;
-  const double scale = scale_s;
+  const double scale = row_scale(ks, pk_s);
 
   // ---- pass 2: gather + renormalise ----
   for (int cidx = 0; cidx < nchunks; ++cidx) {

@@ -10,7 +10,8 @@ from oracle import mps_oracle as orc
 sites = orc.random_mps(16, 100, 10, seed=0)
 with MpsSampler(MPS(sites)) as eng:
     eng.set_small_chain(1)
-    cfg = MpsSamplerConfig(N=100, seed=0, alpha_sigma=0.5, batch_size=100)
+    import os
+    cfg = MpsSamplerConfig(N=100, seed=0, alpha_sigma=None if os.environ.get('TRACE_IDENT') else 0.5, batch_size=100)
     for _ in range(3):
         eng.sample(cfg)
     L = eng.L
