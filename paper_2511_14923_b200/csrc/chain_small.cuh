@@ -36,9 +36,11 @@ constexpr int SC_NMAX = 1024;                     // chi_r * D bound (complex co
 constexpr int SC_FMAX = SC_NMAX / 8 / SC_CL;      // 8-column fragments per CTA (8)
 constexpr int SC_FW = SC_FMAX / 8;                // per compute warp (1)
 #ifndef SC_KS_DEF  // tuning knob of tools/chain_trace.py
-#define SC_KS_DEF 2
+#define SC_KS_DEF 3
 #endif
-constexpr int SC_KS = SC_KS_DEF;                  // k stages (8 complex k each) per ring slot
+constexpr int SC_KS = SC_KS_DEF;                  // k stages (8 complex k each) per ring slot: one mbarrier
+                                                  // wait (a pipeline drain) per slot; 3 measured best at C2
+                                                  // (profiles/r02_small_chain_ring_sweep.txt)
 #ifndef SC_KSTAGES_DEF  // k stages of Gamma in flight (tuning knob)
 #define SC_KSTAGES_DEF 12
 #endif
