@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(SC_THREADS, 1) small_chain_kernel(const __grid
     const uint32_t cbar_addr = smem_u32(c_full), vbar_addr = smem_u32(v_full);
     for (int q = 0; q < nsteps; ++q) {
       const int m = P.m_begin + q % nmodes;
-      const int K = P.chi[m], chi_r = P.chi[m + 1], N = chi_r * D;
+      const int K = P.chi[m], chi_r = P.chi[m + 1];
       const int KT = (K + 7) >> 3, F = F_of(m);
       const int f0 = rank * F / SC_CL, fc = (rank + 1) * F / SC_CL - f0;
       const int b = row_of(q);
