@@ -262,6 +262,18 @@ int mps_stream_uniforms(uint64_t seed, int64_t first, int count, int M, double* 
 /* Debug builds only (-DSC_TRACE, tools/chain_trace.py): copy the small-chain kernel's clock64
  * stamps of CTA 0 (2 x 256 x 8 long long: producer / owner side, per mode) to out. */
 int mps_debug_chain_trace(long long* out);
+/* (-DSC_TRACE) the pipelined-halves kernel's stamps (4 x 256 x 8 long long), tools/chain2_trace.py */
+int mps_debug_chain2_trace(long long* out);
+#endif
+#ifdef TC_TRACE
+/* Debug builds only (-DTC_TRACE, tools/tiny_trace.py): the tiny-chain kernel's clock64 stamps of
+ * CTA 0, warp 0 (64 modes x 8 long long). */
+int mps_debug_tiny_trace(long long* out);
+#endif
+#ifdef DRAW_TRACE
+/* Debug builds only (-DDRAW_TRACE, tools/draw_trace.py): m >= 0 arms the per-CTA globaltimer trace
+ * of the draw kernel for mode m; m < 0 copies it (8192 CTAs x 8 long long: 6 phase stamps, -, smid). */
+int mps_debug_draw_trace(int m, long long* out);
 #endif
 
 #ifdef __cplusplus

@@ -345,6 +345,27 @@ __device__ inline RowDraw draw_row_warp(const double (*red)[DMAX], int nwarps, d
 // the reduction order (and every result bit) is the same with and without the ring.
 // ring slots of the draw kernel's C-row stream (a CTA keeps RING_SLOTS - 1 chunk loads in flight
 // while it works on one); the c64 chunks are half the bytes, so it affords a deeper ring
+#ifdef DRAW_TRACE  // debug build only (tools/draw_trace.py): per-CTA globaltimer stamps of one mode's launch
+__device__ int dr_trace_m = -1;
+__device__ long long dr_trace[8192][8];
+__device__ __forceinline__ long long dr_now() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define DR_STAMP(k)                                                          \
+  if (A.m == dr_trace_m && threadIdx.x == 0 && blockIdx.x < 8192) {         \
+    dr_trace[blockIdx.x][k] = dr_now();                                      \
+    if ((k) == 0) {                                                          \
+      unsigned smid;                                                         \
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));                      \
+      dr_trace[blockIdx.x][7] = smid;                                        \
+    }                                                                        \
+  }
+#else
+#define DR_STAMP(k)
+#endif
+
 #ifndef DRAW_SLOTS_C128
 #define DRAW_SLOTS_C128 2
 #endif
@@ -399,6 +420,7 @@ __global__ void __launch_bounds__(DRAW_THREADS, C64 ? 8 : 4)
 
   // ---- displacement matrix for (b, m): inputs only, so it runs before the PDL wait and
   //      overlaps the tail of the site GEMM that produces C ----
+  DR_STAMP(0);
   griddep_launch_dependents();
   if (RING && tid == 0) {
     for (int i = 0; i < NS; ++i) mbar_init(&ring_bar[i], 1);
@@ -421,7 +443,9 @@ __global__ void __launch_bounds__(DRAW_THREADS, C64 ? 8 : 4)
     __syncthreads();
     for (int e = tid; e < D * D; e += DRAW_THREADS) Tf[e] = make_float2((float)T[e].x, (float)T[e].y);
   }
+  DR_STAMP(1);
   griddep_wait();  // the GEMM (and transitively the previous draw) is complete: C, status valid
+  DR_STAMP(2);
   const bool dead = (A.status[b] & ST_FAILED) != 0;
   // with one chunk the row stays in slot 0 for pass 2 (no re-load); else loads 0 and 1 go out now
   if (RING && tid == 0 && !dead) {
@@ -508,6 +532,7 @@ __global__ void __launch_bounds__(DRAW_THREADS, C64 ? 8 : 4)
       red[warp][k] = (double)acc[k];
     }
   __syncthreads();
+  DR_STAMP(3);
   if (warp == 0) {  // the draw, on warp 0 (draw_row_warp: the serial rule's exact operations)
     const long long ui = (long long)b * A.ld_u + A.m;
     const double u = A.forced ? 0.0
@@ -531,6 +556,7 @@ __global__ void __launch_bounds__(DRAW_THREADS, C64 ? 8 : 4)
   }
   const int ks = k_s;
   const double scale = row_scale(ks, pk_s);
+  DR_STAMP(4);
 
   // ---- pass 2: gather + renormalise ----
   for (int cidx = 0; cidx < nchunks; ++cidx) {
@@ -582,6 +608,7 @@ __global__ void __launch_bounds__(DRAW_THREADS, C64 ? 8 : 4)
       }
     }
   }
+  DR_STAMP(5);
 }
 
 // chi = 1 complex64 starting state as tf32 planes (row pitch 4 floats): (1, 0, 0, 0) / zeros

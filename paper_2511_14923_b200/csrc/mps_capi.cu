@@ -2140,6 +2140,12 @@ int mps_debug_tiny_trace(long long* out) {
   return cudaMemcpyFromSymbol(out, tc_trace, sizeof(tc_trace)) == cudaSuccess ? MPS_OK : MPS_ERR_GENERIC;
 }
 #endif
+#ifdef DRAW_TRACE
+int mps_debug_draw_trace(int m, long long* out) {  // m >= 0: arm the trace for mode m; m < 0: read it
+  if (m >= 0) return cudaMemcpyToSymbol(dr_trace_m, &m, sizeof(int)) == cudaSuccess ? MPS_OK : MPS_ERR_GENERIC;
+  return cudaMemcpyFromSymbol(out, dr_trace, sizeof(dr_trace)) == cudaSuccess ? MPS_OK : MPS_ERR_GENERIC;
+}
+#endif
 #ifdef SC_TRACE
 int mps_debug_chain_trace(long long* out) {
   return cudaMemcpyFromSymbol(out, sc_trace, sizeof(sc_trace)) == cudaSuccess ? MPS_OK : MPS_ERR_GENERIC;

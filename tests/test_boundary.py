@@ -31,7 +31,7 @@ ROOT = Path(__file__).resolve().parents[1]
 def _header_symbols():
     text = (ROOT / "include" / "mps_sampler.h").read_text()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    text = re.sub(r"#ifdef SC_TRACE.*?#endif", "", text, flags=re.S)  # debug-build-only entry points
+    text = re.sub(r"#ifdef [A-Z_]*TRACE.*?#endif", "", text, flags=re.S)  # debug-build-only entry points
     return sorted(set(re.findall(r"\b(mps_[a-z_0-9]+)\s*\(", text)))
 
 
