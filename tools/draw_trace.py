@@ -2,7 +2,7 @@
 
 Build:  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -shared -Xcompiler -fPIC -I include \
             -DDRAW_TRACE -o /tmp/lib_drtrace.so paper_2511_14923_b200/csrc/mps_capi.cu -lcuda
-Run:    MPS_LIB=/tmp/lib_drtrace.so python tools/draw_trace.py
+Run:    MPS_LIB=/tmp/lib_drtrace.so python tools/draw_trace.py [mode] [c64]
 Stamps (globaltimer, ns) per CTA: 0 entry, 1 D(alpha) built, 2 after griddepcontrol.wait, 3 pass 1 done
 (partials reduced), 4 draw published, 5 exit; plus the SM id.  One lane (so the launch is not overlapped
 by another lane's GEMM), n = 1024."""
@@ -12,7 +12,10 @@ from paper_2511_14923_b200 import MPS, MpsSampler
 from bench import CONFIGS
 M, chi, D, n, sigma, _, _ = CONFIGS["c3"]
 mode = int(sys.argv[1]) if len(sys.argv) > 1 else 30
+c64 = len(sys.argv) > 2 and sys.argv[2] == "c64"
 mps = MPS.random(M, chi, D, seed=0, device="cuda")
+if c64:
+    mps = mps.astype("complex64")
 with MpsSampler(mps) as eng:
     eng.set_lanes(1)
     eng.set_streams(0, sigma)
@@ -32,7 +35,7 @@ a = buf[:n].astype(np.float64)
 t0 = a[:, 0].min()
 rel = (a[:, :6] - t0) / 1e3  # us
 dur = np.diff(a[:, :6], axis=1) / 1e3
-print(f"draw kernel, C3 mode {mode}, n={n}: launch span {rel[:, 5].max():.1f} us (first entry -> last exit)")
+print(f"draw kernel ({'complex64' if c64 else 'complex128'}), C3 mode {mode}, n={n}: launch span {rel[:, 5].max():.1f} us (first entry -> last exit)")
 print("phase means (us): D(alpha) %.2f | PDL wait %.2f | pass 1 %.2f | draw %.2f | pass 2 %.2f" % tuple(dur.mean(0)))
 print("phase max   (us): D(alpha) %.2f | PDL wait %.2f | pass 1 %.2f | draw %.2f | pass 2 %.2f" % tuple(dur.max(0)))
 print("CTA lifetime mean %.2f us, max %.2f" % ((a[:, 5] - a[:, 0]).mean() / 1e3, (a[:, 5] - a[:, 0]).max() / 1e3))
