@@ -446,6 +446,9 @@ __global__ void __launch_bounds__(DRAW_THREADS, C64 ? 8 : 4)
   DR_STAMP(1);
   griddep_wait();  // the GEMM (and transitively the previous draw) is complete: C, status valid
   DR_STAMP(2);
+#ifdef DRAW_NOOP  // timing experiment only (wrong results): the chain with the draw's work removed
+  return;
+#endif
   const bool dead = (A.status[b] & ST_FAILED) != 0;
   // with one chunk the row stays in slot 0 for pass 2 (no re-load); else loads 0 and 1 go out now
   if (RING && tid == 0 && !dead) {
