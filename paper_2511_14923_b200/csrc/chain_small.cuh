@@ -415,13 +415,7 @@ __global__ void __launch_bounds__(SC_THREADS, 1) small_chain_kernel(const __grid
             }
           }
           if (tid == 0) SC_STAMP(0, q, 4);
-          warp_tree_sum(acc);
-          if (lane == 0)
-#pragma unroll
-            for (int k = 0; k < DR; ++k) {
-              if (!DT && k >= D) break;
-              red[warp][k] = acc[k];
-            }
+          warp_tree_scatter(acc, red[warp], D);
         }
         sc_bar_compute();  // red[][] complete
         if (tid == 0) SC_STAMP(0, q, 5);

@@ -325,13 +325,7 @@ __global__ void __launch_bounds__(SC2_THREADS, 1) small_chain2_kernel(const __gr
             }
           }
         }
-        warp_tree_sum(acc);
-        if (lane == 0)
-#pragma unroll
-          for (int k = 0; k < DR; ++k) {
-            if (!DT && k >= D) break;
-            red[dw][k] = acc[k];
-          }
+        warp_tree_scatter(acc, red[dw], D);
         sc2_bar_draw();  // red[][] complete
         if (dw == 0) SC2_STAMP(2, q, 2);
         if (dw == 0) {  // the draw (draw_row_warp, as displace_draw_kernel)

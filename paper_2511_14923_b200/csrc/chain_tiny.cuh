@@ -254,13 +254,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tiny_chain_kernel(const __grid_
           }
         }
       }
-      warp_tree_sum(acc);
-      if (lane == 0)
-#pragma unroll
-        for (int k = 0; k < DR; ++k) {
-          if (!DT && k >= D) break;
-          red[warp][k] = acc[k];
-        }
+      warp_tree_scatter(acc, red[warp], D);
       __syncwarp();
       TC_STAMP(q, 5);
       const RowDraw r = draw_row_warp<DT>(red + warp, 1, p_s[warp], D, st, A.forced != 0, kf, u, A.tie_eps);

@@ -277,16 +277,48 @@ struct RowDraw {
 // overlaps the gather instead of sitting between the draw and pass 2.
 __device__ __forceinline__ double row_scale(int k, double pk) { return (k >= 0 && pk > 0.0) ? 1.0 / sqrt(pk) : 0.0; }
 
-// The xor-shuffle tree sum of the draw's partial marginals over the 32 lanes, in place over the N
-// partials of one lane (rounds outermost: the N shuffle chains of a round are independent).  All
-// five rounds always run: skipping the rounds that only add the exact zeros of lanes past chi_r
-// (same bits) measured slower, the runtime branch between rounds costs more than the shuffles.
-template <int N, typename T>
-__device__ __forceinline__ void warp_tree_sum(T (&v)[N]) {
+// The draw's partial marginals summed over the 32 lanes with the xor-shuffle butterfly's association
+// (rounds 16, 8, 4, 2, 1 -- the fixed order every path shares), done as a reduce-scatter.  The N partials are padded to NP = 2^ceil(log2 N) (zeros for
+// k >= N).  At round o the lanes i and i ^ o hold the same NP / (32 / o)-long set (their higher lane
+// bits agree); the lower lane keeps the first half, the upper the second, each sends the half it drops
+// and adds the partner's copy of the half it keeps.  Every kept value is own + partner of exactly the
+// butterfly's pairs (addition commutes), so the totals carry the butterfly's bits, but a round moves
+// half the set instead of all of it (N = 10: 16 shuffles instead of 50; N = 4: 6 instead of 20).  Once a
+// set is one value the lower lane keeps the sum and the upper drops out.  Afterwards lane L holds the
+// total of k = base (when alive); it writes out[k] for k < nvalid.  All indices are compile-time.
+template <int N, typename T, typename O>
+__device__ __forceinline__ void warp_tree_scatter(const T (&in)[N], O* out, int nvalid) {
+  constexpr int NP = N <= 1 ? 1 : N <= 2 ? 2 : N <= 4 ? 4 : N <= 8 ? 8 : 16;
+  static_assert(N <= 16, "at most 16 partials");
+  const int lane = threadIdx.x & 31;
+  T v[NP];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1)
+  for (int k = 0; k < NP; ++k) v[k] = k < N ? in[k] : T(0);
+  int base = 0;
+  bool alive = true;
 #pragma unroll
-    for (int k = 0; k < N; ++k) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+  for (int r = 0; r < 5; ++r) {
+    const int o = 16 >> r;
+    const bool up = (lane & o) != 0;
+    const int CM = NP >> r;  // compile-time after unrolling (0 once the set is a single value)
+    if (CM >= 2) {
+      const int H = CM / 2;
+#pragma unroll
+      for (int t = 0; t < NP / 2; ++t) {
+        if (t < H) {
+          const T x = up ? v[t] : v[H + t];
+          const T y = __shfl_xor_sync(0xffffffffu, x, o);
+          v[t] = (up ? v[H + t] : v[t]) + y;
+        }
+      }
+      if (up) base += H;
+    } else {
+      const T y = __shfl_xor_sync(0xffffffffu, v[0], o);
+      v[0] = v[0] + y;
+      alive = alive && !up;
+    }
+  }
+  if (alive && base < nvalid) out[base] = (O)v[0];
 }
 template <int DT>
 __device__ inline RowDraw draw_row_warp(const double (*red)[DMAX], int nwarps, double* p_s, int D, uint8_t st0,
@@ -527,13 +559,7 @@ __global__ void __launch_bounds__(DRAW_THREADS, C64 ? 8 : 4)
       }
     }
   }
-  warp_tree_sum(acc);
-  if (lane == 0)
-#pragma unroll
-    for (int k = 0; k < DR; ++k) {
-      if (!DT && k >= D) break;
-      red[warp][k] = (double)acc[k];
-    }
+  warp_tree_scatter(acc, red[warp], D);
   __syncthreads();
   DR_STAMP(3);
   if (warp == 0) {  // the draw, on warp 0 (draw_row_warp: the serial rule's exact operations)
