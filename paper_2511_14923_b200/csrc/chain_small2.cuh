@@ -264,6 +264,7 @@ __global__ void __launch_bounds__(SC2_THREADS, 1) small_chain2_kernel(const __gr
       if (dt == 0 && q + 1 < nsteps) mbar_arrive_expect_tx(&c_full[(q + 1) & 1], (uint32_t)F_of(P.m_begin + (q + 1) % nmodes) * 128u);
       mbar_wait(&t_full[q & 1], (q >> 1) & 1);
       sc2_bar_draw();  // st_s of a group's first mode visible to every draw thread
+      if (dw == 0) SC2_STAMP(2, q, 5);
       const double2* Crow = reinterpret_cast<const double2*>(smem + SC_OFF_C) + (q & 1) * SC_NMAX;
       const double2* T = reinterpret_cast<const double2*>(smem + SC_OFF_T) + (q & 1) * DMAX * DMAX;
       const int jpad = (chi_r + 7) & ~7;

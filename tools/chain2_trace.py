@@ -23,5 +23,5 @@ for q in range(16):
     k1a, k1b, d_a, d_b = buf[0, q], buf[1, q], buf[2, q], buf[3, q]
     f = lambda x: x - t0
     print(f"mode {q:2d}: K1(cta0) A wait {f(k1a[0]):7d} start {f(k1a[1]):7d} end {f(k1a[2]):7d} | B wait {f(k1a[4]):7d} start {f(k1a[5]):7d} end {f(k1a[6]):7d}"
-          f" || drawA(cta0) cwait {f(d_a[0]):7d} cdone {f(d_a[1]):7d} p1 {f(d_a[2]):7d} draw {f(d_a[3]):7d} end {f(d_a[4]):7d}"
+          f" || drawA(cta0) cwait {f(d_a[0]):7d} cdone {f(d_a[1]):7d} T {f(d_a[5]):7d} p1 {f(d_a[2]):7d} draw {f(d_a[3]):7d} end {f(d_a[4]):7d}"
           f" || drawB(cta8) cdone {f(d_b[1]):7d} end {f(d_b[4]):7d}")
