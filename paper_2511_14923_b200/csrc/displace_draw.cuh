@@ -96,13 +96,18 @@ __device__ inline double2 stream_alpha(uint64_t seed, unsigned long long i, int 
 __constant__ double c_sqrt[17] = {0.0, 1.0, 1.4142135623730951, 1.7320508075688772, 2.0, 2.23606797749979, 2.449489742783178, 2.6457513110645907, 2.8284271247461903, 3.0, 3.1622776601683795, 3.3166247903554, 3.4641016151377544, 3.605551275463989, 3.7416573867739413, 3.872983346207417, 4.0};
 __constant__ double c_rsqrt[17] = {0.0, 1.0, 0.7071067811865475, 0.5773502691896258, 0.5, 0.4472135954999579, 0.4082482904638631, 0.3779644730092272, 0.35355339059327373, 0.3333333333333333, 0.31622776601683794, 0.30151134457776363, 0.2886751345948129, 0.2773500981126146, 0.2672612419124244, 0.2581988897471611, 0.25};
 
-// Exact truncated <k|D(alpha)|d> (oracle decision 6), row-major T[k*D + d].  The
-// operation order mirrors the oracle's numpy expressions with explicit _rn
-// intrinsics (no FMA contraction), so host and device agree to the last bit except
-// where exp() differs by an ulp.
-__device__ __forceinline__ double2 cmul_rn(double2 a, double2 b) {  // numpy complex multiply
-  return make_double2(__dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)),
-                      __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x)));
+// Exact truncated <k|D(alpha)|d> (oracle decision 6), row-major T[k*D + d].  The operation order
+// mirrors the oracle's numpy expressions with explicit _rn intrinsics, so host and device agree to
+// the last bit except where exp() differs by an ulp (a common factor of the whole matrix).
+// cmul_rn is numpy's complex multiply a * b as its SIMD loops form it (numpy 2.x on FMA3 / AVX-512
+// hosts: one fmaddsub of a.re * (b.re, b.im) against a.im * (b.im, b.re)), checked bit for bit
+// against numpy 2.3 on random contiguous and strided pairs.  With it, a CPU emulation of the
+// recurrence below reproduces oracle.displacement_matrix exactly when given numpy's exp()
+// (tools/displacement_emulation.py, profiles/r02_conditioning.txt).  The plain two-rounding form
+// disagreed with numpy on about half of the products.  At D = 16 and |alpha| ~ 2.4 the recurrence
+// amplified that to ~1e-12 in D(alpha).
+__device__ __forceinline__ double2 cmul_rn(double2 a, double2 b) {
+  return make_double2(__fma_rn(a.x, b.x, -__dmul_rn(a.y, b.y)), __fma_rn(a.x, b.y, __dmul_rn(a.y, b.x)));
 }
 
 __device__ inline void displacement_column0(double2 a, int D, double2* T) {

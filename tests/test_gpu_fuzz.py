@@ -169,3 +169,44 @@ def test_random_knobs_bit_identical(case):
     other = _run_knobs(sites, c, c["knobs"])
     for a, b, name in zip(plain, other, ("counts", "marginals", "status")):
         assert np.array_equal(a, b), (name, c)
+
+
+# Large ragged chains (tools/fuzz_large.py runs the seeded sweep of these, profiles/r02_fuzz_large.txt):
+# bond dimensions that are not multiples of any tile edge, up to chi = 1333, sample counts just past
+# the 64-row K1 tiles and the 1024-row lane split, every complex128 K1 product.
+_LARGE = [
+    dict(dims=[1, 10, 100, 887, 1333, 1000, 100, 10, 1], D=10, N=1025, gemm=3, lanes=2, micro=0, sigma=0.5),
+    dict(dims=[1, 7, 49, 343, 777, 343, 49, 7, 1], D=7, N=257, gemm=4, lanes=3, micro=200, sigma=0.9),
+    dict(dims=[1, 16, 202, 1100, 256, 16, 1], D=16, N=65, gemm=8, lanes=1, micro=0, sigma=0.0),
+]
+
+
+@pytest.mark.parametrize("case", _LARGE, ids=lambda c: "chi{}-D{D}-N{N}-g{gemm}".format(max(c["dims"]), **c))
+def test_large_ragged_chain_vs_oracle(case):
+    from paper_2511_14923_b200.mps import device_site
+
+    c = case
+    dims, D, N = c["dims"], c["D"], c["N"]
+    M = len(dims) - 1
+    sites = [device_site(11, m, dims[m], dims[m + 1], D) for m in range(M)]
+    sigma = c["sigma"] or None
+    u = stream_uniforms(11, 5000, N, M)
+    al = alpha_stream(11, 5000, N, M, sigma) if sigma else None
+    counts = np.zeros((N, M), dtype=np.int32)
+    status = np.zeros(N, dtype=np.uint8)
+    marg = np.zeros((N, M, D))
+    with MpsSampler(MPS(sites)) as eng:
+        eng.set_gemm_mode(c["gemm"])
+        eng.set_lanes(c["lanes"])
+        eng.set_micro_batch(c["micro"])
+        eng.set_streams(11, sigma)
+        eng.run(5000, N, counts, marginals=marg, status=status)
+    assert not (status & _native.MPS_STATUS_FAILED).any()
+    host = [G.cpu().numpy() for G in sites]
+    ref = orc.sample_chain(host, u, alpha=al, forced=counts, return_marginals=True)
+    ab, rel, _ = marginal_errors(marg, ref["marginals"])
+    assert ab <= 1e-10 and rel <= REL_TOL_C128, (ab, rel)
+    free = orc.sample_chain(host, u, alpha=al)
+    flagged = (status & _native.MPS_STATUS_FLAGGED) != 0
+    mism = (counts != free["counts"]).any(axis=1) & ~flagged & ~free["flagged"]
+    assert not mism.any(), int(mism.sum())

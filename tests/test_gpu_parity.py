@@ -104,9 +104,12 @@ def test_displacement_kernel_vs_oracle():
         out = torch.empty(len(a), D, D, dtype=torch.complex128, device="cuda")
         assert L.mps_displacement(_c(a).data_ptr(), len(a), D, out.data_ptr(), 0) == 0
         torch.cuda.synchronize()
-        # same operation order as the oracle; residual differences are exp() ulps and
-
-        assert np.abs(out.cpu().numpy() - orc.displacement_matrix(a, D)).max() < 1e-11
+        # same operation order and complex-multiply rounding as the oracle's numpy (cmul_rn): with
+        # numpy's own exp() a CPU emulation of the device recurrence is bit-identical to the oracle
+        # (profiles/r02_conditioning.txt); the residual is exp()'s last bit, a common factor of the
+        # whole matrix that cancels in the normalised marginals and the renormalised state
+        ref = orc.displacement_matrix(a, D)
+        assert np.abs(out.cpu().numpy() - ref).max() <= 1e-13 * max(1.0, np.abs(ref).max()), D
 
 
 # numpy routes key lists holding ints >= 2^63 through float64 (2^64 - 1 casts with a RuntimeWarning);
